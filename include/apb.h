@@ -1,0 +1,167 @@
+/*
+ * apb.h — C ABI of libapb, the B200 (sm_100a) implementation of APB's per-layer
+ * sequence-parallel prefill hot path (arXiv 2502.12085, "APB: Accelerating Distributed
+ * Long-Context Inference by Passing Compressed Context Blocks across GPUs").
+ *
+ * Citations are PAPER.md line numbers of the paper's LaTeX source (P:<line>) plus the
+ * algorithm / equation label.  Readings of points the paper leaves open (G1..G16) are
+ * listed in DESIGN.md.
+ *
+ * Per layer, on every host h = host + 1 (one host = one GPU in deployment; several hosts
+ * may be emulated on one GPU), Alg. apb_prefill runs four steps:
+ *   1. apb_retain_score      s = R([Q_h, K_h, V_h])
+ *   2. apb_select_topk       idx = ArgTop-l_p(s); K^C, V^C = K_h[idx], V_h[idx]
+ *   3. apb_exchange_passing  AllGather(K^C_h, V^C_h)
+ *   4. apb_attention_fwd     Attention([Q_a,Q_h], [K_a,K_p,K_h], [V_a,V_p,V_h])  (eq:apb)
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Tensors are caller-owned DEVICE memory (e.g. torch tensors).  libapb never allocates,
+ *    frees or retains them beyond the call's stream work.  Workspace is caller-provided;
+ *    query its size with apb_workspace_size().
+ *  - bf16 tensors are passed as `const void*` of 16-bit IEEE bfloat16 values.
+ *  - Host-local rows: L_A = (host == 0) ? 0 : l_q + l_a anchor rows, then
+ *    l_b = n / H block rows.  Q is [L_A + l_b][n_heads][head_dim] with a row stride of
+ *    q_row_stride ELEMENTS (>= n_heads*head_dim, multiple of 8); K and V are
+ *    [L_A + l_b][n_kv_heads][head_dim] with row stride kv_row_stride.  head_dim is
+ *    contiguous; heads are head_dim apart.
+ *  - l_p' = min(l_p, l_b) (reading G6).  P_h = host * l_p' passing keys.
+ *  - Every call validates synchronously, then enqueues on `stream` and returns without a
+ *    host synchronisation.  Ordering across calls/streams is the caller's job (events).
+ *  - Errors: no exception crosses the ABI and nothing aborts.  The return value is an
+ *    apb_status; apb_last_error() gives a thread-local detail string.
+ *      APB_ERR_CONFIG      inconsistent sizes (n != H*l_b, host out of range, ...)
+ *      APB_ERR_CONTRACT    NULL / misaligned (16 B) pointer, bad stride, missing buffer
+ *      APB_ERR_UNSUPPORTED head_dim not in {64,128}, device not sm_100, d_hidden % 128 != 0
+ *      APB_ERR_CUDA        a CUDA call failed (launch error, no device, ...)
+ *      APB_ERR_NCCL        NCCL missing or an NCCL call failed
+ */
+#ifndef APB_H_
+#define APB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* apb_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    APB_OK = 0,
+    APB_ERR_CONFIG = 1,
+    APB_ERR_CONTRACT = 2,
+    APB_ERR_UNSUPPORTED = 3,
+    APB_ERR_CUDA = 4,
+    APB_ERR_NCCL = 5
+} apb_status;
+
+/* Problem statement of one host's layer.
+ *  n           document length l_d (tokens) — the query part is counted in l_q
+ *  H           number of hosts; host in [0, H) is this call's host (h = host + 1)
+ *  l_q, l_a    query length and anchor length; anchor = [q_1..q_lq, d_1..d_la] on host >= 1
+ *  l_b         block length; must equal n / H exactly (reading G15)
+ *  l_p         passing length per host (clamped to l_b)
+ *  n_heads, n_kv_heads, head_dim   GQA: query head qh reads KV head qh / (n_heads/n_kv_heads)
+ *  softmax_scale   <= 0 selects 1/sqrt(head_dim) (1/sqrt(d_m))            */
+typedef struct {
+    int64_t n;
+    int32_t H, host, l_q, l_a, l_b, l_p;
+    int32_t n_heads, n_kv_heads, head_dim;
+    float softmax_scale;
+} apb_dims;
+
+/* Retaining-head weights of one layer (hidden size d_hidden = 1024 at P:798).
+ *   z = W1 x + b1,  a = SiLU(z),  o = W2 a + b2,  s[j] = max_{c in group j} o[c]   (G2, G4)
+ *  d_in      must equal (n_heads + 2 n_kv_heads) * head_dim (x = [Q_t | K_t | V_t])
+ *  d_hidden  multiple of 128
+ *  n_out     n_kv_heads (identity pool) or n_heads (max over each KV head's query group)
+ *  w1  bf16 [d_hidden][d_in] row-major (device);  b1 fp32 [d_hidden] or NULL;
+ *  w2  fp32 [n_out][d_hidden] row-major;          b2 fp32 [n_out] or NULL.            */
+typedef struct {
+    int32_t d_in, d_hidden, n_out;
+    const void* w1;
+    const float* b1;
+    const float* w2;
+    const float* b2;
+} apb_retain_weights;
+
+typedef enum {
+    APB_PHASE_ALL = 0,     /* whole eq:apb in one launch                                         */
+    APB_PHASE_LOCAL = 1,   /* anchor rows (final) + local rows over anchor and local keys;
+                              local rows go to the workspace as an (O, lse) partial when P_h > 0,
+                              else straight to `out` (no passing needed)                         */
+    APB_PHASE_PASSING = 2  /* local rows over the passing keys, merged with the LOCAL partial by
+                              its log-sum-exp (exact online-softmax merge, P:753 MergeScore);
+                              writes the final `out` rows [L_A, L_A+l_b).  No-op if P_h == 0.   */
+} apb_phase;
+
+typedef enum { APB_WS_RETAIN = 0, APB_WS_SELECT = 1, APB_WS_ATTENTION = 2 } apb_ws_kind;
+
+/* ---------------------------------------------------------------- step 1: scoring
+ * scores[j][t] (fp32 [n_kv_heads][l_b]) for block rows t = L_A .. L_A+l_b-1 of q/k/v.
+ * Kernel: tcgen05 GEMM (A = [Q|K|V] rows via three TMA maps, B = W1) with a fused fp32
+ * epilogue (b1, SiLU, W2 dot, b2, group max).  Deterministic (no atomics).          */
+apb_status apb_retain_score(const apb_dims* dims, const apb_retain_weights* w,
+                            const void* q, const void* k, const void* v,
+                            int64_t q_row_stride, int64_t kv_row_stride,
+                            float* scores, void* ws, size_t ws_bytes, apb_stream_t stream);
+
+/* ---------------------------------------------------------------- step 2: select + compact
+ * For each KV head j: idx[j] = the l_p' block indices with the largest scores[j][.]
+ * (ties -> lower index, reading G5), written ASCENDING to indices (int32 [n_kv_heads][l_p']),
+ * then send[0][j][m] = K[L_A + idx[j][m]][j][:], send[1][j][m] = V[...] (bf16
+ * [2][n_kv_heads][l_p'][head_dim], contiguous).  -0.0 and +0.0 compare equal.
+ * `send` may alias gathered + host * slot (the in-place AllGather layout); no other aliasing. */
+apb_status apb_select_topk(const apb_dims* dims, const float* scores,
+                           const void* k, const void* v, int64_t kv_row_stride,
+                           int32_t* indices, void* send, void* ws, size_t ws_bytes,
+                           apb_stream_t stream);
+
+/* ---------------------------------------------------------------- step 3: exchange
+ * One in-place AllGather of the packed compressed blocks over NCCL (the
+ * paper's two AllGathers of K and V are fused into one, reading G11).
+ * gathered: bf16 [H][2][n_kv_heads][l_p'][head_dim].  The comm's nranks must divide H; rank
+ * r owns (and must already have written) slots [r*H/nranks, (r+1)*H/nranks).  After the
+ * call (in stream order) every slot holds that host's payload on every rank.  A comm with
+ * nranks == 1 (or comm == NULL) makes this a no-op.  dims->host is not used.           */
+typedef struct apb_comm apb_comm;
+apb_status apb_comm_get_unique_id(uint8_t id_out[128]);
+apb_status apb_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, apb_comm** out);
+apb_status apb_comm_destroy(apb_comm* comm);
+apb_status apb_exchange_passing(apb_comm* comm, const apb_dims* dims, void* gathered,
+                                apb_stream_t stream);
+
+/* ---------------------------------------------------------------- step 4: masked attention
+ * eq:apb: for query head qh and query row r in [0, L_A + l_b), with the key
+ * sequence [anchor rows of k | passing P_h | block rows of k] (passing = slots 0..host-1 of
+ * gathered, host order then ascending index):
+ *   r <  L_A : keys 0..r                                     (anchor: causal over the anchor)
+ *   r >= L_A : all L_A anchor keys, all P_h passing keys, block keys 0..r-L_A   (reading G1)
+ *   out[r][qh] = sum softmax(scale q.k) v (bf16), lse[qh][r] = log sum exp (fp32, natural log)
+ * gathered may be NULL iff P_h == 0 or phase == APB_PHASE_LOCAL.
+ * out: bf16 rows with out_row_stride elements (multiple of 8).  lse: NULL or [n_heads][L_A+l_b].
+ * ws: APB_WS_ATTENTION bytes, shared by the LOCAL and PASSING calls of one layer.
+ * Kernel: warp-specialised tcgen05 (TMEM accumulators, TMA loads, online softmax),
+ * fully masked tiles never visited.                                                    */
+apb_status apb_attention_fwd(const apb_dims* dims, const void* q, const void* k, const void* v,
+                             int64_t q_row_stride, int64_t kv_row_stride, const void* gathered,
+                             void* out, int64_t out_row_stride, float* lse, apb_phase phase,
+                             void* ws, size_t ws_bytes, apb_stream_t stream);
+
+/* ---------------------------------------------------------------- plumbing */
+apb_status apb_workspace_size(const apb_dims* dims, apb_ws_kind which, size_t* bytes);
+/* Validates dims alone (APB_ERR_CONFIG / APB_ERR_UNSUPPORTED) without touching a GPU. */
+apb_status apb_check_dims(const apb_dims* dims);
+const char* apb_status_string(apb_status s);
+const char* apb_last_error(void);
+int32_t apb_version(void);
+
+/* Counts of kernel launches issued by this process (for the bench's gpu_launches claim). */
+int64_t apb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APB_H_ */

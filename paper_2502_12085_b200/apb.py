@@ -1,0 +1,254 @@
+"""Thin Python binding of libapb (include/apb.h): argument marshalling only.
+
+Every step of the APB hot path runs in libapb's sm_100a kernels (or NCCL for the exchange);
+this module only turns torch tensors / streams into pointers, row strides and the C structs.
+There is no CPU fallback: if libapb.so cannot be loaded, or a call fails, an ApbError is
+raised.  Function names mirror the C entry points:
+
+    retain_score      -> apb_retain_score      (retaining heads)
+    select_topk       -> apb_select_topk       (ArgTop-l_p + compaction)
+    exchange_passing  -> apb_exchange_passing  (AllGather)
+    attention_fwd     -> apb_attention_fwd     (eq:apb)
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libapb.so")
+
+OK, ERR_CONFIG, ERR_CONTRACT, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL = range(6)
+PHASE_ALL, PHASE_LOCAL, PHASE_PASSING = 0, 1, 2
+WS_RETAIN, WS_SELECT, WS_ATTENTION = 0, 1, 2
+
+EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
+            "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
+            "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count")
+
+
+class ApbError(RuntimeError):
+    def __init__(self, status: int, fn: str, detail: str):
+        self.status = status
+        super().__init__(f"{fn} failed: status {status} ({_status_name(status)}): {detail}")
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("H", ctypes.c_int32), ("host", ctypes.c_int32),
+                ("l_q", ctypes.c_int32), ("l_a", ctypes.c_int32), ("l_b", ctypes.c_int32),
+                ("l_p", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
+
+
+class _Weights(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_int32), ("d_hidden", ctypes.c_int32), ("n_out", ctypes.c_int32),
+                ("w1", ctypes.c_void_p), ("b1", ctypes.c_void_p), ("w2", ctypes.c_void_p),
+                ("b2", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load libapb.so (fails loudly if it is missing — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise ApbError(ERR_CUDA, "load", f"{path} not built; run `python -m paper_2502_12085_b200.build`")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    dp = ctypes.POINTER(_Dims)
+    lib.apb_retain_score.argtypes = [dp, ctypes.POINTER(_Weights), vp, vp, vp, i64, i64, vp, vp, sz, vp]
+    lib.apb_select_topk.argtypes = [dp, vp, vp, vp, i64, vp, vp, vp, sz, vp]
+    lib.apb_exchange_passing.argtypes = [vp, dp, vp, vp]
+    lib.apb_attention_fwd.argtypes = [dp, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.c_int, vp, sz, vp]
+    lib.apb_comm_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.apb_comm_init.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
+    lib.apb_comm_destroy.argtypes = [vp]
+    lib.apb_workspace_size.argtypes = [dp, ctypes.c_int, ctypes.POINTER(sz)]
+    lib.apb_check_dims.argtypes = [dp]
+    for f in ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
+              "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
+              "apb_check_dims"):
+        getattr(lib, f).restype = ctypes.c_int
+    lib.apb_status_string.argtypes = [ctypes.c_int]
+    lib.apb_status_string.restype = ctypes.c_char_p
+    lib.apb_last_error.restype = ctypes.c_char_p
+    lib.apb_version.restype = ctypes.c_int32
+    lib.apb_launch_count.restype = ctypes.c_int64
+    _lib = lib
+    return lib
+
+
+def _status_name(s: int) -> str:
+    names = ["APB_OK", "APB_ERR_CONFIG", "APB_ERR_CONTRACT", "APB_ERR_UNSUPPORTED", "APB_ERR_CUDA", "APB_ERR_NCCL"]
+    return names[s] if 0 <= s < len(names) else "?"
+
+
+def _check(rc: int, fn: str) -> None:
+    if rc != OK:
+        raise ApbError(rc, fn, load().apb_last_error().decode(errors="replace"))
+
+
+# ----------------------------------------------------------------------------- problem dims
+
+@dataclasses.dataclass
+class Dims:
+    """apb_dims: one host's layer (symbols as the paper)."""
+    n: int
+    H: int
+    host: int
+    l_a: int
+    l_p: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    l_q: int = 0
+    l_b: int | None = None
+    softmax_scale: float = 0.0
+
+    def __post_init__(self):
+        if self.l_b is None:
+            self.l_b = self.n // self.H if self.H > 0 else 0
+
+    @property
+    def L_A(self) -> int:
+        return 0 if self.host == 0 else self.l_q + self.l_a
+
+    @property
+    def l_pp(self) -> int:
+        return min(self.l_p, self.l_b)
+
+    @property
+    def rows(self) -> int:
+        return self.L_A + self.l_b
+
+    @property
+    def P(self) -> int:
+        return self.host * self.l_pp
+
+    def with_host(self, host: int) -> "Dims":
+        return dataclasses.replace(self, host=host)
+
+    def c(self) -> _Dims:
+        return _Dims(self.n, self.H, self.host, self.l_q, self.l_a, self.l_b, self.l_p, self.n_heads,
+                     self.n_kv_heads, self.head_dim, self.softmax_scale)
+
+
+@dataclasses.dataclass
+class RetainWeights:
+    """apb_retain_weights: w1 bf16 [d_hidden][d_in]; b1 fp32 [d_hidden] | None; w2 fp32
+    [n_out][d_hidden]; b2 fp32 [n_out] | None (device tensors)."""
+    w1: torch.Tensor
+    w2: torch.Tensor
+    b1: torch.Tensor | None = None
+    b2: torch.Tensor | None = None
+
+    def c(self) -> _Weights:
+        d_hidden, d_in = self.w1.shape
+        return _Weights(d_in, d_hidden, self.w2.shape[0], self.w1.data_ptr(),
+                        self.b1.data_ptr() if self.b1 is not None else None, self.w2.data_ptr(),
+                        self.b2.data_ptr() if self.b2 is not None else None)
+
+
+def _rowstride(t: torch.Tensor, name: str) -> int:
+    """Row stride (elements) of a [rows][heads][head_dim] (or [rows][width]) tensor whose
+    inner dims are dense."""
+    if t.dim() == 3:
+        if t.stride(2) != 1 or t.stride(1) != t.shape[2]:
+            raise ApbError(ERR_CONTRACT, name, "inner dims must be dense [rows][heads][head_dim]")
+    elif t.dim() == 2:
+        if t.stride(1) != 1:
+            raise ApbError(ERR_CONTRACT, name, "last dim must be contiguous")
+    return t.stride(0)
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+# ----------------------------------------------------------------------------- entry points
+
+def workspace_size(dims: Dims, kind: int) -> int:
+    out = ctypes.c_size_t(0)
+    d = dims.c()
+    _check(load().apb_workspace_size(ctypes.byref(d), kind, ctypes.byref(out)), "apb_workspace_size")
+    return out.value
+
+
+def check_dims(dims: Dims) -> None:
+    d = dims.c()
+    _check(load().apb_check_dims(ctypes.byref(d)), "apb_check_dims")
+
+
+def retain_score(dims: Dims, w: RetainWeights, q, k, v, scores, stream=None) -> None:
+    d, wc = dims.c(), w.c()
+    _check(load().apb_retain_score(ctypes.byref(d), ctypes.byref(wc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                   _rowstride(q, "q"), _rowstride(k, "k"), scores.data_ptr(), None, 0,
+                                   _stream(stream)), "apb_retain_score")
+
+
+def select_topk(dims: Dims, scores, k, v, indices, send, stream=None) -> None:
+    d = dims.c()
+    _check(load().apb_select_topk(ctypes.byref(d), scores.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                  _rowstride(k, "k"), indices.data_ptr(), send.data_ptr(), None, 0,
+                                  _stream(stream)), "apb_select_topk")
+
+
+def attention_fwd(dims: Dims, q, k, v, gathered, out, lse=None, phase: int = PHASE_ALL, ws=None,
+                  stream=None) -> None:
+    d = dims.c()
+    _check(load().apb_attention_fwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), _rowstride(q, "q"),
+                                    _rowstride(k, "k"), _ptr(gathered), out.data_ptr(), _rowstride(out, "out"),
+                                    _ptr(lse), phase, _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                                    _stream(stream)), "apb_attention_fwd")
+
+
+class Comm:
+    """apb_comm: an NCCL communicator owned by libapb.  Build it on every rank from a 128-byte
+    id that rank 0 draws with `Comm.unique_id()` and broadcasts (e.g. torch.distributed)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        self._h = ctypes.c_void_p()
+        _check(load().apb_comm_init(uid, nranks, rank, ctypes.byref(self._h)), "apb_comm_init")
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load().apb_comm_get_unique_id(buf), "apb_comm_get_unique_id")
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if self._h:
+            _check(load().apb_comm_destroy(self._h), "apb_comm_destroy")
+            self._h = ctypes.c_void_p()
+
+
+def exchange_passing(comm: Comm | None, dims: Dims, gathered, stream=None) -> None:
+    d = dims.c()
+    _check(load().apb_exchange_passing(comm.handle if comm is not None else None, ctypes.byref(d),
+                                       gathered.data_ptr(), _stream(stream)), "apb_exchange_passing")
+
+
+def launch_count() -> int:
+    return int(load().apb_launch_count())
+
+
+def version() -> int:
+    return int(load().apb_version())

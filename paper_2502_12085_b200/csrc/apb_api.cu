@@ -1,0 +1,412 @@
+// apb_api.cu — the C ABI of libapb (include/apb.h): argument validation, workspace sizing, TMA
+// descriptor construction, NCCL exchange (dlopen'ed, no link-time dependency) and dispatch to
+// the sm_100a kernels.  No exception crosses the ABI; every failure is an apb_status plus a
+// thread-local detail string.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <dlfcn.h>
+#include <mutex>
+#include <string>
+
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include "internal.h"
+
+namespace apb {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+apb_status fail(apb_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                    const uint64_t* strides_bytes, const uint32_t* box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!encode) {
+    set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+    return false;
+  }
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+  }
+  for (int i = 0; i + 1 < rank; ++i) s[i] = strides_bytes[i];
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b, e,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed, CUresult " + std::to_string((int)r));
+    return false;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- validation helpers
+static int64_t L_A_of(const apb_dims* d) { return d->host == 0 ? 0 : (int64_t)d->l_q + d->l_a; }
+static int64_t lpp_of(const apb_dims* d) { return d->l_p < d->l_b ? d->l_p : d->l_b; }
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static apb_status check_dims(const apb_dims* d) {
+  if (!d) return fail(APB_ERR_CONTRACT, "dims is NULL");
+  if (d->H < 1) return fail(APB_ERR_CONFIG, "H must be >= 1");
+  if (d->host < 0 || d->host >= d->H) return fail(APB_ERR_CONFIG, "host must be in [0, H)");
+  if (d->l_q < 0 || d->l_a < 0 || d->l_p < 0 || d->l_b < 1) return fail(APB_ERR_CONFIG, "negative length");
+  if (d->n != (int64_t)d->H * d->l_b) return fail(APB_ERR_CONFIG, "n must equal H * l_b (reading G15)");
+  if (d->l_a > d->n) return fail(APB_ERR_CONFIG, "l_a must be <= n");
+  if (d->n_heads < 1 || d->n_kv_heads < 1 || d->n_heads % d->n_kv_heads)
+    return fail(APB_ERR_CONFIG, "n_heads must be a positive multiple of n_kv_heads");
+  if (d->head_dim != 64 && d->head_dim != 128) return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  const int64_t rows = L_A_of(d) + d->l_b;
+  if (rows > (int64_t)1 << 30) return fail(APB_ERR_CONFIG, "too many rows on one host");
+  if ((int64_t)d->H * lpp_of(d) > ((int64_t)1 << 30)) return fail(APB_ERR_CONFIG, "passing too long");
+  return APB_OK;
+}
+
+static apb_status check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  static int cached_major = -1, cached_minor = -1, cached_dev = -1;
+  if (cached_dev != dev) {
+    cudaDeviceGetAttribute(&cached_major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&cached_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached_dev = dev;
+  }
+  if (cached_major != 10 || cached_minor != 0)
+    return fail(APB_ERR_UNSUPPORTED, "libapb is built for sm_100a (B200); device is sm_" +
+                                         std::to_string(cached_major) + std::to_string(cached_minor));
+  return APB_OK;
+}
+
+static apb_status check_rows(const void* p, int64_t stride, int64_t min_stride, const char* what) {
+  if (!p) return fail(APB_ERR_CONTRACT, std::string(what) + " is NULL");
+  if (!aligned16(p)) return fail(APB_ERR_CONTRACT, std::string(what) + " is not 16-byte aligned");
+  if (stride < min_stride || stride % 8) return fail(APB_ERR_CONTRACT, std::string(what) + " row stride invalid");
+  return APB_OK;
+}
+
+}  // namespace apb
+
+using namespace apb;
+
+// ---------------------------------------------------------------- plumbing
+extern "C" const char* apb_status_string(apb_status s) {
+  switch (s) {
+    case APB_OK: return "APB_OK";
+    case APB_ERR_CONFIG: return "APB_ERR_CONFIG";
+    case APB_ERR_CONTRACT: return "APB_ERR_CONTRACT";
+    case APB_ERR_UNSUPPORTED: return "APB_ERR_UNSUPPORTED";
+    case APB_ERR_CUDA: return "APB_ERR_CUDA";
+    case APB_ERR_NCCL: return "APB_ERR_NCCL";
+  }
+  return "APB_ERR_UNKNOWN";
+}
+extern "C" const char* apb_last_error(void) { return g_last_error.c_str(); }
+extern "C" int32_t apb_version(void) { return 100; }
+extern "C" int64_t apb_launch_count(void) { return g_launches.load(); }
+extern "C" apb_status apb_check_dims(const apb_dims* d) { return check_dims(d); }
+
+extern "C" apb_status apb_workspace_size(const apb_dims* d, apb_ws_kind which, size_t* bytes) {
+  if (!bytes) return fail(APB_ERR_CONTRACT, "bytes is NULL");
+  apb_status st = check_dims(d);
+  if (st) return st;
+  *bytes = 0;
+  if (which == APB_WS_ATTENTION) {
+    if (d->host > 0 && lpp_of(d) > 0) {
+      size_t o = (size_t)d->l_b * d->n_heads * d->head_dim * sizeof(float);
+      o = (o + 255) & ~size_t(255);
+      *bytes = o + (size_t)d->n_heads * d->l_b * sizeof(float);
+    }
+  } else if (which != APB_WS_RETAIN && which != APB_WS_SELECT) {
+    return fail(APB_ERR_CONTRACT, "unknown workspace kind");
+  }
+  return APB_OK;
+}
+
+// ---------------------------------------------------------------- step 4: attention
+extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const void* k, const void* v,
+                                        int64_t q_row_stride, int64_t kv_row_stride, const void* gathered, void* out,
+                                        int64_t out_row_stride, float* lse, apb_phase phase, void* ws, size_t ws_bytes,
+                                        apb_stream_t stream) {
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (phase != APB_PHASE_ALL && phase != APB_PHASE_LOCAL && phase != APB_PHASE_PASSING)
+    return fail(APB_ERR_CONTRACT, "unknown phase");
+  const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
+  if ((st = check_rows(q, q_row_stride, (int64_t)hq * D, "q"))) return st;
+  if ((st = check_rows(k, kv_row_stride, (int64_t)hk * D, "k"))) return st;
+  if ((st = check_rows(v, kv_row_stride, (int64_t)hk * D, "v"))) return st;
+  if ((st = check_rows(out, out_row_stride, (int64_t)hq * D, "out"))) return st;
+  if (lse && (reinterpret_cast<uintptr_t>(lse) & 3)) return fail(APB_ERR_CONTRACT, "lse misaligned");
+  const int64_t L_A = L_A_of(d), lpp = lpp_of(d), rows = L_A + d->l_b;
+  const int n_slots = d->host;
+  const bool has_pass = n_slots > 0 && lpp > 0;
+  if (has_pass && phase != APB_PHASE_LOCAL) {
+    if (!gathered) return fail(APB_ERR_CONTRACT, "gathered is NULL but host > 0 and l_p > 0");
+    if (!aligned16(gathered)) return fail(APB_ERR_CONTRACT, "gathered is not 16-byte aligned");
+  }
+  size_t need = 0;
+  apb_workspace_size(d, APB_WS_ATTENTION, &need);
+  const bool use_ws = has_pass && phase != APB_PHASE_ALL;
+  if (use_ws && (ws == nullptr || ws_bytes < need || !aligned16(ws)))
+    return fail(APB_ERR_CONTRACT, "attention workspace missing, too small or misaligned");
+  if ((st = check_device())) return st;
+  if (phase == APB_PHASE_PASSING && !has_pass) return APB_OK;  // nothing to merge
+
+  AttnParams p{};
+  p.L_A = (int)L_A;
+  p.l_b = d->l_b;
+  p.lp = (int)lpp;
+  p.n_slots = has_pass ? n_slots : 0;
+  p.hq = hq;
+  p.hk = hk;
+  p.g = hq / hk;
+  p.np = (p.g + 1) / 2;
+  p.nA_rt = (int)((L_A + 127) / 128);
+  p.nB_rt = (d->l_b + 127) / 128;
+  p.nA_kv = p.nA_rt;
+  p.nP_kv = (int)((lpp + 127) / 128);
+  p.phase = (int)phase;
+  if (!has_pass && phase == APB_PHASE_LOCAL) p.phase = APB_PHASE_ALL;  // LOCAL == ALL without passing
+  p.local_to_ws = (phase == APB_PHASE_LOCAL && has_pass) ? 1 : 0;
+  p.n_local_items = p.nB_rt * hk * p.np;
+  p.n_anchor_items = (phase == APB_PHASE_PASSING) ? 0 : p.nA_rt * hk * p.np;
+  const float scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)D);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.out_row_stride = out_row_stride;
+  p.lse = lse;
+  p.lse_ld = rows;
+  if (use_ws) {
+    size_t o = (size_t)d->l_b * hq * D * sizeof(float);
+    o = (o + 255) & ~size_t(255);
+    p.ws_o = static_cast<float*>(ws);
+    p.ws_lse = reinterpret_cast<float*>(static_cast<char*>(ws) + o);
+  }
+
+  CUtensorMap tq, tk, tv, tg;
+  {
+    uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)rows};
+    uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};
+    uint32_t box[3] = {64, 1, 128};
+    if (!make_tmap_bf16(&tq, q, 3, dims, str, box)) return APB_ERR_CUDA;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)D, (uint64_t)hk, (uint64_t)rows};
+    uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)kv_row_stride * 2};
+    uint32_t box[3] = {64, 1, 128};
+    if (!make_tmap_bf16(&tk, k, 3, dims, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&tv, v, 3, dims, str, box)) return APB_ERR_CUDA;
+  }
+  if (p.n_slots > 0 && phase != APB_PHASE_LOCAL) {
+    uint64_t dims[4] = {(uint64_t)D, (uint64_t)lpp, (uint64_t)hk, (uint64_t)2 * d->H};
+    uint64_t str[3] = {(uint64_t)D * 2, (uint64_t)lpp * D * 2, (uint64_t)hk * lpp * D * 2};
+    uint32_t box[4] = {64, 128, 1, 1};
+    if (!make_tmap_bf16(&tg, gathered, 4, dims, str, box)) return APB_ERR_CUDA;
+  } else {
+    tg = tk;  // never dereferenced
+  }
+  return launch_attention(D, p, tq, tk, tv, tg, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- step 1: scoring
+extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weights* w, const void* q, const void* k,
+                                       const void* v, int64_t q_row_stride, int64_t kv_row_stride, float* scores,
+                                       void* ws, size_t ws_bytes, apb_stream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (!w) return fail(APB_ERR_CONTRACT, "weights is NULL");
+  const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
+  if (w->d_in != (hq + 2 * hk) * D) return fail(APB_ERR_CONFIG, "d_in must equal (n_heads + 2 n_kv_heads) * head_dim");
+  if (w->n_out != hk && w->n_out != hq) return fail(APB_ERR_CONFIG, "n_out must be n_kv_heads or n_heads");
+  if (w->d_hidden < 256 || w->d_hidden % 256) return fail(APB_ERR_UNSUPPORTED, "d_hidden must be a multiple of 256");
+  if (w->n_out > 64) return fail(APB_ERR_UNSUPPORTED, "n_out must be <= 64");
+  if (!w->w1 || !aligned16(w->w1) || !w->w2) return fail(APB_ERR_CONTRACT, "w1/w2 NULL or misaligned");
+  if ((st = check_rows(q, q_row_stride, (int64_t)hq * D, "q"))) return st;
+  if ((st = check_rows(k, kv_row_stride, (int64_t)hk * D, "k"))) return st;
+  if ((st = check_rows(v, kv_row_stride, (int64_t)hk * D, "v"))) return st;
+  if (!scores || (reinterpret_cast<uintptr_t>(scores) & 15)) return fail(APB_ERR_CONTRACT, "scores NULL or misaligned");
+  if ((st = check_device())) return st;
+  const int64_t L_A = L_A_of(d), rows = L_A + d->l_b;
+  ScoreParams p{};
+  p.l_b = d->l_b;
+  p.L_A = (int)L_A;
+  p.hq = hq;
+  p.hk = hk;
+  p.D = D;
+  p.d_in = w->d_in;
+  p.d_hidden = w->d_hidden;
+  p.n_out = w->n_out;
+  p.kq = hq * D / 64;
+  p.kk = hk * D / 64;
+  p.b1 = w->b1;
+  p.w2 = w->w2;
+  p.b2 = w->b2;
+  p.scores = scores;
+  CUtensorMap tq, tk, tv, tw;
+  uint32_t box[2] = {64, 128};
+  {
+    uint64_t dims[2] = {(uint64_t)hq * D, (uint64_t)rows};
+    uint64_t str[1] = {(uint64_t)q_row_stride * 2};
+    if (!make_tmap_bf16(&tq, q, 2, dims, str, box)) return APB_ERR_CUDA;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)hk * D, (uint64_t)rows};
+    uint64_t str[1] = {(uint64_t)kv_row_stride * 2};
+    if (!make_tmap_bf16(&tk, k, 2, dims, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&tv, v, 2, dims, str, box)) return APB_ERR_CUDA;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)w->d_in, (uint64_t)w->d_hidden};
+    uint64_t str[1] = {(uint64_t)w->d_in * 2};
+    uint32_t wbox[2] = {64, 256};
+    if (!make_tmap_bf16(&tw, w->w1, 2, dims, str, wbox)) return APB_ERR_CUDA;
+  }
+  return launch_retain_score(p, tq, tk, tv, tw, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- step 2: select + compact
+extern "C" apb_status apb_select_topk(const apb_dims* d, const float* scores, const void* k, const void* v,
+                                      int64_t kv_row_stride, int32_t* indices, void* send, void* ws, size_t ws_bytes,
+                                      apb_stream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
+  apb_status st = check_dims(d);
+  if (st) return st;
+  const int D = d->head_dim, hk = d->n_kv_heads;
+  const int64_t lpp = lpp_of(d);
+  if (lpp == 0) return APB_OK;
+  if (!scores || !indices) return fail(APB_ERR_CONTRACT, "scores/indices NULL");
+  if ((st = check_rows(k, kv_row_stride, (int64_t)hk * D, "k"))) return st;
+  if ((st = check_rows(v, kv_row_stride, (int64_t)hk * D, "v"))) return st;
+  if (!send || !aligned16(send)) return fail(APB_ERR_CONTRACT, "send NULL or misaligned");
+  if ((st = check_device())) return st;
+  return launch_select_compact(d->l_b, (int)lpp, hk, D, (int)L_A_of(d), scores, k, v, kv_row_stride, indices, send,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- step 3: exchange (NCCL)
+struct apb_comm {
+  ncclComm_t comm;
+  int32_t nranks, rank;
+};
+
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi* nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // Prefer the NCCL already loaded into the process (torch's), else the system one.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+    api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather) api.h = h;
+  });
+  return api.h ? &api : nullptr;
+}
+apb_status nccl_fail(NcclApi* api, ncclResult_t r, const char* what) {
+  return fail(APB_ERR_NCCL, std::string(what) + ": " + (api->getErrorString ? api->getErrorString(r) : "nccl error"));
+}
+}  // namespace
+
+extern "C" apb_status apb_comm_get_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(APB_ERR_CONTRACT, "id_out is NULL");
+  NcclApi* api = nccl();
+  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  ncclResult_t r = api->getUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclGetUniqueId");
+  static_assert(sizeof(id.internal) == 128, "NCCL unique id is 128 bytes");
+  std::memcpy(id_out, id.internal, 128);
+  return APB_OK;
+}
+
+extern "C" apb_status apb_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, apb_comm** out) {
+  if (!id || !out) return fail(APB_ERR_CONTRACT, "id/out is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(APB_ERR_CONFIG, "bad nranks/rank");
+  *out = nullptr;
+  apb_comm* c = new apb_comm{nullptr, nranks, rank};
+  if (nranks > 1) {
+    NcclApi* api = nccl();
+    if (!api) {
+      delete c;
+      return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+    }
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    ncclResult_t r = api->commInitRank(&c->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return nccl_fail(api, r, "ncclCommInitRank");
+    }
+  }
+  *out = c;
+  return APB_OK;
+}
+
+extern "C" apb_status apb_comm_destroy(apb_comm* c) {
+  if (!c) return APB_OK;
+  apb_status st = APB_OK;
+  if (c->comm) {
+    NcclApi* api = nccl();
+    if (api) {
+      ncclResult_t r = api->commDestroy(c->comm);
+      if (r != ncclSuccess) st = nccl_fail(api, r, "ncclCommDestroy");
+    }
+  }
+  delete c;
+  return st;
+}
+
+extern "C" apb_status apb_exchange_passing(apb_comm* c, const apb_dims* d, void* gathered, apb_stream_t stream) {
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (!c || c->nranks == 1) return APB_OK;
+  const int64_t lpp = lpp_of(d);
+  if (lpp == 0) return APB_OK;
+  if (!gathered || !aligned16(gathered)) return fail(APB_ERR_CONTRACT, "gathered NULL or misaligned");
+  if (d->H % c->nranks) return fail(APB_ERR_CONFIG, "comm nranks must divide H");
+  NcclApi* api = nccl();
+  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+  const size_t slot = (size_t)2 * d->n_kv_heads * lpp * d->head_dim;  // bf16 elements per host slot
+  const size_t count = slot * (d->H / c->nranks);                         // elements per rank
+  char* base = static_cast<char*>(gathered);
+  ncclResult_t r = api->allGather(base + (size_t)c->rank * count * 2, base, count, ncclBfloat16, c->comm,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather");
+  return APB_OK;
+}

@@ -1,0 +1,59 @@
+// internal.h — declarations shared by libapb's translation units (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <cuda_runtime.h>
+#include <cuda.h>
+#include "../../include/apb.h"
+
+namespace apb {
+
+// thread-local error detail for apb_last_error()
+void set_error(const std::string& msg);
+apb_status fail(apb_status s, const std::string& msg);
+void count_launch(int n = 1);
+
+// TMA descriptor encoding through the driver entry point (no -lcuda at link time).
+// Returns false (and sets the error) if the driver call fails.
+bool make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                    const uint64_t* strides_bytes, const uint32_t* box);
+
+// ---------------------------------------------------------------- attention
+struct AttnParams {
+  int L_A, l_b, lp, n_slots;  // n_slots = host: passing slots 0..host-1
+  int hq, hk, g, np;          // np = ceil(g/2): Q-tile pairs per (row tile, KV head)
+  int nA_rt, nB_rt;           // 128-row query tiles of the anchor / local segment
+  int nA_kv, nP_kv;           // 128-key tiles of the anchor segment / of one passing slot
+  int n_local_items, n_anchor_items;
+  int phase;                  // apb_phase
+  int local_to_ws;            // LOCAL phase: local rows -> fp32 partial in ws
+  float scale_log2;           // softmax_scale * log2(e)
+  void* out;
+  int64_t out_row_stride;
+  float* lse;
+  int64_t lse_ld;
+  float* ws_o;                // [l_b][hq][D] fp32
+  float* ws_lse;              // [hq][l_b] fp32, log2 domain
+};
+apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                            const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream);
+
+// ---------------------------------------------------------------- retaining-head scoring
+struct ScoreParams {
+  int l_b, L_A, hq, hk, D, d_in, d_hidden, n_out;
+  int kq, kk;                 // number of 64-wide K blocks coming from Q and from K (rest from V)
+  const float* b1;
+  const float* w2;
+  const float* b2;
+  float* scores;              // [hk][l_b]
+};
+apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                               const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream);
+
+// ---------------------------------------------------------------- selection + compaction
+apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores,
+                                 const void* k, const void* v, int64_t kv_row_stride, int32_t* indices,
+                                 void* send, cudaStream_t stream);
+
+}  // namespace apb

@@ -1,0 +1,201 @@
+// retain_score_sm100.cu — retaining-head scoring s = R([Q_h, K_h, V_h]) (PAPER.md:171-180,
+// Alg. apb_prefill line retbeg; hidden size 1024 at P:798; readings G2/G4 in DESIGN.md).
+//
+//   z = W1 x + b1  (tcgen05 GEMM, bf16 x bf16 -> fp32 in TMEM)
+//   a = SiLU(z);  o = W2 a + b2;  s[j] = max over KV head j's group of o   (fp32 epilogue)
+//
+// CTA = 128 block tokens.  The A operand x_t = [Q_t | K_t | V_t] is never materialised: its
+// 64-wide K blocks come straight from three TMA maps over the caller's Q, K and V rows.  The
+// hidden dimension is walked in 256-wide chunks; each chunk's accumulator (128 x 256 fp32 =
+// 256 TMEM columns) is double buffered so the epilogue of chunk c overlaps the MMAs of c+1.
+// The W2 dot products stay in fp32 (rounding the hidden activations to bf16 changes the
+// selected index sets) and are accumulated in a fixed order — no atomics, so the
+// scores are bit-reproducible run to run.
+// Warps 0-7: epilogue (warpgroup w handles columns [128w, 128w+128) of a chunk), warp 8: TMA,
+// warp 9: MMA issuer.
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace apb {
+namespace score {
+
+using namespace apb::sm100;
+
+constexpr int TM = 128;     // tokens per CTA
+constexpr int TN = 256;     // hidden units per chunk (MMA N)
+constexpr int TK = 64;      // K block (one 128-byte swizzle atom)
+constexpr int STAGES = 3;
+constexpr int kThreads = 320;
+constexpr int kLoadWarp = 8, kMmaWarp = 9;
+constexpr int kMaxOut = 64;
+
+constexpr int kABytes = TM * TK * 2;  // 16 KB
+constexpr int kBBytes = TN * TK * 2;  // 32 KB
+constexpr int kOffA = 0;
+constexpr int kOffB = kOffA + STAGES * kABytes;
+constexpr int kOffO = kOffB + STAGES * kBBytes;              // fp32 partial o: [2][kMaxOut][TM]
+constexpr int kOffBar = kOffO + 2 * kMaxOut * TM * 4;
+constexpr int kNumBars = 2 * STAGES + 4;                      // full/empty per stage, acc full/empty x2
+constexpr int kOffTmem = kOffBar + kNumBars * 8;
+constexpr int kSmem = kOffTmem + 16 + 1024;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    retain_score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_w1,
+                        const ScoreParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + kOffBar;
+  auto bFull = [&](int s) { return bar0 + 8u * s; };
+  auto bEmpty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto bAccFull = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
+  auto bAccEmpty = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  float* opart = reinterpret_cast<float*>(smem + kOffO);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.x * TM;
+  const int nkb = p.d_in / TK;
+  const int nchunks = p.d_hidden / TN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bFull(s), 1);
+      mbar_init(bEmpty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bAccFull(b), 1);
+      mbar_init(bAccEmpty(b), 256);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kLoadWarp) tmem_alloc<512>(smem_u32(tmem_ptr));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == kLoadWarp) {
+    if (lane == 0) {
+      const int row = p.L_A + m0;
+      for (int c = 0; c < nchunks; ++c) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int it = c * nkb + kb, s = it % STAGES;
+          mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(bFull(s), kABytes + kBBytes);
+          const uint32_t dA = sbase + kOffA + s * kABytes;
+          if (kb < p.kq)
+            tma_load_2d(dA, &tm_q, bFull(s), kb * TK, row);
+          else if (kb < p.kq + p.kk)
+            tma_load_2d(dA, &tm_k, bFull(s), (kb - p.kq) * TK, row);
+          else
+            tma_load_2d(dA, &tm_v, bFull(s), (kb - p.kq - p.kk) * TK, row);
+          tma_load_2d(sbase + kOffB + s * kBBytes, &tm_w1, bFull(s), kb * TK, c * TN);
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(TM, TN, false, false);
+      for (int c = 0; c < nchunks; ++c) {
+        const int b = c & 1;
+        mbar_wait(bAccEmpty(b), ((c >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int it = c * nkb + kb, s = it % STAGES;
+          mbar_wait(bFull(s), (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t aA = sbase + kOffA + s * kABytes, aB = sbase + kOffB + s * kBBytes;
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)
+            mma_ss(tmem + b * TN, sdesc_sw128(aA + k * 32, 16, 1024), sdesc_sw128(aB + k * 32, 16, 1024), idesc,
+                   (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit(bEmpty(s));
+        }
+        mma_commit(bAccFull(b));
+      }
+    }
+  } else {
+    // ================================================================ epilogue (256 threads)
+    const int wg = warp / 4;          // column half of the chunk
+    const int r = threadIdx.x % 128;  // token row in the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float* my_o = opart + (size_t)wg * kMaxOut * TM;
+    for (int oc = 0; oc < p.n_out; ++oc) my_o[oc * TM + r] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int b = c & 1;
+      mbar_wait(bAccFull(b), (c >> 1) & 1);
+      tc_fence_after();
+      uint32_t zr[128];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        tmem_ld32(tmem + lane_base + b * TN + wg * 128 + q4 * 32, *reinterpret_cast<uint32_t(*)[32]>(&zr[q4 * 32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bAccEmpty(b));  // TMEM buffer free: the next-but-one chunk may accumulate into it
+      const int u0 = c * TN + wg * 128;
+      float* a = reinterpret_cast<float*>(zr);
+#pragma unroll
+      for (int e = 0; e < 128; ++e) {
+        float z = a[e] + (p.b1 ? __ldg(p.b1 + u0 + e) : 0.f);
+        a[e] = __fdividef(z, 1.f + __expf(-z));  // SiLU
+      }
+      for (int oc = 0; oc < p.n_out; ++oc) {
+        const float4* w = reinterpret_cast<const float4*>(p.w2 + (size_t)oc * p.d_hidden + u0);
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+        for (int e4 = 0; e4 < 32; ++e4) {
+          const float4 wv = __ldg(w + e4);
+          acc0 = fmaf(wv.x, a[4 * e4 + 0], acc0);
+          acc1 = fmaf(wv.y, a[4 * e4 + 1], acc1);
+          acc2 = fmaf(wv.z, a[4 * e4 + 2], acc2);
+          acc3 = fmaf(wv.w, a[4 * e4 + 3], acc3);
+        }
+        my_o[oc * TM + r] += (acc0 + acc1) + (acc2 + acc3);
+      }
+    }
+    named_bar_sync(1, 256);
+    if (wg == 0 && m0 + r < p.l_b) {
+      const int rr = p.n_out / p.hk;
+      const float* o0 = opart;
+      const float* o1 = opart + (size_t)kMaxOut * TM;
+      for (int j = 0; j < p.hk; ++j) {
+        float m = -INFINITY;
+        for (int cc = j * rr; cc < (j + 1) * rr; ++cc) {
+          const float o = o0[cc * TM + r] + o1[cc * TM + r] + (p.b2 ? __ldg(p.b2 + cc) : 0.f);
+          m = fmaxf(m, o);
+        }
+        p.scores[(int64_t)j * p.l_b + m0 + r] = m;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kLoadWarp) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace score
+
+apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                               const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(score::retain_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         score::kSmem);
+    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    attr_set = true;
+  }
+  const int grid = (p.l_b + score::TM - 1) / score::TM;
+  score::retain_score_kernel<<<grid, score::kThreads, score::kSmem, stream>>>(tq, tk, tv, tw1, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("retain_score launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+}  // namespace apb

@@ -1,0 +1,102 @@
+"""APB prefill hot path for the hosts one rank owns — stream/event orchestration over libapb.
+
+Alg. apb_prefill per layer, for every host h this rank owns:
+
+    side stream:  apb_retain_score(h) -> apb_select_topk(h) (writes gathered[h] in place)
+                  -> apb_exchange_passing (one NCCL AllGather of all slots)  -> event E
+    main stream:  apb_attention_fwd(h, LOCAL)   (anchor rows + local rows over anchor/local
+                                                 keys: overlaps the side stream)
+                  wait E -> apb_attention_fwd(h, PASSING)  (local rows over the passing keys,
+                                                 merged with the LOCAL partial by LSE)
+
+With H hosts over N ranks, rank r owns hosts [r*H/N, (r+1)*H/N) (N = H is the paper's
+deployment, one host per GPU; N < H emulates several hosts per GPU).  Everything numeric runs
+in libapb; this module only allocates buffers and orders launches.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import apb
+
+
+@dataclasses.dataclass
+class HostIO:
+    """One host's per-layer tensors (device): q [L_A+l_b][hq][d], k/v [L_A+l_b][hk][d] bf16;
+    out like q; lse fp32 [hq][L_A+l_b] or None."""
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    out: torch.Tensor
+    lse: torch.Tensor | None = None
+
+
+class PrefillRank:
+    def __init__(self, base: apb.Dims, hosts: list[int], comm: apb.Comm | None = None,
+                 device: torch.device | str = "cuda", skip_unused_last: bool = False):
+        """base: problem dims (its `host` field is ignored); hosts: host indices this rank owns
+        (contiguous, in order).  skip_unused_last: do not score/select host H-1 — its
+        compressed block is ignored by every host, so outputs are unchanged."""
+        self.base, self.hosts, self.comm = base, list(hosts), comm
+        self.device = torch.device(device)
+        self.skip_unused_last = skip_unused_last
+        b = base
+        lpp, hk, hq, d = b.l_pp, b.n_kv_heads, b.n_heads, b.head_dim
+        self.gathered = torch.zeros((b.H, 2, hk, lpp, d), dtype=torch.bfloat16, device=self.device)
+        self.scores = {h: torch.empty((hk, b.l_b), dtype=torch.float32, device=self.device) for h in hosts}
+        self.indices = {h: torch.empty((hk, max(lpp, 1)), dtype=torch.int32, device=self.device) for h in hosts}
+        self.ws = {}
+        for h in hosts:
+            n = apb.workspace_size(b.with_host(h), apb.WS_ATTENTION)
+            self.ws[h] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device) if n else None
+        self.side = torch.cuda.Stream(device=self.device)
+        self.ev_exchanged = torch.cuda.Event()
+
+    def dims(self, h: int) -> apb.Dims:
+        return self.base.with_host(h)
+
+    def compress(self, io: dict[int, HostIO], weights: apb.RetainWeights, stream=None) -> None:
+        """Steps 1-2 for every owned host: scores -> top-l_p indices -> gathered[h] (in place)."""
+        for h in self.hosts:
+            if self.base.l_pp == 0 or (self.skip_unused_last and h == self.base.H - 1):
+                continue
+            d, x = self.dims(h), io[h]
+            apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h], stream=stream)
+            apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h], self.gathered[h], stream=stream)
+
+    def exchange(self, stream=None) -> None:
+        """Step 3: one in-place AllGather of the packed [2][hk][l_p'][d] slots."""
+        apb.exchange_passing(self.comm, self.base, self.gathered, stream=stream)
+
+    def attention(self, io: dict[int, HostIO], phase: int, stream=None) -> None:
+        for h in self.hosts:
+            x = io[h]
+            apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse, phase=phase,
+                              ws=self.ws[h], stream=stream)
+
+    def layer(self, io: dict[int, HostIO], weights: apb.RetainWeights, overlap: bool = True) -> None:
+        """One layer of the hot path for all owned hosts, enqueued on the current stream."""
+        main = torch.cuda.current_stream(self.device)
+        if not overlap:
+            self.compress(io, weights, main)
+            self.exchange(main)
+            self.attention(io, apb.PHASE_ALL, main)
+            return
+        self.side.wait_stream(main)  # this layer's inputs are produced on the main stream
+        self.compress(io, weights, self.side)
+        self.exchange(self.side)
+        self.ev_exchanged.record(self.side)
+        self.attention(io, apb.PHASE_LOCAL, main)
+        main.wait_event(self.ev_exchanged)
+        self.attention(io, apb.PHASE_PASSING, main)
+        # the side stream's buffers (scores, gathered) are reused next layer only after main
+        # has consumed them: next layer's side.wait_stream(main) orders that.
+
+
+def hosts_of_rank(H: int, world: int, rank: int) -> list[int]:
+    if H % world:
+        raise ValueError(f"world size {world} must divide H={H}")
+    per = H // world
+    return list(range(rank * per, (rank + 1) * per))

@@ -36,8 +36,8 @@ _T_Q, _T_K, _T_V, _T_QQ, _T_W1, _T_B1, _T_W2, _T_NEEDLE, _T_SCORES = range(9)
 def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """Round fp32 -> bf16 (round-to-nearest-even), returned as uint16 bit patterns."""
     x = np.ascontiguousarray(x, dtype=np.float32)
-    u = x.view(np.uint32).astype(np.uint64)
-    rounding = ((u >> 16) & 1) + 0x7FFF
+    u = x.view(np.uint32)
+    rounding = ((u >> 16) & np.uint32(1)) + np.uint32(0x7FFF)  # finite inputs never overflow
     return ((u + rounding) >> 16).astype(np.uint16)
 
 

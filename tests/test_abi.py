@@ -1,0 +1,153 @@
+"""libapb C ABI: the library loads on a CPU-only box, exports every symbol include/apb.h declares,
+and validates arguments synchronously (config / contract errors) before touching a GPU — and
+fails loudly (APB_ERR_CUDA), never silently, when no GPU is present."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+import torch
+
+from paper_2502_12085_b200 import apb
+from paper_2502_12085_b200 import build as apb_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    apb_build.build()
+    return apb.load()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "apb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(apb_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert {"apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", apb.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (apb_\w+)", out))
+    assert set(names) <= exported, set(names) - exported
+
+
+def test_binary_is_sm100a_with_tcgen05_and_tma(lib):
+    sass = subprocess.run(["cuobjdump", "-sass", apb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", apb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass  # tcgen05.mma
+    assert "UTMALDG" in sass  # TMA loads
+    assert "LDTM" in sass and "STTM" in sass  # TMEM <-> registers
+    assert "HMMA" not in re.sub(r"UTCHMMA", "", sass)  # no legacy mma.sync path
+
+
+def _dims(**kw):
+    base = dict(n=2048, H=4, host=1, l_a=128, l_p=64, n_heads=4, n_kv_heads=2, head_dim=64)
+    base.update(kw)
+    return apb.Dims(**base)
+
+
+def test_status_strings_and_version(lib):
+    assert lib.apb_status_string(0) == b"APB_OK"
+    assert lib.apb_status_string(5) == b"APB_ERR_NCCL"
+    assert apb.version() >= 100
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(H=0), apb.ERR_CONFIG),
+    (dict(host=4), apb.ERR_CONFIG),
+    (dict(host=-1), apb.ERR_CONFIG),
+    (dict(l_b=500), apb.ERR_CONFIG),          # n != H * l_b (reading G15)
+    (dict(n_heads=3), apb.ERR_CONFIG),        # not a multiple of n_kv_heads
+    (dict(l_a=-1), apb.ERR_CONFIG),
+    (dict(head_dim=96), apb.ERR_UNSUPPORTED),
+])
+def test_check_dims_rejects(lib, kw, status):
+    with pytest.raises(apb.ApbError) as e:
+        apb.check_dims(_dims(**kw))
+    assert e.value.status == status
+
+
+def test_check_dims_accepts_paper_configs(lib):
+    apb.check_dims(_dims())
+    apb.check_dims(apb.Dims(n=131072, H=8, host=7, l_a=4096, l_p=2048, n_heads=32, n_kv_heads=8, head_dim=128))
+    apb.check_dims(apb.Dims(n=131072, H=1, host=0, l_a=4096, l_p=2048, n_heads=32, n_kv_heads=8, head_dim=128))
+
+
+def test_workspace_sizes(lib):
+    d = _dims(host=2)
+    assert apb.workspace_size(d, apb.WS_ATTENTION) >= d.l_b * 4 * 64 * 4 + 4 * d.l_b * 4
+    assert apb.workspace_size(_dims(host=0), apb.WS_ATTENTION) == 0   # host 1: no passing
+    assert apb.workspace_size(_dims(l_p=0), apb.WS_ATTENTION) == 0    # l_p = 0: no passing
+    assert apb.workspace_size(d, apb.WS_SELECT) == 0
+
+
+class _FakeT:
+    """Stands in for a device tensor: only data_ptr / stride / shape are read by the binding."""
+
+    def __init__(self, ptr, shape, elem=2):
+        self._p, self.shape = ptr, shape
+        st, s = [], 1
+        for x in reversed(shape):
+            st.append(s)
+            s *= x
+        self._st = tuple(reversed(st))
+        self._e = elem
+
+    def data_ptr(self):
+        return self._p
+
+    def stride(self, i):
+        return self._st[i]
+
+    def dim(self):
+        return len(self.shape)
+
+    def numel(self):
+        n = 1
+        for x in self.shape:
+            n *= x
+        return n
+
+    def element_size(self):
+        return self._e
+
+
+def test_contract_errors_before_any_gpu_work(lib):
+    d = _dims(host=0)
+    rows = d.rows
+    q = _FakeT(0x10000, (rows, 4, 64)); k = _FakeT(0x20000, (rows, 2, 64)); v = _FakeT(0x30000, (rows, 2, 64))
+    out = _FakeT(0x40000, (rows, 4, 64))
+    # misaligned q
+    with pytest.raises(apb.ApbError) as e:
+        apb.attention_fwd(d, _FakeT(0x10002, (rows, 4, 64)), k, v, None, out, stream=0)
+    assert e.value.status == apb.ERR_CONTRACT
+    # NULL gathered although host > 0 and l_p > 0
+    with pytest.raises(apb.ApbError) as e:
+        apb.attention_fwd(_dims(host=1), q, k, v, None, out, stream=0)
+    assert e.value.status == apb.ERR_CONTRACT
+    # weights with the wrong d_in
+    w = apb.RetainWeights(w1=_FakeT(0x50000, (1024, 100)), w2=_FakeT(0x60000, (4, 1024), 4))
+    with pytest.raises(apb.ApbError) as e:
+        apb.retain_score(d, w, q, k, v, _FakeT(0x70000, (2, 512), 4), stream=0)
+    assert e.value.status == apb.ERR_CONFIG
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_fails_loudly_without_gpu(lib):
+    d = _dims(host=0)
+    rows = d.rows
+    q = _FakeT(0x10000, (rows, 4, 64)); k = _FakeT(0x20000, (rows, 2, 64)); v = _FakeT(0x30000, (rows, 2, 64))
+    with pytest.raises(apb.ApbError) as e:
+        apb.attention_fwd(d, q, k, v, None, _FakeT(0x40000, (rows, 4, 64)), stream=0)
+    assert e.value.status == apb.ERR_CUDA
+
+
+def test_exchange_single_rank_is_noop(lib):
+    # comm == NULL (one rank) is a legal no-op that never touches memory
+    apb.exchange_passing(None, _dims(), _FakeT(0x10000, (4, 2, 2, 64, 64)), stream=0)

@@ -1,0 +1,309 @@
+"""GPU parity: libapb (sm_100a, through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star, made precise in SURVEY.md 8(c) / DESIGN.md):
+  attention  max|O - O_or| <= 2e-2, mean|O - O_or| <= 2e-3, |lse - lse_or| <= 1e-2
+  scores     |s - s_or| <= 1e-2 * max(|s_or|, rms_j(s_or))
+  indices    bit-exact vs the oracle's stable sort of the SAME fp32 scores; end to end, every
+             index in the symmetric difference has an oracle score within 1e-3 of the cut
+  compaction / gathered buffer: bit-exact
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ATOL_MAX, ATOL_MEAN, LSE_TOL = 2e-2, 2e-3, 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2502_12085_b200 import apb, build
+    build.build()
+    apb.load()
+
+
+def dev(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def to_bits(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def dims_of(cfg, host):
+    from paper_2502_12085_b200 import apb
+    return apb.Dims(n=cfg.n, H=cfg.H, host=host, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq,
+                    n_kv_heads=cfg.hk, head_dim=cfg.d, l_q=cfg.l_q)
+
+
+def weights_dev(w):
+    from paper_2502_12085_b200 import apb
+    return apb.RetainWeights(w1=dev(w["w1"]), w2=torch.from_numpy(w["w2"]).cuda(),
+                             b1=torch.from_numpy(w["b1"]).cuda(), b2=torch.from_numpy(w["b2"]).cuda())
+
+
+def check_attention(O, lse, O_ref, lse_ref, what):
+    err = np.abs(O - O_ref)
+    lerr = np.abs(lse - lse_ref)
+    msg = f"{what}: max {err.max():.3e} mean {err.mean():.3e} lse {lerr.max():.3e}"
+    print(msg)
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN and lerr.max() <= LSE_TOL, msg
+
+
+def run_attention(cfg, host, x, gathered_bits, phase):
+    """x: synth host dict; returns (O fp64 [rows][hq][d], lse fp64 [rows][hq])."""
+    from paper_2502_12085_b200 import apb
+    d = dims_of(cfg, host)
+    q, k, v = dev(x["q"]), dev(x["k"]), dev(x["v"])
+    out = torch.full_like(q, float("nan"))
+    lse = torch.full((cfg.hq, d.rows), float("nan"), device="cuda")
+    g = dev(gathered_bits) if gathered_bits is not None else None
+    n_ws = apb.workspace_size(d, apb.WS_ATTENTION)
+    ws = torch.empty(max(n_ws, 16), dtype=torch.uint8, device="cuda")
+    if phase == "split":
+        apb.attention_fwd(d, q, k, v, None, out, lse, phase=apb.PHASE_LOCAL, ws=ws)
+        apb.attention_fwd(d, q, k, v, g, out, lse, phase=apb.PHASE_PASSING, ws=ws)
+    else:
+        apb.attention_fwd(d, q, k, v, g, out, lse, phase=apb.PHASE_ALL, ws=ws)
+    torch.cuda.synchronize()
+    return out.float().cpu().double().numpy(), lse.cpu().double().numpy().T
+
+
+def oracle_layer(cfg):
+    hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    return hosts, oracle.prefill_layer(hosts, synth.retain_weights(cfg, 0), cfg.l_p)
+
+
+# ----------------------------------------------------------------------------- attention
+
+CASES = {
+    "toy": synth.CONFIGS["toy"],
+    "d128-ragged": synth.Config("d128-ragged", 11, n=1536, H=3, l_a=200, l_p=100, hq=8, hk=2, d=128, d_hidden=256),
+    "gqa3": synth.Config("gqa3", 12, n=1024, H=4, l_a=64, l_p=48, hq=6, hk=2, d=128, d_hidden=256),
+    "d64-peaky": synth.Config("d64-peaky", 13, n=1280, H=5, l_a=40, l_p=30, hq=4, hk=1, d=64, d_hidden=256,
+                              dist="D2"),
+    "d128-sink": synth.Config("d128-sink", 14, n=2048, H=4, l_a=256, l_p=128, hq=4, hk=2, d=128, d_hidden=256,
+                              dist="D3"),
+    "lq": synth.Config("lq", 15, n=1024, H=2, l_a=100, l_p=64, hq=4, hk=2, d=64, d_hidden=256, l_q=37),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("phase", ["all", "split"])
+def test_attention_parity(name, phase):
+    cfg = CASES[name]
+    hosts, ref = oracle_layer(cfg)
+    for h in range(cfg.H):
+        O, lse = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
+        check_attention(O, lse, ref["O"][h], ref["lse"][h], f"{name} host {h} {phase}")
+
+
+def test_attention_single_host_causal():
+    """H = 1: plain causal attention, no anchor, no passing."""
+    cfg = synth.Config("h1", 16, n=700, H=1, l_a=64, l_p=32, hq=4, hk=2, d=128, d_hidden=256)
+    hosts, ref = oracle_layer(cfg)
+    O, lse = run_attention(cfg, 0, hosts[0], None, "all")
+    check_attention(O, lse, ref["O"][0], ref["lse"][0], "H=1")
+
+
+def test_attention_lp_zero():
+    """l_p = 0: StarAttn-style, gathered may be NULL."""
+    cfg = synth.CONFIGS["toy"].replace(l_p=0)
+    hosts, ref = oracle_layer(cfg)
+    for h in range(cfg.H):
+        O, lse = run_attention(cfg, h, hosts[h], None, "split")
+        check_attention(O, lse, ref["O"][h], ref["lse"][h], f"lp0 host {h}")
+
+
+def test_attention_uniform_closed_form():
+    """Q = 0 => lse = ln|vis(r)| exactly and O = mean of visible V (pin P16 on the GPU path)."""
+    from paper_2502_12085_b200 import apb
+    cfg = CASES["d128-ragged"]
+    h = 2
+    x = dict(synth.host_qkv(cfg, 0, h))
+    x["q"] = np.zeros_like(x["q"])
+    hosts, ref = oracle_layer(cfg)
+    O, lse = run_attention(cfg, h, x, ref["gathered"], "split")
+    L_A, P = cfg.L_A(h), cfg.P(h)
+    counts = np.array([r + 1 for r in range(L_A)] + [L_A + P + i + 1 for i in range(cfg.l_b)], np.float64)
+    assert np.abs(lse - np.log(counts)[:, None]).max() < 1e-4
+
+
+# ----------------------------------------------------------------------------- scoring / selection
+
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3"])
+@pytest.mark.parametrize("n_out", ["hq", "hk"])
+def test_retain_score_parity(name, n_out):
+    from paper_2502_12085_b200 import apb
+    cfg = CASES[name].replace(d_hidden=1024)
+    w = synth.retain_weights(cfg, 0, n_out=cfg.hq if n_out == "hq" else cfg.hk)
+    for h in range(cfg.H):
+        x = synth.host_qkv(cfg, 0, h)
+        s = torch.empty((cfg.hk, cfg.l_b), dtype=torch.float32, device="cuda")
+        apb.retain_score(dims_of(cfg, h), weights_dev(w), dev(x["q"]), dev(x["k"]), dev(x["v"]), s)
+        torch.cuda.synchronize()
+        s = s.cpu().double().numpy()
+        s_or = oracle.retain_score(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
+        floor = np.sqrt((s_or ** 2).mean(axis=1, keepdims=True))
+        rel = np.abs(s - s_or) / np.maximum(np.abs(s_or), floor)
+        print(f"{name} h{h} n_out={n_out}: max rel {rel.max():.3e} max abs {np.abs(s - s_or).max():.3e}")
+        assert rel.max() <= 1e-2
+        # determinism (pin P15): bit-identical on a second run
+        s2 = torch.empty((cfg.hk, cfg.l_b), dtype=torch.float32, device="cuda")
+        apb.retain_score(dims_of(cfg, h), weights_dev(w), dev(x["q"]), dev(x["k"]), dev(x["v"]), s2)
+        assert np.array_equal(s2.cpu().double().numpy(), s)
+
+
+def _select_gpu(cfg, h, x, scores_np):
+    from paper_2502_12085_b200 import apb
+    s = torch.from_numpy(np.ascontiguousarray(scores_np, dtype=np.float32)).cuda()
+    idx = torch.full((cfg.hk, cfg.l_pp), -1, dtype=torch.int32, device="cuda")
+    send = torch.zeros((2, cfg.hk, cfg.l_pp, cfg.d), dtype=torch.bfloat16, device="cuda")
+    apb.select_topk(dims_of(cfg, h), s, dev(x["k"]), dev(x["v"]), idx, send)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), to_bits(send)
+
+
+@pytest.mark.parametrize("ties", [False, True])
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3"])
+def test_select_compact_bit_exact(name, ties):
+    cfg = CASES[name]
+    for h in range(cfg.H):
+        x = synth.host_qkv(cfg, 0, h)
+        sc = synth.random_scores(cfg, 0, h, ties=ties)
+        if h == 1:
+            sc[:, ::7] = -0.0  # -0.0 and +0.0 must tie
+            sc[:, 3::7] = 0.0
+            sc[0, 5] = np.inf
+            sc[-1, 9] = -np.inf
+        idx, send = _select_gpu(cfg, h, x, sc)
+        idx_or = oracle.select_all_heads(sc.astype(np.float64), cfg.l_p)
+        assert np.array_equal(idx, idx_or), f"host {h}"
+        assert np.array_equal(send, oracle.compact(x["k"], x["v"], x["L_A"], idx_or))
+
+
+@pytest.mark.parametrize("lp,l_b", [(1, 300), (300, 300), (500, 300), (129, 1000), (4096, 70000)])
+def test_select_sizes(lp, l_b):
+    cfg = synth.Config("sel", 17, n=l_b * 2, H=2, l_a=8, l_p=lp, hq=2, hk=2, d=64, d_hidden=256)
+    x = synth.host_qkv(cfg, 0, 1)
+    sc = synth.random_scores(cfg, 0, 1, ties=True)
+    idx, send = _select_gpu(cfg, 1, x, sc)
+    idx_or = oracle.select_all_heads(sc.astype(np.float64), cfg.l_p)
+    assert np.array_equal(idx, idx_or)
+    assert np.array_equal(send, oracle.compact(x["k"], x["v"], x["L_A"], idx_or))
+
+
+# ----------------------------------------------------------------------------- whole layer
+
+def _index_sets_ok(idx_gpu, s_or, lp):
+    for j in range(s_or.shape[0]):
+        tau = np.sort(s_or[j])[::-1][lp - 1]
+        diff = set(idx_gpu[j].tolist()) ^ set(oracle.select_topk(s_or[j], lp).tolist())
+        for i in diff:
+            assert abs(s_or[j][i] - tau) < 1e-3, (j, i, s_or[j][i], tau)
+
+
+@pytest.mark.parametrize("name", ["toy", "d128-sink"])
+@pytest.mark.parametrize("overlap", [True, False])
+def test_prefill_layer_end_to_end(name, overlap):
+    """All four steps through PrefillRank (side-stream scoring/select + exchange, LOCAL/PASSING
+    phases), every host of the layer emulated on one GPU."""
+    from paper_2502_12085_b200 import apb
+    from paper_2502_12085_b200.prefill import HostIO, PrefillRank
+    cfg = CASES[name].replace(d_hidden=1024)
+    hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    w = synth.retain_weights(cfg, 0)
+    rank = PrefillRank(dims_of(cfg, 0), list(range(cfg.H)))
+    io = {}
+    for h in range(cfg.H):
+        q = dev(hosts[h]["q"])
+        io[h] = HostIO(q=q, k=dev(hosts[h]["k"]), v=dev(hosts[h]["v"]), out=torch.empty_like(q),
+                       lse=torch.empty((cfg.hq, q.shape[0]), device="cuda"))
+    rank.layer(io, weights_dev(w), overlap=overlap)
+    torch.cuda.synchronize()
+    gathered = to_bits(rank.gathered)
+    for h in range(cfg.H):
+        x = hosts[h]
+        s_or = oracle.retain_score(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
+        idx = rank.indices[h].cpu().numpy()
+        _index_sets_ok(idx, s_or, cfg.l_pp)
+        # selection is bit-exact on the GPU's own scores; compaction is verbatim
+        s_gpu = rank.scores[h].cpu().double().numpy()
+        assert np.array_equal(idx, oracle.select_all_heads(s_gpu, cfg.l_p))
+        assert np.array_equal(gathered[h], oracle.compact(x["k"], x["v"], x["L_A"], idx))
+    for h in range(cfg.H):
+        x = hosts[h]
+        pk, pv = oracle.passing(gathered, h)
+        O_or, lse_or = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv)
+        O = io[h].out.float().cpu().double().numpy()
+        lse = io[h].lse.cpu().double().numpy().T
+        check_attention(O, lse, O_or, lse_or, f"{name} e2e host {h}")
+
+
+def test_attention_determinism():
+    cfg = CASES["toy"]
+    hosts, ref = oracle_layer(cfg)
+    a = run_attention(cfg, 3, hosts[3], ref["gathered"], "split")
+    b = run_attention(cfg, 3, hosts[3], ref["gathered"], "split")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ----------------------------------------------------------------------------- full size
+
+def _sample_rows(L_A, l_b, extra, rng):
+    rows = {0, max(L_A - 1, 0), L_A, L_A + 1, L_A + l_b - 1}
+    for t in range(128, L_A + l_b, 128 * 16):
+        rows.update({t - 1, t, t + 1})
+    rows.update(rng.choice(L_A + l_b, extra, replace=False).tolist())
+    return sorted(r for r in rows if 0 <= r < L_A + l_b)
+
+
+def test_full_size_llama8b_128k_sampled():
+    """BASELINE configs[1] (Llama-3.1-8B-shaped, n = 128K, H = 8, l_a = 4K, l_p = 2K) in the
+    launch configuration bench.py times (PrefillRank, LOCAL/PASSING split, all 8 hosts on one
+    GPU): sampled attention rows of hosts 1, 2 and 8 (critical) vs the oracle, sampled scores,
+    bit-exact selection and gathered buffer."""
+    from paper_2502_12085_b200.prefill import HostIO, PrefillRank
+    cfg = synth.CONFIGS["llama8b-128k"]
+    w = synth.retain_weights(cfg, 0)
+    rank = PrefillRank(dims_of(cfg, 0), list(range(cfg.H)))
+    hosts, io = {}, {}
+    for h in range(cfg.H):
+        hosts[h] = synth.host_qkv(cfg, 0, h)
+        q = dev(hosts[h]["q"])
+        io[h] = HostIO(q=q, k=dev(hosts[h]["k"]), v=dev(hosts[h]["v"]), out=torch.empty_like(q),
+                       lse=torch.empty((cfg.hq, q.shape[0]), device="cuda"))
+    rank.layer(io, weights_dev(w), overlap=True)
+    torch.cuda.synchronize()
+    gathered = to_bits(rank.gathered)
+    rng = np.random.default_rng(0)
+    for h in range(cfg.H):
+        x = hosts[h]
+        idx = rank.indices[h].cpu().numpy()
+        s_gpu = rank.scores[h].cpu().double().numpy()
+        if h in (0, 7):
+            assert np.array_equal(idx, oracle.select_all_heads(s_gpu, cfg.l_p))
+        assert np.array_equal(gathered[h], oracle.compact(x["k"], x["v"], x["L_A"], idx))
+        # sampled scores
+        toks = rng.choice(cfg.l_b, 24, replace=False)
+        L_A = x["L_A"]
+        sub = {k: np.concatenate([x[k][:L_A][:0], x[k][L_A + toks]]) for k in ("q", "k", "v")}
+        s_or = oracle.retain_score(sub["q"], sub["k"], sub["v"], 0, w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
+        floor = np.sqrt((s_gpu ** 2).mean(axis=1, keepdims=True))
+        assert (np.abs(s_gpu[:, toks] - s_or) / np.maximum(np.abs(s_or), floor)).max() <= 1e-2
+    for h in (1, 2, 7):
+        x = hosts[h]
+        rows = _sample_rows(x["L_A"], cfg.l_b, 24, rng)
+        pk, pv = oracle.passing(gathered, h)
+        O_or, lse_or = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv, rows=rows)
+        O = io[h].out[rows].float().cpu().double().numpy()
+        lse = io[h].lse[:, rows].cpu().double().numpy().T
+        check_attention(O, lse, O_or, lse_or, f"L8-128K host {h} sampled ({len(rows)} rows)")

@@ -1,0 +1,99 @@
+"""N > 1 host logic on CPU (gloo, world size 2): host ownership, the in-place slot layout the
+exchange uses (rank r owns slots [r*H/N, (r+1)*H/N) of gathered [H][2][hk][l_p'][d]), the
+128-byte communicator-id broadcast, and that a 2-rank run reproduces the single-process APB
+layer.  The arithmetic here is the oracle's (CPU); the GPU exchange itself (NCCL) is covered
+by the GPU tests / bench."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2502_12085_b200.prefill import hosts_of_rank
+
+
+def test_hosts_of_rank():
+    assert hosts_of_rank(8, 1, 0) == list(range(8))
+    assert hosts_of_rank(8, 2, 1) == [4, 5, 6, 7]
+    assert hosts_of_rank(8, 8, 3) == [3]
+    with pytest.raises(ValueError):
+        hosts_of_rank(8, 3, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cfg():
+    return synth.CONFIGS["toy"].replace(n=512, H=4, l_a=32, l_p=16, d_hidden=32)
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = _cfg()
+    # communicator id: rank 0 draws 128 bytes, everyone receives the same
+    uid = [os.urandom(128) if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ids = [None] * world
+    dist.all_gather_object(ids, uid[0])
+    w = synth.retain_weights(cfg, 0)
+    mine = hosts_of_rank(cfg.H, world, rank)
+    hosts = {h: synth.host_qkv(cfg, 0, h) for h in mine}
+    # steps 1-2 for owned hosts, written into their own slots of a full-size buffer
+    gathered = np.zeros((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d), np.uint16)
+    for h in mine:
+        x = hosts[h]
+        s = oracle.retain_score(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
+        gathered[h] = oracle.compact(x["k"], x["v"], x["L_A"], oracle.select_all_heads(s, cfg.l_p))
+    # step 3: in-place all-gather of contiguous per-rank slot ranges (apb_exchange_passing layout)
+    flat = torch.from_numpy(gathered.view(np.int32)).reshape(world, -1)  # bf16 pairs as int32 (gloo)
+    parts = [torch.empty_like(flat[0]) for _ in range(world)]
+    dist.all_gather(parts, flat[rank].clone())
+    gathered = torch.stack(parts).numpy().view(np.uint16).reshape(gathered.shape)
+    # step 4
+    outs = {}
+    for h in mine:
+        x = hosts[h]
+        pk, pv = oracle.passing(gathered, h)
+        outs[h] = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv)[0]
+    q.put((rank, ids[0] == ids[-1], gathered, outs))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_layer_matches_single_process():
+    cfg = _cfg()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = []
+    for _ in range(world):
+        try:
+            res.append(q.get(timeout=120))
+        except Exception:
+            break
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(res) == world
+    ref = oracle.prefill_layer([synth.host_qkv(cfg, 0, h) for h in range(cfg.H)], synth.retain_weights(cfg, 0),
+                               cfg.l_p)
+    for rank, same_id, gathered, outs in res:
+        assert same_id
+        assert np.array_equal(gathered, ref["gathered"])  # every rank holds [C_1..C_H]
+        for h, O in outs.items():
+            assert np.array_equal(O, ref["O"][h])
