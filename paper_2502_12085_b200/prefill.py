@@ -76,21 +76,34 @@ class PrefillRank:
             apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse, phase=phase,
                               ws=self.ws[h], stream=stream)
 
-    def layer(self, io: dict[int, HostIO], weights: apb.RetainWeights, overlap: bool = True) -> None:
-        """One layer of the hot path for all owned hosts, enqueued on the current stream."""
+    def layer(self, io: dict[int, HostIO], weights: apb.RetainWeights, overlap: bool = True,
+              events: list | None = None) -> None:
+        """One layer of the hot path for all owned hosts, enqueued on the current stream.
+        events: if a list is given, (start, end) timing-event pairs bracketing the attention
+        launches on the main stream are appended to it (the bench's in-situ kernel time)."""
         main = torch.cuda.current_stream(self.device)
+
+        def timed(fn):
+            if events is None:
+                return fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(main)
+            fn()
+            b.record(main)
+            events.append((a, b))
+
         if not overlap:
             self.compress(io, weights, main)
             self.exchange(main)
-            self.attention(io, apb.PHASE_ALL, main)
+            timed(lambda: self.attention(io, apb.PHASE_ALL, main))
             return
         self.side.wait_stream(main)  # this layer's inputs are produced on the main stream
         self.compress(io, weights, self.side)
         self.exchange(self.side)
         self.ev_exchanged.record(self.side)
-        self.attention(io, apb.PHASE_LOCAL, main)
+        timed(lambda: self.attention(io, apb.PHASE_LOCAL, main))
         main.wait_event(self.ev_exchanged)
-        self.attention(io, apb.PHASE_PASSING, main)
+        timed(lambda: self.attention(io, apb.PHASE_PASSING, main))
         # the side stream's buffers (scores, gathered) are reused next layer only after main
         # has consumed them: next layer's side.wait_stream(main) orders that.
 
