@@ -4,6 +4,7 @@
 // thread-local detail string.
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <dlfcn.h>
 #include <mutex>
@@ -203,6 +204,7 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
     p.ws_lse = reinterpret_cast<float*>(static_cast<char*>(ws) + o);
   }
 
+  if (const char* dbg = std::getenv("APB_DEBUG_SKIP")) p.dbg_skip = std::atoi(dbg);  // timing experiments only
   CUtensorMap tq, tk, tv, tg;
   {
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)rows};

@@ -8,11 +8,12 @@
 // fully masked are never visited.
 //
 // CTA = one "work item": two 128-row query tiles of the same KV head (two GQA query heads, same
-// rows) sharing every K/V tile load.  Warp roles (320 threads):
+// rows) sharing every K/V tile load.  Warp roles (384 threads):
 //   warps 0-3  softmax warpgroup for Q tile 0 (thread i owns query row i = TMEM lane i)
 //   warps 4-7  softmax warpgroup for Q tile 1
 //   warp  8    TMA producer (Q once, then a 2-stage K ring and a 2-stage V ring)
-//   warp  9    tcgen05.mma issuer (one thread)
+//   warp  9    tcgen05.mma issuer (one thread);  warps 10-11 idle (complete the 3rd warpgroup
+//              so setmaxnreg can move registers to the softmax warpgroups)
 // TMEM (512 columns): S_0 [0,128)  S_1 [128,256)  O_0 [256,256+D)  O_1 [256+D, 256+2D).
 // P_t (bf16) is written over the first 64 columns of S_t and consumed from TMEM as the A
 // operand of O_t += P_t V (FlashAttention-4 style); S_t(j+1) is issued after PV_t(j), so the
@@ -30,10 +31,45 @@ using namespace apb::sm100;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int KS = 2;  // K and V ring stages
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, {TMA, MMA, 2 idle}
 constexpr int kLoadWarp = 8;
 constexpr int kMmaWarp = 9;
 constexpr float kRescaleThreshold = 8.0f;
+constexpr int kPolyPairs = 6;  // of every 16 column pairs, evaluated with the FMA-pipe polynomial
+
+// 2^x for a pair of fp32 (x <= ~8): clamp at -126 (masked columns give ~0 denormals), split
+// x = j + f with j = rint(x) via the 1.5*2^23 magic constant, 2^f by a degree-3 minimax
+// polynomial on [-0.5, 0.5], then add j to the exponent field with one integer multiply-add.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  using namespace apb::sm100;
+  float x0, x1;
+  f2_unpack(x2, x0, x1);
+  x2 = f2_pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f), nmagic = f2_pack(-12582912.f, -12582912.f);
+  const uint64_t t2 = fadd2(x2, magic);
+  const uint64_t j2 = fadd2(t2, nmagic);
+  const uint64_t f2 = ffma2(j2, f2_pack(-1.f, -1.f), x2);
+  uint64_t p2 = ffma2(f2_pack(0.05517166681468331f, 0.05517166681468331f), f2, f2_pack(0.2426111350945245f, 0.2426111350945245f));
+  p2 = ffma2(p2, f2, f2_pack(0.6932609870112001f, 0.6932609870112001f));
+  p2 = ffma2(p2, f2, f2_pack(0.9999280727914263f, 0.9999280727914263f));
+  float t0, t1, q0, q1;
+  f2_unpack(t2, t0, t1);
+  f2_unpack(p2, q0, q1);
+  const uint32_t r0 = __float_as_uint(t0) * (1u << 23) + __float_as_uint(q0);
+  const uint32_t r1 = __float_as_uint(t1) * (1u << 23) + __float_as_uint(q1);
+  return f2_pack(__uint_as_float(r0), __uint_as_float(r1));
+}
+
+#ifdef APB_TRACE
+// Debug instrumentation (libapb_trace.so only): clock64 stamps of one CTA's pipeline events.
+// [0..): per KV step i < 64: MMA S issue (t), MMA P-half wait done (t, half), softmax S ready (t),
+// softmax P-half published (t, half).
+__device__ unsigned long long g_trace[64 * 32];
+__device__ int g_trace_block = 0;
+#define TRACE(slot, i) do { if (blockIdx.x == g_trace_block && (i) < 64) g_trace[(i) * 32 + (slot)] = clock64(); } while (0)
+#else
+#define TRACE(slot, i) do {} while (0)
+#endif
 
 template <int D>
 struct Layout {
@@ -44,8 +80,8 @@ struct Layout {
   static constexpr int kK = kQ + 2 * kTile;
   static constexpr int kV = kK + KS * kTile;
   static constexpr int kBar = kV + KS * kTile;
-  // barriers: Qfull, Kfull[KS], Kempty[KS], Vfull[KS], Vempty[KS], Sfull[2], Pfull[2], Odone[2]
-  static constexpr int kNumBars = 1 + 4 * KS + 6;
+  // barriers: Qfull, Kfull[KS], Kempty[KS], Vfull[KS], Vempty[KS], Sfull[2], Pfull[2][2 halves], Odone[2]
+  static constexpr int kNumBars = 1 + 4 * KS + 8;
   static constexpr int kTmemPtr = kBar + kNumBars * 8;
   static constexpr int kUsed = kTmemPtr + 16;
   // keep one CTA per SM (each CTA allocates all 512 TMEM columns)
@@ -137,12 +173,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bVf = [&](int s) { return bar0 + 8u * (1 + 2 * KS + s); };
   auto bVe = [&](int s) { return bar0 + 8u * (1 + 3 * KS + s); };
   auto bS = [&](int t) { return bar0 + 8u * (1 + 4 * KS + t); };
-  auto bP = [&](int t) { return bar0 + 8u * (3 + 4 * KS + t); };
-  auto bO = [&](int t) { return bar0 + 8u * (5 + 4 * KS + t); };
+  auto bP = [&](int t, int half) { return bar0 + 8u * (3 + 4 * KS + 2 * t + half); };
+  auto bO = [&](int t) { return bar0 + 8u * (7 + 4 * KS + t); };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtr);
 
-  const int warp = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   const Item it = decode_item(p, blockIdx.x);
 
   if (threadIdx.x == 0) {
@@ -155,115 +190,160 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(bS(t), 1);
-      mbar_init(bP(t), BM);
+      mbar_init(bP(t, 0), BM);
+      mbar_init(bP(t, 1), BM);
       mbar_init(bO(t), 1);
     }
     fence_mbar_init();
   }
   if (warp == kLoadWarp) {
     tmem_alloc<512>(smem_u32(tmem_ptr));
-    if (lane == 0) {
+    if (elect_one()) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_g);
     }
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_ptr;
-
-  if (warp == kLoadWarp) {
-    // ================================================================ TMA producer
-    if (lane == 0) {
+  // TMEM base broadcast from lane 0: provably warp-uniform, so every TMEM address and UMMA
+  // operand below lives in uniform registers (no per-instruction waterfall loops).
+  const uint32_t tmem = warp_uniform(*tmem_ptr);
+  // Register split: the softmax warpgroups hold a 128-wide S row per thread; the producer / MMA
+  // warpgroup needs few registers.  (per SMSP: 2 x 200 + 1 x 104 regs x 32 lanes <= 16384)
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+    if (warp == kLoadWarp) {
+      // ============================================================== TMA producer (warp-converged)
       const int qrow0 = (it.seg == 0 ? 0 : p.L_A) + it.rt * BM;
-      mbar_arrive_expect_tx(bQ, it.ntiles * L::kTile);
-      for (int t = 0; t < it.ntiles; ++t)
-        for (int h = 0; h < L::kHalves; ++h)
-          tma_load_3d(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qh0 + t, qrow0);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(bQ, it.ntiles * L::kTile);
+        for (int t = 0; t < it.ntiles; ++t)
+          for (int h = 0; h < L::kHalves; ++h)
+            tma_load_3d(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qh0 + t, qrow0);
+      }
+      __syncwarp();
       for (int i = 0; i < it.nkv; ++i) {
         const int s = i % KS;
         const uint32_t ph = (i / KS) & 1;
         const KvTile kt = kv_tile(p, it, i);
         const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
         mbar_wait(bKe(s), ph ^ 1);
-        mbar_arrive_expect_tx(bKf(s), L::kTile);
-        for (int h = 0; h < L::kHalves; ++h) {
-          if (kt.kind == 1)
-            tma_load_4d(sK + s * L::kTile + h * L::kSub, &tm_g, bKf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 0);
-          else
-            tma_load_3d(sK + s * L::kTile + h * L::kSub, &tm_k, bKf(s), h * 64, it.j, row0);
+        if (elect_one()) {
+          if ((p.dbg_skip & 1) && i >= KS) {
+            mbar_arrive(bKf(s));
+          } else {
+            mbar_arrive_expect_tx(bKf(s), L::kTile);
+            for (int h = 0; h < L::kHalves; ++h) {
+              if (kt.kind == 1)
+                tma_load_4d(sK + s * L::kTile + h * L::kSub, &tm_g, bKf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 0);
+              else
+                tma_load_3d(sK + s * L::kTile + h * L::kSub, &tm_k, bKf(s), h * 64, it.j, row0);
+            }
+          }
         }
+        __syncwarp();
         mbar_wait(bVe(s), ph ^ 1);
-        mbar_arrive_expect_tx(bVf(s), L::kTile);
-        for (int h = 0; h < L::kHalves; ++h) {
-          if (kt.kind == 1)
-            tma_load_4d(sV + s * L::kTile + h * L::kSub, &tm_g, bVf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 1);
-          else
-            tma_load_3d(sV + s * L::kTile + h * L::kSub, &tm_v, bVf(s), h * 64, it.j, row0);
+        if (elect_one()) {
+          if ((p.dbg_skip & 2) && i >= KS) {
+            mbar_arrive(bVf(s));
+          } else {
+            mbar_arrive_expect_tx(bVf(s), L::kTile);
+            for (int h = 0; h < L::kHalves; ++h) {
+              if (kt.kind == 1)
+                tma_load_4d(sV + s * L::kTile + h * L::kSub, &tm_g, bVf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 1);
+              else
+                tma_load_3d(sV + s * L::kTile + h * L::kSub, &tm_v, bVf(s), h * 64, it.j, row0);
+            }
+          }
         }
+        __syncwarp();
       }
-    }
-  } else if (warp == kMmaWarp) {
-    // ================================================================ MMA issuer
-    if (lane == 0) {
+    } else if (warp == kMmaWarp) {
+      // ============================================================== MMA issuer (warp-converged,
+      // one elected lane issues every tcgen05.mma / tcgen05.commit)
       constexpr uint32_t idS = idesc_bf16_f32(BM, BN, false, false);  // S = Q K^T: both K-major
       constexpr uint32_t idPV = idesc_bf16_f32(BM, D, false, true);   // O += P V: V is MN-major
       auto issue_S = [&](int t, int s) {
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * L::kSub + (k % 4) * 32;
-          mma_ss(tmem + t * 128, sdesc_sw128(sQ + t * L::kTile + off, 16, 1024),
-                 sdesc_sw128(sK + s * L::kTile + off, 16, 1024), idS, k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k / 4) * L::kSub + (k % 4) * 32;
+            mma_ss(tmem + t * 128, sdesc_sw128(sQ + t * L::kTile + off, 16, 1024),
+                   sdesc_sw128(sK + s * L::kTile + off, 16, 1024), idS, k > 0);
+          }
+          mma_commit(bS(t));
         }
+        __syncwarp();
       };
-      auto issue_PV = [&](int t, int s, bool acc) {
+      auto commit = [&](uint32_t bar) {
+        if (elect_one()) mma_commit(bar);
+        __syncwarp();
+      };
+      int trace_i = 0;
+      (void)trace_i;
+      // O_t += P_t V in two K halves: keys [0,64) as soon as the softmax publishes the first half
+      // of P_t, keys [64,128) after the second half.
+      auto issue_PV = [&](int t, int s, bool acc, uint32_t parity) {
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) {
-          mma_ts(tmem + 256 + t * D, tmem + t * 128 + k * 8, sdesc_sw128(sV + s * L::kTile + k * 2048, L::kSub, 1024),
-                 idPV, (acc || k > 0) ? 1u : 0u);
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(bP(t, half), parity);
+          TRACE(2 + 2 * t + half, trace_i);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int k = half * (BN / 32); k < (half + 1) * (BN / 32); ++k) {
+              mma_ts(tmem + 256 + t * D, tmem + t * 128 + k * 8,
+                     sdesc_sw128(sV + s * L::kTile + k * 2048, L::kSub, 1024), idPV, (acc || k > 0) ? 1u : 0u);
+            }
+          }
+          __syncwarp();
         }
       };
       const bool carry = (p.phase == APB_PHASE_PASSING);
       mbar_wait(bQ, 0);
       tc_fence_after();
       for (int i = 0; i < it.nkv; ++i) {
+        trace_i = i;
         const int s = i % KS;
         const uint32_t ph = (i / KS) & 1;
         if (i == 0) {
           mbar_wait(bKf(s), ph);
           tc_fence_after();
           for (int t = 0; t < it.ntiles; ++t) {
+            TRACE(t, 0);
             issue_S(t, s);
-            mma_commit(bS(t));
           }
-          mma_commit(bKe(s));
+          commit(bKe(s));
         }
         mbar_wait(bVf(s), ph);
+        TRACE(12, i);
         tc_fence_after();
         const int s1 = (i + 1) % KS;
         const uint32_t ph1 = ((i + 1) / KS) & 1;
         for (int t = 0; t < it.ntiles; ++t) {
-          mbar_wait(bP(t), i & 1);
-          tc_fence_after();
-          issue_PV(t, s, carry || i > 0);
-          if (t == it.ntiles - 1) mma_commit(bVe(s));
+          issue_PV(t, s, carry || i > 0, i & 1);
+          if (t == it.ntiles - 1) commit(bVe(s));
           if (i + 1 < it.nkv) {
             if (t == 0) {
               mbar_wait(bKf(s1), ph1);
+              TRACE(13, i + 1);
               tc_fence_after();
             }
+            TRACE(t, i + 1);
             issue_S(t, s1);
-            mma_commit(bS(t));
-            if (t == it.ntiles - 1) mma_commit(bKe(s1));
+            if (t == it.ntiles - 1) commit(bKe(s1));
           } else {
-            mma_commit(bO(t));
+            commit(bO(t));
           }
         }
       }
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
     // ================================================================ softmax warpgroups
     const int t = warp / 4;
     if (t < it.ntiles) {
@@ -305,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const KvTile kt = kv_tile(p, it, i);
         const int nv = visible_cols(p, it, kt, row);
         mbar_wait(bS(t), i & 1);
+        if (tid == 0) TRACE(6 + t, i);
         tc_fence_after();
         uint32_t sr[128];
         tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -312,15 +393,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
         tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
         tmem_wait_ld();
+        if (tid == 0) TRACE(24 + t * 4, i);
         float* s = reinterpret_cast<float*>(sr);
         if (nv < BN) {
 #pragma unroll
           for (int c = 0; c < BN; ++c)
             if (c >= nv) s[c] = -INFINITY;
         }
-        float mx = -INFINITY;
+        // row max: 8 independent 3-input max chains, then a short tree
+        float mx8[8];
 #pragma unroll
-        for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
+        for (int q = 0; q < 8; ++q) mx8[q] = fmax3(s[2 * q], s[2 * q + 1], s[16 + 2 * q]);
+#pragma unroll
+        for (int c = 32; c < BN; c += 16) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) mx8[q] = fmax3(mx8[q], s[c + 2 * q], s[c + 2 * q + 1]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], s[16 + 2 * q + 1]);
+        float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
         mx *= sl2;
         const float m_new = fmaxf(m_run, mx);
         const bool grow = (m_new > m_run + kRescaleThreshold) || (m_run == -INFINITY);
@@ -330,36 +421,62 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_run = m_new;
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        float rowsum = 0.f;
+        if (tid == 0) TRACE(25 + t * 4, i);
+        // rescale the running O_t before any PV_t(i) MMA (PV_t(i-1) is complete: S_t(i) was
+        // issued after it).  Rare after the first few key tiles.
+        if (__any_sync(0xffffffffu, grow && o_valid && alpha != 1.f)) {
+          const float a = o_valid ? alpha : 1.f;
+#pragma unroll
+          for (int c = 0; c < D / 16; ++c) {
+            uint32_t r[16];
+            tmem_ld16(tO + c * 16, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * a);
+            tmem_st16(tO + c * 16, r);
+          }
+        }
+        if (tid == 0) TRACE(26 + t * 4, i);
+        // p = 2^(s * scale * log2e - m): packed FFMA2 for the argument; kPolyPairs of every 16
+        // column pairs evaluate 2^x on the FMA pipe (Cody-Waite split + degree-3 polynomial,
+        // rel. error 7.5e-5 << bf16's 3.9e-3), the rest on MUFU.EX2 — balancing the two pipes.
+        const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_use, -m_use);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t pk[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
-            const float p0 = ex2(fmaf(s[half * 64 + 2 * c], sl2, -m_use));
-            const float p1 = ex2(fmaf(s[half * 64 + 2 * c + 1], sl2, -m_use));
-            rowsum += p0 + p1;
+            const int col = half * 64 + 2 * c;
+            const uint64_t x2 = ffma2(f2_pack(s[col], s[col + 1]), sc2, nm2);
+            float p0, p1;
+            uint64_t p2;
+            if ((c % 16) < kPolyPairs) {
+              p2 = exp2_poly2(x2);
+              f2_unpack(p2, p0, p1);
+            } else {
+              float x0, x1;
+              f2_unpack(x2, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+              p2 = f2_pack(p0, p1);
+            }
+            acc2[c & 3] = fadd2(acc2[c & 3], p2);
             pk[c] = pack_bf16x2(p0, p1);
           }
           tmem_st32(tS + half * 32, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bP(t, half));
+          if (tid == 0) TRACE(8 + 2 * t + half, i);
+          if (tid == 96 && half == 0) TRACE(14 + t, i);
+          if ((tid & 31) == 0) TRACE(16 + t * 8 + half * 4 + (tid >> 5), i);
         }
-        l_run = l_run * alpha + rowsum;
-        // rescale the running O_t (PV_t(i-1) is complete: S_t(i) was issued after it)
-        if (__any_sync(0xffffffffu, grow && o_valid && alpha != 1.f)) {
-          const float a = o_valid ? alpha : 1.f;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * a);
-            tmem_st32(tO + c * 32, r);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(bP(t));
+        float r0, r1, r2, r3, r4, r5, r6, r7;
+        f2_unpack(fadd2(acc2[0], acc2[1]), r0, r1);
+        f2_unpack(fadd2(acc2[2], acc2[3]), r2, r3);
+        (void)r4; (void)r5; (void)r6; (void)r7;
+        l_run = l_run * alpha + ((r0 + r1) + (r2 + r3));
         o_valid = true;
       }
 
@@ -435,6 +552,15 @@ static apb_status launch_impl(const AttnParams& p, const CUtensorMap& tq, const 
 }
 
 }  // namespace attn
+
+#ifdef APB_TRACE
+extern "C" int apb_debug_trace(unsigned long long* out, int n, int block) {
+  if (block >= 0) {
+    return cudaMemcpyToSymbol(attn::g_trace_block, &block, sizeof(int)) == cudaSuccess ? 0 : 1;
+  }
+  return cudaMemcpyFromSymbol(out, attn::g_trace, sizeof(unsigned long long) * (n < 2048 ? n : 2048)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream) {

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   float* opart = reinterpret_cast<float*>(smem + kOffO);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   const int m0 = blockIdx.x * TM;
   const int nkb = p.d_in / TK;
   const int nchunks = p.d_hidden / TN;
@@ -74,15 +74,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_ptr;
+  const uint32_t tmem = warp_uniform(*tmem_ptr);  // uniform: UMMA operands stay in uniform registers
 
   if (warp == kLoadWarp) {
-    if (lane == 0) {
-      const int row = p.L_A + m0;
-      for (int c = 0; c < nchunks; ++c) {
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int it = c * nkb + kb, s = it % STAGES;
-          mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
+    // warp-converged producer; one elected lane issues the TMA copies
+    const int row = p.L_A + m0;
+    for (int c = 0; c < nchunks; ++c) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int it = c * nkb + kb, s = it % STAGES;
+        mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(bFull(s), kABytes + kBBytes);
           const uint32_t dA = sbase + kOffA + s * kABytes;
           if (kb < p.kq)
@@ -93,27 +94,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(dA, &tm_v, bFull(s), (kb - p.kq - p.kk) * TK, row);
           tma_load_2d(sbase + kOffB + s * kBBytes, &tm_w1, bFull(s), kb * TK, c * TN);
         }
+        __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(TM, TN, false, false);
-      for (int c = 0; c < nchunks; ++c) {
-        const int b = c & 1;
-        mbar_wait(bAccEmpty(b), ((c >> 1) & 1) ^ 1);
+    // warp-converged MMA issuer; one elected lane issues tcgen05.mma / commit
+    constexpr uint32_t idesc = idesc_bf16_f32(TM, TN, false, false);
+    for (int c = 0; c < nchunks; ++c) {
+      const int b = c & 1;
+      mbar_wait(bAccEmpty(b), ((c >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int it = c * nkb + kb, s = it % STAGES;
+        mbar_wait(bFull(s), (it / STAGES) & 1);
         tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int it = c * nkb + kb, s = it % STAGES;
-          mbar_wait(bFull(s), (it / STAGES) & 1);
-          tc_fence_after();
+        if (elect_one()) {
           const uint32_t aA = sbase + kOffA + s * kABytes, aB = sbase + kOffB + s * kBBytes;
 #pragma unroll
           for (int k = 0; k < TK / 16; ++k)
             mma_ss(tmem + b * TN, sdesc_sw128(aA + k * 32, 16, 1024), sdesc_sw128(aB + k * 32, 16, 1024), idesc,
                    (kb > 0 || k > 0) ? 1u : 0u);
           mma_commit(bEmpty(s));
+          if (kb == nkb - 1) mma_commit(bAccFull(b));
         }
-        mma_commit(bAccFull(b));
+        __syncwarp();
       }
     }
   } else {
