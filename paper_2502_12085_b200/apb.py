@@ -57,7 +57,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("APB_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ApbError(ERR_CUDA, "load", f"{path} not built; run `python -m paper_2502_12085_b200.build`")
     lib = ctypes.CDLL(path)

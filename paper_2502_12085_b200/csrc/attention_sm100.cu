@@ -32,10 +32,13 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int KS = 2;  // K and V ring stages
 constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, {TMA, MMA, 2 idle}
-constexpr int kLoadWarp = 8;
+constexpr int kLoadWarp = 10;  // SMSP 2 (warps 0/4 on SMSP 0 would otherwise share with it)
 constexpr int kMmaWarp = 9;
 constexpr float kRescaleThreshold = 8.0f;
-constexpr int kPolyPairs = 6;  // of every 16 column pairs, evaluated with the FMA-pipe polynomial
+#ifndef APB_POLY_PAIRS
+#define APB_POLY_PAIRS 0
+#endif
+constexpr int kPolyPairs = APB_POLY_PAIRS;  // of every 16 column pairs, evaluated with the FMA-pipe polynomial
 
 // 2^x for a pair of fp32 (x <= ~8): clamp at -126 (masked columns give ~0 denormals), split
 // x = j + f with j = rint(x) via the 1.5*2^23 magic constant, 2^f by a degree-3 minimax
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = (i / KS) & 1;
         const KvTile kt = kv_tile(p, it, i);
         const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
-        mbar_wait(bKe(s), ph ^ 1);
+        mbar_wait_sleep(bKe(s), ph ^ 1);
         if (elect_one()) {
           if ((p.dbg_skip & 1) && i >= KS) {
             mbar_arrive(bKf(s));
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
-        mbar_wait(bVe(s), ph ^ 1);
+        mbar_wait_sleep(bVe(s), ph ^ 1);
         if (elect_one()) {
           if ((p.dbg_skip & 2) && i >= KS) {
             mbar_arrive(bVf(s));
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_PV = [&](int t, int s, bool acc, uint32_t parity) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          mbar_wait(bP(t, half), parity);
+          mbar_wait_sleep(bP(t, half), parity);
           TRACE(2 + 2 * t + half, trace_i);
           tc_fence_after();
           if (elect_one()) {
@@ -304,14 +307,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       const bool carry = (p.phase == APB_PHASE_PASSING);
-      mbar_wait(bQ, 0);
+      mbar_wait_sleep(bQ, 0);
       tc_fence_after();
       for (int i = 0; i < it.nkv; ++i) {
         trace_i = i;
         const int s = i % KS;
         const uint32_t ph = (i / KS) & 1;
         if (i == 0) {
-          mbar_wait(bKf(s), ph);
+          mbar_wait_sleep(bKf(s), ph);
           tc_fence_after();
           for (int t = 0; t < it.ntiles; ++t) {
             TRACE(t, 0);
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           commit(bKe(s));
         }
-        mbar_wait(bVf(s), ph);
+        mbar_wait_sleep(bVf(s), ph);
         TRACE(12, i);
         tc_fence_after();
         const int s1 = (i + 1) % KS;
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (t == it.ntiles - 1) commit(bVe(s));
           if (i + 1 < it.nkv) {
             if (t == 0) {
-              mbar_wait(bKf(s1), ph1);
+              mbar_wait_sleep(bKf(s1), ph1);
               TRACE(13, i + 1);
               tc_fence_after();
             }
@@ -384,7 +387,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < it.nkv; ++i) {
         const KvTile kt = kv_tile(p, it, i);
         const int nv = visible_cols(p, it, kt, row);
+#ifdef APB_SOFTMAX_SLEEP
+        mbar_wait_sleep(bS(t), i & 1);
+#else
         mbar_wait(bS(t), i & 1);
+#endif
         if (tid == 0) TRACE(6 + t, i);
         tc_fence_after();
         uint32_t sr[128];
@@ -393,58 +400,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
         tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
         tmem_wait_ld();
-        if (tid == 0) TRACE(24 + t * 4, i);
         float* s = reinterpret_cast<float*>(sr);
+        if (tid == 0) TRACE(16 + t * 4, i);
         if (nv < BN) {
 #pragma unroll
           for (int c = 0; c < BN; ++c)
             if (c >= nv) s[c] = -INFINITY;
         }
-        // row max: 8 independent 3-input max chains, then a short tree
-        float mx8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmax3(s[2 * q], s[2 * q + 1], s[16 + 2 * q]);
-#pragma unroll
-        for (int c = 32; c < BN; c += 16) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) mx8[q] = fmax3(mx8[q], s[c + 2 * q], s[c + 2 * q + 1]);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], s[16 + 2 * q + 1]);
-        float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        mx *= sl2;
-        const float m_new = fmaxf(m_run, mx);
-        const bool grow = (m_new > m_run + kRescaleThreshold) || (m_run == -INFINITY);
-        float alpha = 1.f;
-        if (grow) {
-          alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
-          m_run = m_new;
-        }
-        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        if (tid == 0) TRACE(25 + t * 4, i);
-        // rescale the running O_t before any PV_t(i) MMA (PV_t(i-1) is complete: S_t(i) was
-        // issued after it).  Rare after the first few key tiles.
-        if (__any_sync(0xffffffffu, grow && o_valid && alpha != 1.f)) {
-          const float a = o_valid ? alpha : 1.f;
-#pragma unroll
-          for (int c = 0; c < D / 16; ++c) {
-            uint32_t r[16];
-            tmem_ld16(tO + c * 16, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * a);
-            tmem_st16(tO + c * 16, r);
-          }
-        }
-        if (tid == 0) TRACE(26 + t * 4, i);
-        // p = 2^(s * scale * log2e - m): packed FFMA2 for the argument; kPolyPairs of every 16
-        // column pairs evaluate 2^x on the FMA pipe (Cody-Waite split + degree-3 polynomial,
+        // 2^(s*scale*log2e - m) for the 64 columns of one half; packed FFMA2 for the argument;
+        // kPolyPairs of every 16 column pairs on the FMA pipe (Cody-Waite + degree-3 polynomial,
         // rel. error 7.5e-5 << bf16's 3.9e-3), the rest on MUFU.EX2 — balancing the two pipes.
-        const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_use, -m_use);
-        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          uint32_t pk[32];
+        auto exp_half = [&](int half, float m_use, uint32_t (&pk)[32], uint64_t (&acc2)[4]) {
+          const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_use, -m_use);
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             const int col = half * 64 + 2 * c;
@@ -464,18 +431,71 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc2[c & 3] = fadd2(acc2[c & 3], p2);
             pk[c] = pack_bf16x2(p0, p1);
           }
-          tmem_st32(tS + half * 32, pk);
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(bP(t, half));
-          if (tid == 0) TRACE(8 + 2 * t + half, i);
-          if (tid == 96 && half == 0) TRACE(14 + t, i);
-          if ((tid & 31) == 0) TRACE(16 + t * 8 + half * 4 + (tid >> 5), i);
+        };
+        // Speculation: the running max m_run only moves when a row max grows by more than the
+        // threshold, so the first half's exponentials are computed against m_run on the
+        // MUFU/FMA pipes while the ALU pipe reduces the new row max; the (rare) rows whose max
+        // grew redo the half with the new max.
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t pk[32];
+        const bool have_m = (m_run != -INFINITY);
+        const float m_spec = have_m ? m_run : 0.f;
+        exp_half(0, m_spec, pk, acc2);
+        float mx8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx8[q] = fmax3(s[2 * q], s[2 * q + 1], s[16 + 2 * q]);
+#pragma unroll
+        for (int c = 32; c < BN; c += 16) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) mx8[q] = fmax3(mx8[q], s[c + 2 * q], s[c + 2 * q + 1]);
         }
-        float r0, r1, r2, r3, r4, r5, r6, r7;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], s[16 + 2 * q + 1]);
+        const float mx = sl2 * fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+        const bool grow = !have_m || (mx > m_run + kRescaleThreshold);
+        float alpha = 1.f;
+        if (tid == 0) TRACE(17 + t * 4, i);
+        if (__any_sync(0xffffffffu, grow)) {
+          if (grow) {
+            const float m_new = fmaxf(m_run, mx);
+            alpha = have_m ? ex2(m_run - m_new) : 0.f;
+            m_run = m_new;
+            const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+            acc2[0] = acc2[1] = acc2[2] = acc2[3] = 0ull;
+            exp_half(0, m_use, pk, acc2);
+          }
+          // rescale the running O_t before any PV_t(i) MMA (PV_t(i-1) is complete: S_t(i) was
+          // issued after it)
+          if (__any_sync(0xffffffffu, grow && o_valid && alpha != 1.f)) {
+            const float a = (grow && o_valid) ? alpha : 1.f;
+#pragma unroll
+            for (int c = 0; c < D / 16; ++c) {
+              uint32_t r[16];
+              tmem_ld16(tO + c * 16, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * a);
+              tmem_st16(tO + c * 16, r);
+            }
+          }
+        }
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        if (tid == 0) TRACE(18 + t * 4, i);
+        tmem_st32(tS, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bP(t, 0));
+        if (tid == 0) TRACE(8 + 2 * t, i);
+        exp_half(1, m_use, pk, acc2);
+        tmem_st32(tS + 32, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bP(t, 1));
+        if (tid == 0) TRACE(9 + 2 * t, i);
+        if ((tid & 31) == 0) TRACE(24 + t * 4 + (tid >> 5), i);
+        float r0, r1, r2, r3;
         f2_unpack(fadd2(acc2[0], acc2[1]), r0, r1);
         f2_unpack(fadd2(acc2[2], acc2[3]), r2, r3);
-        (void)r4; (void)r5; (void)r6; (void)r7;
         l_run = l_run * alpha + ((r0 + r1) + (r2 + r3));
         o_valid = true;
       }

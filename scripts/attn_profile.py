@@ -72,9 +72,8 @@ def main():
         t = np.array(list(buf), dtype=np.int64).reshape(64, 32)
         t0 = t[0, 0]
         names = ["S0iss", "S1iss", "P0h0w", "P0h1w", "P1h0w", "P1h1w", "S0rdy", "S1rdy", "P0h0", "P0h1", "P1h0", "P1h1",
-                 "Vrdy", "Krdy", "P0h0w3", "P1h0w3",
-                 "w0t0h0", "w1t0h0", "w2t0h0", "w3t0h0", "w0t0h1", "w1t0h1", "w2t0h1", "w3t0h1",
-                 "ldS0", "max0", "resc0", "-", "ldS1", "max1", "resc1", "-"]
+                 "Vrdy", "Krdy", "-", "-", "ld0", "max0", "exp0", "st0", "ld1", "max1", "exp1", "st1",
+                 "t0w0", "t0w1", "t0w2", "t0w3", "t1w0", "t1w1", "t1w2", "t1w3"]
         print("step " + " ".join(f"{n:>7s}" for n in names) + "   (clk since S0(0) issue)")
         for i in range(64):
             if t[i, 0] == 0 and i > 0:
