@@ -282,7 +282,7 @@ extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weigh
   {
     uint64_t dims[2] = {(uint64_t)w->d_in, (uint64_t)w->d_hidden};
     uint64_t str[1] = {(uint64_t)w->d_in * 2};
-    uint32_t wbox[2] = {64, 256};
+    uint32_t wbox[2] = {64, 64};  // one quarter of a 256-row W1 tile per CTA of a 4-CTA cluster (multicast)
     if (!make_tmap_bf16(&tw, w->w1, 2, dims, str, wbox)) return APB_ERR_CUDA;
   }
   return launch_retain_score(p, tq, tk, tv, tw, reinterpret_cast<cudaStream_t>(stream));

@@ -35,7 +35,7 @@ struct AttnParams {
   int64_t lse_ld;
   float* ws_o;                // [l_b][hq][D] fp32
   float* ws_lse;              // [hq][l_b] fp32, log2 domain
-  int dbg_skip;               // debug-only (env APB_DEBUG_SKIP): bit0 skip K loads, bit1 skip V loads
+  int dbg_skip;               // debug-only (env APB_DEBUG_SKIP): bit0 skip K loads, bit1 skip V loads, bit2 skip softmax (timing experiments)
 };
 apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream);

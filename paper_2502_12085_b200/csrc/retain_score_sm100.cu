@@ -13,6 +13,9 @@
 // scores are bit-reproducible run to run.
 // Warps 0-7: epilogue (warpgroup w handles columns [128w, 128w+128) of a chunk), warp 8: TMA,
 // warp 9: MMA issuer.
+// Clusters of kCluster CTAs (consecutive token tiles) share every W1 tile: each CTA fetches a
+// 1/kCluster slice and multicasts it to the whole cluster, so W1 crosses L2 once per cluster
+// instead of once per CTA (the kernel is otherwise bound by streaming W1 through L2).
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -28,6 +31,8 @@ constexpr int STAGES = 3;
 constexpr int kThreads = 320;
 constexpr int kLoadWarp = 8, kMmaWarp = 9;
 constexpr int kMaxOut = 64;
+constexpr int kCluster = 4;
+constexpr int kBSlice = TN / kCluster;  // W1 rows each CTA fetches per k block
 
 constexpr int kABytes = TM * TK * 2;  // 16 KB
 constexpr int kBBytes = TN * TK * 2;  // 32 KB
@@ -39,7 +44,7 @@ constexpr int kNumBars = 2 * STAGES + 4;                      // full/empty per 
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmem = kOffTmem + 16 + 1024;
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     retain_score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_w1,
                         const ScoreParams p) {
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(bFull(s), 1);
-      mbar_init(bEmpty(s), 1);
+      mbar_init(bEmpty(s), kCluster);  // a stage is free once every CTA of the cluster consumed it
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bAccFull(b), 1);
@@ -72,8 +77,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == kLoadWarp) tmem_alloc<512>(smem_u32(tmem_ptr));
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barrier inits visible cluster-wide before any multicast arrives
   tc_fence_after();
+  const uint32_t crank = cluster_ctarank();
+  constexpr uint16_t kMask = (1u << kCluster) - 1;
   const uint32_t tmem = warp_uniform(*tmem_ptr);  // uniform: UMMA operands stay in uniform registers
 
   if (warp == kLoadWarp) {
@@ -92,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(dA, &tm_k, bFull(s), (kb - p.kq) * TK, row);
           else
             tma_load_2d(dA, &tm_v, bFull(s), (kb - p.kq - p.kk) * TK, row);
-          tma_load_2d(sbase + kOffB + s * kBBytes, &tm_w1, bFull(s), kb * TK, c * TN);
+          tma_load_2d_mc(sbase + kOffB + s * kBBytes + crank * (kBSlice * 128), &tm_w1, bFull(s), kb * TK,
+                         c * TN + crank * kBSlice, kMask);
         }
         __syncwarp();
       }
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < TK / 16; ++k)
             mma_ss(tmem + b * TN, sdesc_sw128(aA + k * 32, 16, 1024), sdesc_sw128(aB + k * 32, 16, 1024), idesc,
                    (kb > 0 || k > 0) ? 1u : 0u);
-          mma_commit(bEmpty(s));
+          mma_commit_mc(bEmpty(s), kMask);  // frees the stage in every CTA (their loads multicast here)
           if (kb == nkb - 1) mma_commit(bAccFull(b));
         }
         __syncwarp();
@@ -181,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  cluster_sync();  // no CTA exits while a peer may still multicast into / arrive on its smem
 }
 
 }  // namespace score
@@ -194,7 +203,8 @@ apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, cons
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     attr_set = true;
   }
-  const int grid = (p.l_b + score::TM - 1) / score::TM;
+  int grid = (p.l_b + score::TM - 1) / score::TM;
+  grid = (grid + score::kCluster - 1) / score::kCluster * score::kCluster;  // whole clusters
   score::retain_score_kernel<<<grid, score::kThreads, score::kSmem, stream>>>(tq, tk, tv, tw1, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("retain_score launch: ") + cudaGetErrorString(e));
