@@ -9,6 +9,9 @@ Alg. apb_prefill per layer, for every host h this rank owns:
                   wait E -> apb_attention_fwd(h, PASSING)  (local rows over the passing keys,
                                                  merged with the LOCAL partial by LSE)
 
+With a single rank (all hosts on this GPU) the exchange is just the slot layout, so each host
+runs one APB_PHASE_ALL launch as soon as the side stream has compressed hosts < h.
+
 With H hosts over N ranks, rank r owns hosts [r*H/N, (r+1)*H/N) (N = H is the paper's
 deployment, one host per GPU; N < H emulates several hosts per GPU).  Everything numeric runs
 in libapb; this module only allocates buffers and orders launches.
@@ -35,13 +38,17 @@ class HostIO:
 
 class PrefillRank:
     def __init__(self, base: apb.Dims, hosts: list[int], comm: apb.Comm | None = None,
-                 device: torch.device | str = "cuda", skip_unused_last: bool = False):
+                 device: torch.device | str = "cuda", skip_unused_last: bool = False,
+                 split_phases: bool | None = None):
         """base: problem dims (its `host` field is ignored); hosts: host indices this rank owns
         (contiguous, in order).  skip_unused_last: do not score/select host H-1 — its
-        compressed block is ignored by every host, so outputs are unchanged."""
+        compressed block is ignored by every host, so outputs are unchanged.
+        split_phases: LOCAL/PASSING launches around the exchange (default: only when a multi-rank
+        communicator is given; a single rank uses one ordered APB_PHASE_ALL launch per host)."""
         self.base, self.hosts, self.comm = base, list(hosts), comm
         self.device = torch.device(device)
         self.skip_unused_last = skip_unused_last
+        self.split_phases = (comm is not None and comm.nranks > 1) if split_phases is None else split_phases
         b = base
         lpp, hk, hq, d = b.l_pp, b.n_kv_heads, b.n_heads, b.head_dim
         self.gathered = torch.zeros((b.H, 2, hk, lpp, d), dtype=torch.bfloat16, device=self.device)
@@ -51,8 +58,11 @@ class PrefillRank:
         for h in hosts:
             n = apb.workspace_size(b.with_host(h), apb.WS_ATTENTION)
             self.ws[h] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device) if n else None
-        self.side = torch.cuda.Stream(device=self.device)
+        # high priority: the side stream's scoring / selection / NCCL CTAs are scheduled ahead of
+        # the main stream's queued attention CTAs, so the exchange completes while LOCAL runs
+        self.side = torch.cuda.Stream(device=self.device, priority=-1)
         self.ev_exchanged = torch.cuda.Event()
+        self.ev_slot = {h: torch.cuda.Event() for h in hosts}
 
     def dims(self, h: int) -> apb.Dims:
         return self.base.with_host(h)
@@ -96,6 +106,26 @@ class PrefillRank:
             self.compress(io, weights, main)
             self.exchange(main)
             timed(lambda: self.attention(io, apb.PHASE_ALL, main))
+            return
+        if not self.split_phases:
+            # Every host lives on this GPU: the "exchange" is the in-place slot layout itself, so
+            # host h's one-pass attention only has to wait for the compressed blocks of hosts
+            # < h (side stream, one event per host) — no LOCAL/PASSING split, no fp32 partial.
+            self.side.wait_stream(main)
+            for h in self.hosts:
+                if self.base.l_pp > 0 and not (self.skip_unused_last and h == self.base.H - 1):
+                    d, x = self.dims(h), io[h]
+                    apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h], stream=self.side)
+                    apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h], self.gathered[h],
+                                    stream=self.side)
+                self.ev_slot[h].record(self.side)
+            self.exchange(self.side)  # no-op without a communicator
+            for h in self.hosts:
+                if h > self.hosts[0]:
+                    main.wait_event(self.ev_slot[h - 1])
+                x = io[h]
+                timed(lambda: apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse,
+                                                phase=apb.PHASE_ALL, ws=self.ws[h], stream=main))
             return
         self.side.wait_stream(main)  # this layer's inputs are produced on the main stream
         self.compress(io, weights, self.side)

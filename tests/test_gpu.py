@@ -212,22 +212,23 @@ def _index_sets_ok(idx_gpu, s_or, lp):
 
 
 @pytest.mark.parametrize("name", ["toy", "d128-sink"])
-@pytest.mark.parametrize("overlap", [True, False])
-def test_prefill_layer_end_to_end(name, overlap):
-    """All four steps through PrefillRank (side-stream scoring/select + exchange, LOCAL/PASSING
-    phases), every host of the layer emulated on one GPU."""
+@pytest.mark.parametrize("mode", ["ordered", "split", "serial"])
+def test_prefill_layer_end_to_end(name, mode):
+    """All four steps through PrefillRank, every host of the layer emulated on one GPU, in the
+    three schedules: ordered one-pass (single rank), LOCAL/PASSING split around the exchange
+    (the multi-rank schedule), and fully serial."""
     from paper_2502_12085_b200 import apb
     from paper_2502_12085_b200.prefill import HostIO, PrefillRank
     cfg = CASES[name].replace(d_hidden=1024)
     hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
     w = synth.retain_weights(cfg, 0)
-    rank = PrefillRank(dims_of(cfg, 0), list(range(cfg.H)))
+    rank = PrefillRank(dims_of(cfg, 0), list(range(cfg.H)), split_phases=(mode == "split"))
     io = {}
     for h in range(cfg.H):
         q = dev(hosts[h]["q"])
         io[h] = HostIO(q=q, k=dev(hosts[h]["k"]), v=dev(hosts[h]["v"]), out=torch.empty_like(q),
                        lse=torch.empty((cfg.hq, q.shape[0]), device="cuda"))
-    rank.layer(io, weights_dev(w), overlap=overlap)
+    rank.layer(io, weights_dev(w), overlap=(mode != "serial"))
     torch.cuda.synchronize()
     gathered = to_bits(rank.gathered)
     for h in range(cfg.H):
@@ -268,9 +269,10 @@ def _sample_rows(L_A, l_b, extra, rng):
 
 def test_full_size_llama8b_128k_sampled():
     """BASELINE configs[1] (Llama-3.1-8B-shaped, n = 128K, H = 8, l_a = 4K, l_p = 2K) in the
-    launch configuration bench.py times (PrefillRank, LOCAL/PASSING split, all 8 hosts on one
-    GPU): sampled attention rows of hosts 1, 2 and 8 (critical) vs the oracle, sampled scores,
-    bit-exact selection and gathered buffer."""
+    launch configuration bench.py times at N = 1 (PrefillRank, ordered one-pass schedule, all 8
+    hosts on one GPU): sampled attention rows of hosts 2, 3 and 8 (critical) vs the oracle, sampled
+    scores, bit-exact selection and gathered buffer; plus the LOCAL/PASSING launch pair (the N > 1
+    schedule) on the critical host."""
     from paper_2502_12085_b200.prefill import HostIO, PrefillRank
     cfg = synth.CONFIGS["llama8b-128k"]
     w = synth.retain_weights(cfg, 0)
@@ -307,3 +309,15 @@ def test_full_size_llama8b_128k_sampled():
         O = io[h].out[rows].float().cpu().double().numpy()
         lse = io[h].lse[:, rows].cpu().double().numpy().T
         check_attention(O, lse, O_or, lse_or, f"L8-128K host {h} sampled ({len(rows)} rows)")
+        if h == 7:  # the N > 1 schedule: LOCAL launch, then PASSING with the LSE carry-in
+            io[h].out.fill_(float("nan"))
+            from paper_2502_12085_b200 import apb as _apb
+            d = rank.dims(h)
+            _apb.attention_fwd(d, io[h].q, io[h].k, io[h].v, rank.gathered, io[h].out, io[h].lse,
+                               phase=_apb.PHASE_LOCAL, ws=rank.ws[h])
+            _apb.attention_fwd(d, io[h].q, io[h].k, io[h].v, rank.gathered, io[h].out, io[h].lse,
+                               phase=_apb.PHASE_PASSING, ws=rank.ws[h])
+            torch.cuda.synchronize()
+            O = io[h].out[rows].float().cpu().double().numpy()
+            lse = io[h].lse[:, rows].cpu().double().numpy().T
+            check_attention(O, lse, O_or, lse_or, f"L8-128K host {h} LOCAL+PASSING sampled")
