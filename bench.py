@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--schedule", choices=["auto", "split", "ordered"], default="auto",
+                    help="auto: LOCAL/PASSING split around the exchange only when N > 1")
+    ap.add_argument("--same-device", action="store_true",
+                    help="debug: every rank uses cuda:0 (multi-rank logic on a single GPU)")
     return ap.parse_args()
 
 
@@ -215,11 +219,16 @@ def main():
     from paper_2502_12085_b200 import apb
     from paper_2502_12085_b200.prefill import HostIO, PrefillRank, hosts_of_rank
 
+    if args.same_device:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if args.same_device:  # NCCL refuses two ranks on one GPU: plumbing-only test mode
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS[args.config]
     H = args.hosts or cfg.H
     layers = args.layers or cfg.layers
@@ -227,11 +236,14 @@ def main():
                     head_dim=cfg.d, l_q=cfg.l_q)
     hosts = hosts_of_rank(H, world, rank)
     comm = None
-    if world > 1:
+    if world > 1 and not args.same_device:
         uid = [apb.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = apb.Comm(uid[0], world, rank)
-    pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True)
+    split = None if args.schedule == "auto" else (args.schedule == "split")
+    if args.same_device and world > 1 and split is None:
+        split = True  # the multi-rank schedule (the exchange itself is skipped in this mode)
+    pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True, split_phases=split)
 
     # ---- synthetic inputs: D1 N(0,1) Q/K/V (the paper's timing input is synthetic random
     # input), two alternating layer buffer sets, random-init retaining heads.
@@ -272,7 +284,7 @@ def main():
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            dist.barrier() if args.same_device else dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -293,9 +305,9 @@ def main():
     ms = ev0.elapsed_time(ev1)
     attn_ms = sum(a.elapsed_time(b) for a, b in attn_events)
     if world > 1:
-        t = torch.tensor([ms, attn_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, attn_ms_max = t.tolist()
+        t = torch.tensor([ms], device="cpu" if args.same_device else dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # the step time is the slowest rank's
+        ms = t.item()
     ms_per_step = ms / args.steps
     value = cfg.n * args.steps / (ms / 1e3)
 
@@ -393,7 +405,7 @@ def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank,
     barrier()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if args.same_device else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
     return {"value": cfg.n * args.e2e_steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_layer * layers,

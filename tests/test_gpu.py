@@ -321,3 +321,16 @@ def test_full_size_llama8b_128k_sampled():
             O = io[h].out[rows].float().cpu().double().numpy()
             lse = io[h].lse[:, rows].cpu().double().numpy().T
             check_attention(O, lse, O_or, lse_or, f"L8-128K host {h} LOCAL+PASSING sampled")
+
+
+def test_nccl_unique_id_and_single_rank_comm():
+    """libapb's NCCL plumbing on a GPU box: a 128-byte id, a 1-rank communicator (exchange is a
+    no-op), and a clean destroy."""
+    from paper_2502_12085_b200 import apb
+    uid = apb.Comm.unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
+    c = apb.Comm(uid, 1, 0)
+    cfg = CASES["toy"]
+    g = torch.zeros((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d), dtype=torch.bfloat16, device="cuda")
+    apb.exchange_passing(c, dims_of(cfg, 0), g)
+    c.close()
