@@ -222,11 +222,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == kLoadWarp) {
       // ============================================================== TMA producer (warp-converged)
       const int qrow0 = (it.seg == 0 ? 0 : p.L_A) + it.rt * BM;
+#ifndef APB_NO_L2_HINTS
+      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+#define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d_hint(dst, map, bar, a, b, c, pol_kv)
+#define KV_LOAD4(dst, map, bar, a, b, c, d) tma_load_4d_hint(dst, map, bar, a, b, c, d, pol_kv)
+#else
+#define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d(dst, map, bar, a, b, c)
+#define KV_LOAD4(dst, map, bar, a, b, c, d) tma_load_4d(dst, map, bar, a, b, c, d)
+#endif
       if (elect_one()) {
         mbar_arrive_expect_tx(bQ, it.ntiles * L::kTile);
         for (int t = 0; t < it.ntiles; ++t)
           for (int h = 0; h < L::kHalves; ++h)
+#ifndef APB_NO_L2_HINTS
+            tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qh0 + t, qrow0, pol_q);
+#else
             tma_load_3d(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qh0 + t, qrow0);
+#endif
       }
       __syncwarp();
       for (int i = 0; i < it.nkv; ++i) {
@@ -242,9 +254,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(bKf(s), L::kTile);
             for (int h = 0; h < L::kHalves; ++h) {
               if (kt.kind == 1)
-                tma_load_4d(sK + s * L::kTile + h * L::kSub, &tm_g, bKf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 0);
+                KV_LOAD4(sK + s * L::kTile + h * L::kSub, &tm_g, bKf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 0);
               else
-                tma_load_3d(sK + s * L::kTile + h * L::kSub, &tm_k, bKf(s), h * 64, it.j, row0);
+                KV_LOAD3(sK + s * L::kTile + h * L::kSub, &tm_k, bKf(s), h * 64, it.j, row0);
             }
           }
         }
@@ -257,9 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(bVf(s), L::kTile);
             for (int h = 0; h < L::kHalves; ++h) {
               if (kt.kind == 1)
-                tma_load_4d(sV + s * L::kTile + h * L::kSub, &tm_g, bVf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 1);
+                KV_LOAD4(sV + s * L::kTile + h * L::kSub, &tm_g, bVf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 1);
               else
-                tma_load_3d(sV + s * L::kTile + h * L::kSub, &tm_v, bVf(s), h * 64, it.j, row0);
+                KV_LOAD3(sV + s * L::kTile + h * L::kSub, &tm_v, bVf(s), h * 64, it.j, row0);
             }
           }
         }
@@ -435,8 +447,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               float x0, x1;
               f2_unpack(x2, x0, x1);
+#ifdef APB_DEBUG_NO_MUFU
+              p0 = x0 * 1e-30f;  // timing experiment only: no MUFU
+              p1 = x1 * 1e-30f;
+#else
               p0 = ex2(x0);
               p1 = ex2(x1);
+#endif
               p2 = f2_pack(p0, p1);
             }
             acc2[c & 3] = fadd2(acc2[c & 3], p2);
