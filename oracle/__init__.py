@@ -60,7 +60,11 @@ def _load():
             lib.oracle_select_topk.argtypes = [i64, i64, dp, ip]
             lib.oracle_attention.argtypes = [i64, i64, i64, i32, i32, i32, ctypes.c_double,
                                              dp, dp, dp, i64, lp, dp, dp]
-            for f in (lib.oracle_retain_score, lib.oracle_select_topk, lib.oracle_attention):
+            lib.oracle_decode_partial.argtypes = [i64, i64, i32, i32, i32, ctypes.c_double,
+                                                  dp, dp, dp, dp, dp, dp, dp]
+            lib.oracle_merge_score.argtypes = [i32, i64, i32, dp, dp, dp, dp]
+            for f in (lib.oracle_retain_score, lib.oracle_select_topk, lib.oracle_attention,
+                      lib.oracle_decode_partial, lib.oracle_merge_score):
                 f.restype = ctypes.c_int
             lib.oracle_num_threads.restype = ctypes.c_int
             _lib = lib
@@ -189,6 +193,57 @@ def attention(q, k, v, L_A: int, pk, pv, scale: float | None = None, rows=None):
     if rc:
         raise ValueError(f"oracle_attention rc={rc}")
     return O, lse
+
+
+# ----------------------------------------------------------------------------- decode (NEXT #1)
+
+def decode_partial(q, k_cache, v_cache, k_new=None, v_new=None, scale: float | None = None):
+    """Alg. apb_decode lines attnl / attnh: host h's partial attention of the t new
+    tokens over its block cache, plus (last host only) the new tokens' own keys, causally.
+    q: [t][hq][d]; k/v_cache: [c][hk][d]; k/v_new: [t][hk][d] or None.
+    Returns (A_h [t][hq][d] fp64, lse_h [t][hq] fp64, natural log)."""
+    q = np.ascontiguousarray(_as_f64(q))
+    kc, vc = np.ascontiguousarray(_as_f64(k_cache)), np.ascontiguousarray(_as_f64(v_cache))
+    kn = None if k_new is None else np.ascontiguousarray(_as_f64(k_new))
+    vn = None if v_new is None else np.ascontiguousarray(_as_f64(v_new))
+    t, hq, d = q.shape
+    c, hk = kc.shape[0], kc.shape[1]
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    O = np.empty((t, hq, d), np.float64)
+    lse = np.empty((t, hq), np.float64)
+    rc = _load().oracle_decode_partial(t, c, hq, hk, d, float(scale), _p(q), _p(kc), _p(vc), _p(kn), _p(vn),
+                                       _p(O), _p(lse))
+    if rc:
+        raise ValueError(f"oracle_decode_partial rc={rc}")
+    return O, lse
+
+
+def merge_score(parts_o, parts_lse):
+    """MergeScore: merge partial attentions by their log-sum-exp.
+    parts_o: [n][rows...][d], parts_lse: [n][rows...].  Returns (A [rows...][d], L [rows...])."""
+    po = np.ascontiguousarray(parts_o, dtype=np.float64)
+    pl = np.ascontiguousarray(parts_lse, dtype=np.float64)
+    n, d = po.shape[0], po.shape[-1]
+    rows = int(np.prod(po.shape[1:-1]))
+    out = np.empty(po.shape[1:], np.float64)
+    out_lse = np.empty(pl.shape[1:], np.float64)
+    rc = _load().oracle_merge_score(n, rows, d, _p(po), _p(pl), _p(out), _p(out_lse))
+    if rc:
+        raise ValueError(f"oracle_merge_score rc={rc}")
+    return out, out_lse
+
+
+def decode_step(q, caches, k_new, v_new, scale: float | None = None):
+    """One Accu attention (Alg. apb_decode) over H hosts: per-host partials (the last
+    host includes the new tokens' keys), Gather, MergeScore.  caches: list of (k_cache, v_cache)
+    in host order.  Returns (A [t][hq][d], L [t][hq], partials list)."""
+    parts = []
+    for h, (kc, vc) in enumerate(caches):
+        last = h == len(caches) - 1
+        parts.append(decode_partial(q, kc, vc, k_new if last else None, v_new if last else None, scale))
+    A, L = merge_score(np.stack([p[0] for p in parts]), np.stack([p[1] for p in parts]))
+    return A, L, parts
 
 
 # ----------------------------------------------------------------------------- pipeline

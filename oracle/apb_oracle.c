@@ -184,3 +184,87 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------ decode (NEXT #1) */
+/* Alg. apb_decode: the t new tokens' queries attend on host h to its block KV cache
+ * (P:745-746); the last host also attends to the new tokens' own keys, causally among
+ * them (new token s sees new tokens 0..s).  Returns the host's partial attention A_h and lse_h.
+ * Q: [t][hq][d]; Kc, Vc: [c][hk][d]; Kn, Vn: [t][hk][d] or NULL (hosts other than the last).
+ * O: [t][hq][d]; lse: [t][hq] (natural log; -inf when a row sees no key).                    */
+int oracle_decode_partial(int64_t t, int64_t c, int32_t hq, int32_t hk, int32_t d, double scale,
+                          const double* Q, const double* Kc, const double* Vc, const double* Kn,
+                          const double* Vn, double* O, double* lse) {
+    if (t < 0 || c < 0 || hq <= 0 || hk <= 0 || hq % hk || d <= 0) return 1;
+    const int32_t g = hq / hk;
+    const int64_t nmax = c + t;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+    for (int64_t s = 0; s < t; ++s) {
+        for (int32_t qh = 0; qh < hq; ++qh) {
+            const int32_t j = qh / g;
+            const double* q = Q + (s * hq + qh) * (int64_t)d;
+            double* logit = (double*)malloc(sizeof(double) * (size_t)(nmax > 0 ? nmax : 1));
+            const double** vrow = (const double**)malloc(sizeof(double*) * (size_t)(nmax > 0 ? nmax : 1));
+            int64_t n = 0;
+            for (int64_t k = 0; k < c; ++k) {            /* every cached key precedes the new tokens */
+                const double* kk = Kc + (k * hk + j) * (int64_t)d;
+                double dot = 0.0;
+                for (int32_t e = 0; e < d; ++e) dot += q[e] * kk[e];
+                logit[n] = scale * dot;
+                vrow[n++] = Vc + (k * hk + j) * (int64_t)d;
+            }
+            if (Kn) {
+                for (int64_t k = 0; k <= s; ++k) {       /* new tokens: causal among themselves */
+                    const double* kk = Kn + (k * hk + j) * (int64_t)d;
+                    double dot = 0.0;
+                    for (int32_t e = 0; e < d; ++e) dot += q[e] * kk[e];
+                    logit[n] = scale * dot;
+                    vrow[n++] = Vn + (k * hk + j) * (int64_t)d;
+                }
+            }
+            double* o = O + (s * hq + qh) * (int64_t)d;
+            for (int32_t e = 0; e < d; ++e) o[e] = 0.0;
+            if (n == 0) {
+                lse[s * hq + qh] = -INFINITY;
+            } else {
+                double m = -INFINITY;
+                for (int64_t k = 0; k < n; ++k) if (logit[k] > m) m = logit[k];
+                double Z = 0.0;
+                for (int64_t k = 0; k < n; ++k) {
+                    double w = exp(logit[k] - m);
+                    Z += w;
+                    for (int32_t e = 0; e < d; ++e) o[e] += w * vrow[k][e];
+                }
+                for (int32_t e = 0; e < d; ++e) o[e] /= Z;
+                lse[s * hq + qh] = m + log(Z);
+            }
+            free(logit);
+            free(vrow);
+        }
+    }
+    return 0;
+}
+
+/* MergeScore: A = sum_h A_h exp(lse_h - L), L = log sum_h exp(lse_h).
+ * parts_o: [n][rows][d], parts_lse: [n][rows]; out: [rows][d], out_lse: [rows].              */
+int oracle_merge_score(int32_t n, int64_t rows, int32_t d, const double* parts_o, const double* parts_lse,
+                       double* out, double* out_lse) {
+    if (n <= 0 || rows < 0 || d <= 0) return 1;
+    for (int64_t r = 0; r < rows; ++r) {
+        double m = -INFINITY;
+        for (int32_t h = 0; h < n; ++h) if (parts_lse[h * rows + r] > m) m = parts_lse[h * rows + r];
+        double Z = 0.0;
+        for (int32_t h = 0; h < n; ++h)
+            if (parts_lse[h * rows + r] > -INFINITY) Z += exp(parts_lse[h * rows + r] - m);
+        const double L = (m == -INFINITY) ? -INFINITY : m + log(Z);
+        out_lse[r] = L;
+        for (int32_t e = 0; e < d; ++e) {
+            double acc = 0.0;
+            for (int32_t h = 0; h < n; ++h) {
+                const double l = parts_lse[h * rows + r];
+                if (l > -INFINITY) acc += parts_o[(h * rows + r) * (int64_t)d + e] * exp(l - L);
+            }
+            out[r * (int64_t)d + e] = acc;
+        }
+    }
+    return 0;
+}

@@ -397,3 +397,67 @@ def test_synth_bf16_rounding():
     back = synth.bf16_bits_to_f32(b)
     assert back[0] == 1.0 and back[1] == 1.0  # tie -> even
     assert back[2] == 1.0078125 and back[3] == -2.5
+
+
+# ----------------------------------------------------------------------------- decode (NEXT #1)
+
+def _sdpa_new_over_caches(q, caches, k_new, v_new, scale):
+    """torch fp64 SDPA: the t new rows attend to every cached key (in host order) and causally
+    to the new keys — single-host exact attention (SPEC S:413 'equals single-host ... decoding')."""
+    hq, hk = q.shape[1], k_new.shape[1]
+    K = np.concatenate([c[0] for c in caches] + [k_new])
+    V = np.concatenate([c[1] for c in caches] + [v_new])
+    t, nk = q.shape[0], K.shape[0]
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).permute(1, 0, 2)
+    m = torch.ones(t, nk, dtype=torch.bool).tril(diagonal=nk - t)
+    Kt = T(K).repeat_interleave(hq // hk, 0)
+    Vt = T(V).repeat_interleave(hq // hk, 0)
+    O = torch.nn.functional.scaled_dot_product_attention(T(q), Kt, Vt, attn_mask=m, scale=scale)
+    lse = torch.logsumexp((T(q) @ Kt.transpose(1, 2) * scale).masked_fill(~m, -math.inf), -1)
+    return O.permute(1, 0, 2).numpy(), lse.T.numpy()
+
+
+@pytest.mark.parametrize("H,t,c", [(1, 1, 37), (4, 1, 50), (4, 5, 33), (3, 3, 0), (2, 8, 129)])
+def test_decode_step_equals_exact_attention(H, t, c):
+    """Alg. apb_decode is exact: MergeScore of the per-host partials (last host with
+    the new tokens' own keys) == one-shot attention over [B_1 .. B_H | new]."""
+    hq, hk, d = 4, 2, 16
+    rng = np.random.default_rng(H * 100 + t)
+    caches = [(rng.standard_normal((c, hk, d)) * 1.5, rng.standard_normal((c, hk, d))) for _ in range(H)]
+    q = rng.standard_normal((t, hq, d)) * 1.5
+    kn, vn = rng.standard_normal((t, hk, d)) * 1.5, rng.standard_normal((t, hk, d))
+    A, L, parts = oracle.decode_step(q, caches, kn, vn)
+    ref, ref_lse = _sdpa_new_over_caches(q, caches, kn, vn, 1 / math.sqrt(d))
+    assert np.allclose(A, ref, atol=1e-12) and np.allclose(L, ref_lse, atol=1e-12)
+    # every host's partial is itself exact attention over that host's keys
+    for h, (O_h, l_h) in enumerate(parts):
+        last = h == H - 1
+        ks = [caches[h]] if c else []
+        if last:
+            r, rl = _sdpa_new_over_caches(q, ks, kn, vn, 1 / math.sqrt(d))
+            assert np.allclose(O_h, r, atol=1e-12) and np.allclose(l_h, rl, atol=1e-12)
+        elif c:
+            Kc, Vc = caches[h]
+            T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).permute(1, 0, 2)
+            r = torch.nn.functional.scaled_dot_product_attention(
+                T(q), T(Kc).repeat_interleave(2, 0), T(Vc).repeat_interleave(2, 0), scale=1 / math.sqrt(d))
+            assert np.allclose(O_h, r.permute(1, 0, 2).numpy(), atol=1e-12)
+        else:
+            assert np.all(np.isneginf(l_h)) and np.all(O_h == 0)
+
+
+def test_merge_score_spec_examples():
+    """single part = identity; two identical parts = same vector; two disjoint key
+    halves of an 8-key attention == attention over all 8 keys."""
+    rng = np.random.default_rng(7)
+    o, l = rng.standard_normal((1, 3, 5)), rng.standard_normal((1, 3))
+    A, L = oracle.merge_score(o, l)
+    assert np.array_equal(A, o[0]) and np.array_equal(L, l[0])
+    A, L = oracle.merge_score(np.concatenate([o, o]), np.concatenate([l, l]))
+    assert np.allclose(A, o[0], atol=1e-15) and np.allclose(L, l[0] + math.log(2), atol=1e-15)
+    q = rng.standard_normal((1, 1, 4)); k = rng.standard_normal((8, 1, 4)); v = rng.standard_normal((8, 1, 4))
+    full, full_l = oracle.decode_partial(q, k, v)
+    a1, l1 = oracle.decode_partial(q, k[:3], v[:3])
+    a2, l2 = oracle.decode_partial(q, k[3:], v[3:])
+    A, L = oracle.merge_score(np.stack([a1, a2]), np.stack([l1, l2]))
+    assert np.allclose(A, full, atol=1e-14) and np.allclose(L, full_l, atol=1e-14)
