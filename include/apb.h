@@ -150,6 +150,47 @@ apb_status apb_attention_fwd(const apb_dims* dims, const void* q, const void* k,
                              void* out, int64_t out_row_stride, float* lse, apb_phase phase,
                              void* ws, size_t ws_bytes, apb_stream_t stream);
 
+/* ---------------------------------------------------------------- decode step
+ * Alg. apb_decode ("Accu"): after prefill every host holds its block's KV cache
+ * (P:675-678).  For t new tokens (t = 1 when generating; the whole query chunk on the first
+ * decoding iteration) host h computes a partial attention of their queries over its cache
+ * (P:745-746); the last host (host == H-1) also attends to the new tokens' own keys, causally
+ * among them.  The partials are gathered and merged by log-sum-exp
+ * (MergeScore) — exact attention over [B_1 .. B_H | new tokens].
+ *  cache_len      rows of this host's cache (K/V: [cache_len][n_kv_heads][head_dim], row stride
+ *                 cache_row_stride elements, multiple of 8; may be 0)
+ *  t_new          new tokens; t_new * (n_heads / n_kv_heads) must be <= 64 (else
+ *                 APB_ERR_UNSUPPORTED: chunk the query)                                       */
+typedef struct {
+    int32_t H, host, t_new;
+    int64_t cache_len;
+    int32_t n_heads, n_kv_heads, head_dim;
+    float softmax_scale;  /* <= 0 selects 1/sqrt(head_dim) */
+} apb_decode_dims;
+
+/* Partial attention of host `host`: q bf16 [t_new][n_heads][head_dim]; k_new/v_new bf16
+ * [t_new][n_kv_heads][head_dim] (row stride new_row_stride; read only when host == H-1, may be
+ * NULL otherwise).  Writes part_o fp32 [t_new][n_heads][head_dim] (normalised) and part_lse fp32
+ * [t_new][n_heads] (natural log; -inf for a row that sees no key).  ws: apb_decode_workspace_size.
+ * Kernel: split-KV over 256-key chunks x KV heads (memory-bound), then an LSE fold of the chunks. */
+apb_status apb_decode_attention(const apb_decode_dims* dims, const void* q, const void* k_cache,
+                                const void* v_cache, int64_t cache_row_stride, const void* k_new,
+                                const void* v_new, int64_t new_row_stride, float* part_o,
+                                float* part_lse, void* ws, size_t ws_bytes, apb_stream_t stream);
+apb_status apb_decode_workspace_size(const apb_decode_dims* dims, size_t* bytes);
+
+/* MergeScore: out[r] = sum_h parts_o[h][r] * exp(parts_lse[h][r] - L[r]),
+ * L[r] = log sum_h exp(parts_lse[h][r]).  parts_o fp32 with part stride part_stride_o floats
+ * (rows x head_dim each), parts_lse fp32 with part stride part_stride_lse; out bf16 [rows][head_dim];
+ * out_lse fp32 [rows] or NULL.  Deterministic (fixed host order).                            */
+apb_status apb_merge_partials(int32_t n_parts, int64_t rows, int32_t head_dim, const float* parts_o,
+                              int64_t part_stride_o, const float* parts_lse, int64_t part_stride_lse,
+                              void* out, float* out_lse, apb_stream_t stream);
+
+/* Gather of the partials: in-place AllGather of fp32 buffer [nranks][count_per_rank]
+ * (rank r owns block r).  No-op for comm == NULL or a 1-rank comm.                             */
+apb_status apb_exchange_partials(apb_comm* comm, int64_t count_per_rank, float* buf, apb_stream_t stream);
+
 /* ---------------------------------------------------------------- plumbing */
 apb_status apb_workspace_size(const apb_dims* dims, apb_ws_kind which, size_t* bytes);
 /* Validates dims alone (APB_ERR_CONFIG / APB_ERR_UNSUPPORTED) without touching a GPU. */

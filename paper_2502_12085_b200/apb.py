@@ -27,7 +27,8 @@ WS_RETAIN, WS_SELECT, WS_ATTENTION = 0, 1, 2
 
 EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
             "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
-            "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count")
+            "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count",
+            "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials")
 
 
 class ApbError(RuntimeError):
@@ -40,6 +41,12 @@ class _Dims(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("H", ctypes.c_int32), ("host", ctypes.c_int32),
                 ("l_q", ctypes.c_int32), ("l_a", ctypes.c_int32), ("l_b", ctypes.c_int32),
                 ("l_p", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
+
+
+class _DecodeDims(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int32), ("host", ctypes.c_int32), ("t_new", ctypes.c_int32),
+                ("cache_len", ctypes.c_int64), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
 
 
@@ -72,9 +79,15 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_comm_destroy.argtypes = [vp]
     lib.apb_workspace_size.argtypes = [dp, ctypes.c_int, ctypes.POINTER(sz)]
     lib.apb_check_dims.argtypes = [dp]
+    ddp = ctypes.POINTER(_DecodeDims)
+    lib.apb_decode_attention.argtypes = [ddp, vp, vp, vp, i64, vp, vp, i64, vp, vp, vp, sz, vp]
+    lib.apb_decode_workspace_size.argtypes = [ddp, ctypes.POINTER(sz)]
+    lib.apb_merge_partials.argtypes = [i32, i64, i32, vp, i64, vp, i64, vp, vp, vp]
+    lib.apb_exchange_partials.argtypes = [vp, i64, vp, vp]
     for f in ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
-              "apb_check_dims"):
+              "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
+              "apb_exchange_partials"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -252,3 +265,55 @@ def launch_count() -> int:
 
 def version() -> int:
     return int(load().apb_version())
+
+
+# ----------------------------------------------------------------------------- decode step (NEXT #1)
+
+@dataclasses.dataclass
+class DecodeDims:
+    """apb_decode_dims: one host's decode step (Alg. apb_decode)."""
+    H: int
+    host: int
+    t_new: int
+    cache_len: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    softmax_scale: float = 0.0
+
+    def c(self) -> _DecodeDims:
+        return _DecodeDims(self.H, self.host, self.t_new, self.cache_len, self.n_heads, self.n_kv_heads,
+                           self.head_dim, self.softmax_scale)
+
+
+def decode_workspace_size(dims: DecodeDims) -> int:
+    out = ctypes.c_size_t(0)
+    d = dims.c()
+    _check(load().apb_decode_workspace_size(ctypes.byref(d), ctypes.byref(out)), "apb_decode_workspace_size")
+    return out.value
+
+
+def decode_attention(dims: DecodeDims, q, k_cache, v_cache, k_new, v_new, part_o, part_lse, ws=None,
+                     stream=None) -> None:
+    """Host partial (A_h, lse_h) of the new tokens."""
+    d = dims.c()
+    cs = _rowstride(k_cache, "k_cache") if k_cache is not None and k_cache.numel() else 0
+    ns = _rowstride(k_new, "k_new") if k_new is not None else 0
+    _check(load().apb_decode_attention(ctypes.byref(d), q.data_ptr(), _ptr(k_cache), _ptr(v_cache), cs,
+                                       _ptr(k_new), _ptr(v_new), ns, part_o.data_ptr(), part_lse.data_ptr(),
+                                       _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                                       _stream(stream)), "apb_decode_attention")
+
+
+def merge_partials(n_parts: int, rows: int, head_dim: int, parts_o, stride_o: int, parts_lse, stride_lse: int,
+                   out, out_lse=None, stream=None) -> None:
+    """MergeScore of n_parts partials (fp32) into bf16 out [rows][head_dim]."""
+    _check(load().apb_merge_partials(n_parts, rows, head_dim, parts_o.data_ptr(), stride_o, parts_lse.data_ptr(),
+                                     stride_lse, out.data_ptr(), _ptr(out_lse), _stream(stream)),
+           "apb_merge_partials")
+
+
+def exchange_partials(comm: "Comm | None", count_per_rank: int, buf, stream=None) -> None:
+    """Gather: in-place AllGather of fp32 [nranks][count_per_rank]."""
+    _check(load().apb_exchange_partials(comm.handle if comm is not None else None, count_per_rank,
+                                        buf.data_ptr(), _stream(stream)), "apb_exchange_partials")

@@ -412,3 +412,95 @@ extern "C" apb_status apb_exchange_passing(apb_comm* c, const apb_dims* d, void*
   if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather");
   return APB_OK;
 }
+
+// ---------------------------------------------------------------- decode step (NEXT #1)
+static apb_status check_decode_dims(const apb_decode_dims* d) {
+  if (!d) return fail(APB_ERR_CONTRACT, "dims is NULL");
+  if (d->H < 1 || d->host < 0 || d->host >= d->H) return fail(APB_ERR_CONFIG, "host must be in [0, H)");
+  if (d->t_new < 1 || d->cache_len < 0) return fail(APB_ERR_CONFIG, "t_new >= 1 and cache_len >= 0 required");
+  if (d->n_heads < 1 || d->n_kv_heads < 1 || d->n_heads % d->n_kv_heads)
+    return fail(APB_ERR_CONFIG, "n_heads must be a positive multiple of n_kv_heads");
+  if (d->head_dim != 64 && d->head_dim != 128) return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if ((int64_t)d->t_new * (d->n_heads / d->n_kv_heads) > kDecodeRowsMax)
+    return fail(APB_ERR_UNSUPPORTED, "t_new * (n_heads / n_kv_heads) must be <= 64: chunk the new tokens");
+  return APB_OK;
+}
+
+static int64_t decode_keys(const apb_decode_dims* d) {
+  return d->cache_len + (d->host == d->H - 1 ? d->t_new : 0);
+}
+
+extern "C" apb_status apb_decode_workspace_size(const apb_decode_dims* d, size_t* bytes) {
+  if (!bytes) return fail(APB_ERR_CONTRACT, "bytes is NULL");
+  apb_status st = check_decode_dims(d);
+  if (st) return st;
+  *bytes = decode_workspace_bytes(decode_keys(d), d->t_new, d->n_heads, d->head_dim);
+  return APB_OK;
+}
+
+extern "C" apb_status apb_decode_attention(const apb_decode_dims* d, const void* q, const void* k_cache,
+                                           const void* v_cache, int64_t cache_row_stride, const void* k_new,
+                                           const void* v_new, int64_t new_row_stride, float* part_o, float* part_lse,
+                                           void* ws, size_t ws_bytes, apb_stream_t stream) {
+  apb_status st = check_decode_dims(d);
+  if (st) return st;
+  const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
+  const bool last = d->host == d->H - 1;
+  if (!q || !aligned16(q)) return fail(APB_ERR_CONTRACT, "q NULL or misaligned");
+  if (d->cache_len > 0) {
+    if ((st = check_rows(k_cache, cache_row_stride, (int64_t)hk * D, "k_cache"))) return st;
+    if ((st = check_rows(v_cache, cache_row_stride, (int64_t)hk * D, "v_cache"))) return st;
+  }
+  if (last) {
+    if ((st = check_rows(k_new, new_row_stride, (int64_t)hk * D, "k_new"))) return st;
+    if ((st = check_rows(v_new, new_row_stride, (int64_t)hk * D, "v_new"))) return st;
+  }
+  if (!part_o || !part_lse || !aligned16(part_o)) return fail(APB_ERR_CONTRACT, "part_o/part_lse NULL or misaligned");
+  const size_t need = decode_workspace_bytes(decode_keys(d), d->t_new, hq, D);
+  if (need && (!ws || ws_bytes < need || !aligned16(ws))) return fail(APB_ERR_CONTRACT, "decode workspace missing or too small");
+  if ((st = check_device())) return st;
+  DecodeParams p{};
+  p.t = d->t_new;
+  p.hq = hq;
+  p.hk = hk;
+  p.g = hq / hk;
+  p.D = D;
+  p.has_new = last ? 1 : 0;
+  p.cache_len = d->cache_len;
+  p.cache_row_stride = cache_row_stride;
+  p.new_row_stride = new_row_stride;
+  const float scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)D);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.k_cache = static_cast<const __nv_bfloat16*>(k_cache);
+  p.v_cache = static_cast<const __nv_bfloat16*>(v_cache);
+  p.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  p.ws_o = static_cast<float*>(ws);
+  return launch_decode(p, part_o, part_lse, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_merge_partials(int32_t n_parts, int64_t rows, int32_t head_dim, const float* parts_o,
+                                         int64_t part_stride_o, const float* parts_lse, int64_t part_stride_lse,
+                                         void* out, float* out_lse, apb_stream_t stream) {
+  if (n_parts < 1 || rows < 0) return fail(APB_ERR_CONFIG, "n_parts >= 1 and rows >= 0 required");
+  if (head_dim != 64 && head_dim != 128) return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (!parts_o || !parts_lse || !out) return fail(APB_ERR_CONTRACT, "NULL buffer");
+  if (part_stride_o < rows * head_dim || part_stride_lse < rows) return fail(APB_ERR_CONTRACT, "part stride too small");
+  apb_status st = check_device();
+  if (st) return st;
+  return launch_merge(n_parts, rows, head_dim, parts_o, parts_lse, part_stride_o, part_stride_lse, 0, out, true,
+                      out_lse, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_exchange_partials(apb_comm* c, int64_t count_per_rank, float* buf, apb_stream_t stream) {
+  if (!c || c->nranks == 1 || count_per_rank == 0) return APB_OK;
+  if (count_per_rank < 0) return fail(APB_ERR_CONFIG, "count_per_rank < 0");
+  if (!buf || !aligned16(buf)) return fail(APB_ERR_CONTRACT, "buf NULL or misaligned");
+  NcclApi* api = nccl();
+  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+  ncclResult_t r = api->allGather(buf + (size_t)c->rank * count_per_rank, buf, (size_t)count_per_rank, ncclFloat32,
+                                  c->comm, reinterpret_cast<cudaStream_t>(stream));
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather (partials)");
+  return APB_OK;
+}

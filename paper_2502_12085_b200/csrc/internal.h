@@ -5,6 +5,7 @@
 #include <string>
 #include <cuda_runtime.h>
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include "../../include/apb.h"
 
 namespace apb {
@@ -56,5 +57,25 @@ apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, cons
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores,
                                  const void* k, const void* v, int64_t kv_row_stride, int32_t* indices,
                                  void* send, cudaStream_t stream);
+
+// ---------------------------------------------------------------- decode (Alg. apb_decode)
+constexpr int kDecodeRowsMax = 64;  // t_new * (n_heads / n_kv_heads) per KV head
+struct DecodeParams {
+  int t, hq, hk, g, D, has_new;
+  int64_t cache_len, cache_row_stride, new_row_stride;
+  float scale_log2;
+  const __nv_bfloat16* q;        // [t][hq][D]
+  const __nv_bfloat16* k_cache;  // [cache_len][hk][D] (row stride cache_row_stride)
+  const __nv_bfloat16* v_cache;
+  const __nv_bfloat16* k_new;    // [t][hk][D] (row stride new_row_stride), last host only
+  const __nv_bfloat16* v_new;
+  float* ws_o;                   // [splits][t*hq][D] then (256-B aligned) ws_lse [splits][t*hq]
+  float* ws_lse;
+};
+size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int D);
+apb_status launch_decode(const DecodeParams& p, float* part_o, float* part_lse, cudaStream_t stream);
+apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,
+                        int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,
+                        cudaStream_t stream);
 
 }  // namespace apb

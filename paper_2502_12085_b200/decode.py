@@ -1,0 +1,48 @@
+"""APB decode step (Alg. apb_decode) for the hosts one rank owns.
+
+Per layer:  every owned host h -> apb_decode_attention (partial A_h, lse_h over its block KV cache;
+the last host also over the new tokens' own keys) written into its slot of a packed
+partials buffer [H][t*hq*d + t*hq] (fp32) -> apb_exchange_partials (Gather; one in-place
+AllGather) -> apb_merge_partials (MergeScore) -> the same bf16 A [t][hq][d] on every rank.
+Appending the new K/V to the last host's cache (Alg. apb_infer) is the caller's job.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import apb
+
+
+class DecodeRank:
+    def __init__(self, H: int, hosts: list[int], t_new: int, n_heads: int, n_kv_heads: int, head_dim: int,
+                 comm: apb.Comm | None = None, device="cuda", softmax_scale: float = 0.0):
+        self.H, self.hosts, self.t = H, list(hosts), t_new
+        self.hq, self.hk, self.d = n_heads, n_kv_heads, head_dim
+        self.comm, self.scale = comm, softmax_scale
+        self.device = torch.device(device)
+        self.rows = t_new * n_heads
+        # floats per host: O [rows][d] then lse [rows], padded to 16 B so every slot stays aligned
+        self.slot = (self.rows * head_dim + self.rows + 3) // 4 * 4
+        self.parts = torch.zeros((H, self.slot), dtype=torch.float32, device=self.device)
+        self.ws = {}
+
+    def dims(self, h: int, cache_len: int) -> apb.DecodeDims:
+        return apb.DecodeDims(self.H, h, self.t, cache_len, self.hq, self.hk, self.d, self.scale)
+
+    def step(self, q, caches: dict, k_new, v_new, out, out_lse=None, stream=None) -> None:
+        """q: [t][hq][d] bf16 (same on every host); caches: {host: (k_cache, v_cache)} for the owned
+        hosts ([c_h][hk][d] bf16); k_new/v_new: [t][hk][d] bf16; out: [t][hq][d] bf16."""
+        for h in self.hosts:
+            kc, vc = caches[h]
+            d = self.dims(h, kc.shape[0])
+            n = apb.decode_workspace_size(d)
+            if self.ws.get(h) is None or self.ws[h].numel() < n:
+                self.ws[h] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device)
+            slot = self.parts[h]
+            apb.decode_attention(d, q, kc, vc, k_new if h == self.H - 1 else None,
+                                 v_new if h == self.H - 1 else None, slot[: self.rows * self.d],
+                                 slot[self.rows * self.d:], self.ws[h], stream=stream)
+        per_rank = self.slot * (self.H // (self.comm.nranks if self.comm else 1))
+        apb.exchange_partials(self.comm, per_rank, self.parts, stream=stream)
+        apb.merge_partials(self.H, self.rows, self.d, self.parts, self.slot, self.parts[:, self.rows * self.d:],
+                           self.slot, out, out_lse, stream=stream)
