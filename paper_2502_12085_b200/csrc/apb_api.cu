@@ -189,8 +189,9 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
   p.phase = (int)phase;
   if (!has_pass && phase == APB_PHASE_LOCAL) p.phase = APB_PHASE_ALL;  // LOCAL == ALL without passing
   p.local_to_ws = (phase == APB_PHASE_LOCAL && has_pass) ? 1 : 0;
-  p.n_local_items = p.nB_rt * hk * p.np;
-  p.n_anchor_items = (phase == APB_PHASE_PASSING) ? 0 : p.nA_rt * hk * p.np;
+  // work items: pairs of (row tile, query head) units per KV head (see decode_item)
+  p.n_local_items = (p.nB_rt * p.g + 1) / 2 * hk;
+  p.n_anchor_items = (phase == APB_PHASE_PASSING) ? 0 : (p.nA_rt * p.g + 1) / 2 * hk;
   const float scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)D);
   p.scale_log2 = scale * 1.4426950408889634f;
   p.out = out;

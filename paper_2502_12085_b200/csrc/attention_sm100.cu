@@ -92,30 +92,44 @@ struct Layout {
 };
 
 struct Item {
-  int seg;  // 0 = anchor query rows, 1 = local query rows
-  int rt;   // 128-row tile index inside the segment
-  int j;    // KV head
-  int qh0;  // first query head
+  int seg;     // 0 = anchor query rows, 1 = local query rows
+  int rt;      // 128-row tile index of tile 0 (the heavier one): plans the key-tile walk
+  int rtt[2];  // row tile of each query tile
+  int qht[2];  // query head of each query tile
+  int j;       // KV head (shared by both tiles)
   int ntiles;
   int nkv;
 };
 
+// Work items: per (segment, KV head j) the units (row tile, query head of j's group) are ordered
+// heaviest row tile first and paired consecutively; a pair shares every K/V tile.  For even g both
+// units of a pair have the same row tile; for odd g every other pair spans two adjacent row tiles
+// (the lighter tile then masks the heavier one's extra diagonal key tiles).  Item w -> pair w / hk
+// of KV head w % hk, so the heaviest pairs of all heads come first.
 __device__ __forceinline__ Item decode_item(const AttnParams& p, int w) {
   Item it;
-  const int per_rt = p.hk * p.np;
+  int nrt;
   if (w < p.n_local_items) {
     it.seg = 1;
-    it.rt = p.nB_rt - 1 - w / per_rt;  // heaviest (largest causal extent) first
+    nrt = p.nB_rt;
   } else {
     w -= p.n_local_items;
     it.seg = 0;
-    it.rt = p.nA_rt - 1 - w / per_rt;
+    nrt = p.nA_rt;
   }
-  w %= per_rt;
-  it.j = w / p.np;
-  const int pi = w % p.np;
-  it.qh0 = it.j * p.g + 2 * pi;
-  it.ntiles = (2 * pi + 1 < p.g) ? 2 : 1;
+  it.j = w % p.hk;
+  const int pidx = w / p.hk;
+  const int units = nrt * p.g;
+  it.ntiles = 0;
+  for (int t = 0; t < 2; ++t) {
+    const int u = 2 * pidx + t;
+    const int uu = u < units ? u : units - 1;
+    it.rtt[t] = nrt - 1 - uu / p.g;
+    it.qht[t] = it.j * p.g + uu % p.g;
+    if (u < units) it.ntiles = t + 1;
+  }
+  it.rt = it.rtt[0];
+  // key tiles reachable from query rows [128 rt, 128 rt + 128)
   if (it.seg == 0) {
     it.nkv = it.rt + 1;
   } else {
@@ -221,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
     if (warp == kLoadWarp) {
       // ============================================================== TMA producer (warp-converged)
-      const int qrow0 = (it.seg == 0 ? 0 : p.L_A) + it.rt * BM;
+      const int qbase = it.seg == 0 ? 0 : p.L_A;
 #ifndef APB_NO_L2_HINTS
       const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
 #define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d_hint(dst, map, bar, a, b, c, pol_kv)
@@ -235,9 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < it.ntiles; ++t)
           for (int h = 0; h < L::kHalves; ++h)
 #ifndef APB_NO_L2_HINTS
-            tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qh0 + t, qrow0, pol_q);
+            tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM, pol_q);
 #else
-            tma_load_3d(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qh0 + t, qrow0);
+            tma_load_3d(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM);
 #endif
       }
       __syncwarp();
@@ -366,8 +380,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
       const uint32_t tS = tmem + lane_base + t * 128;
       const uint32_t tO = tmem + lane_base + 256 + t * D;
-      const int qh = it.qh0 + t;
-      const int row = it.rt * BM + tid;  // row index inside the query segment
+      const int qh = it.qht[t];
+      const int row = it.rtt[t] * BM + tid;  // row index inside the query segment
       const bool row_valid = it.seg == 0 ? row < p.L_A : row < p.l_b;
       const float sl2 = p.scale_log2;
       float m_run = -INFINITY, l_run = 0.f;

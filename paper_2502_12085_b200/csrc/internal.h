@@ -23,7 +23,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t
 // ---------------------------------------------------------------- attention
 struct AttnParams {
   int L_A, l_b, lp, n_slots;  // n_slots = host: passing slots 0..host-1
-  int hq, hk, g, np;          // np = ceil(g/2): Q-tile pairs per (row tile, KV head)
+  int hq, hk, g, np;          // np = ceil(g/2) (unused by the unit pairing; kept for the ABI struct layout)
   int nA_rt, nB_rt;           // 128-row query tiles of the anchor / local segment
   int nA_kv, nP_kv;           // 128-key tiles of the anchor segment / of one passing slot
   int n_local_items, n_anchor_items;

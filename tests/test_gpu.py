@@ -334,3 +334,20 @@ def test_nccl_unique_id_and_single_rank_comm():
     g = torch.zeros((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d), dtype=torch.bfloat16, device="cuda")
     apb.exchange_passing(c, dims_of(cfg, 0), g)
     c.close()
+
+
+@pytest.mark.parametrize("name", ["qwen14b-128k", "yi34b-200k"])
+def test_full_size_odd_gqa_sampled(name):
+    """BASELINE configs[2] / [3] (Qwen-2.5-14B: 40 Q / 8 KV heads, g = 5; Yi-34B: 56 / 8, g = 7,
+    n = 200K): the critical host's one-pass attention at full size (query-tile pairs spanning two
+    row tiles), sampled rows vs the oracle."""
+    cfg = synth.CONFIGS[name]
+    h = cfg.H - 1
+    x = synth.host_qkv(cfg, 0, h)
+    rng = np.random.default_rng(1)
+    gathered = synth.f32_to_bf16_bits(rng.standard_normal((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)).astype(np.float32))
+    O, lse = run_attention(cfg, h, x, gathered, "all")
+    rows = _sample_rows(x["L_A"], cfg.l_b, 16, rng)
+    pk, pv = oracle.passing(gathered, h)
+    O_or, lse_or = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv, rows=rows)
+    check_attention(O[rows], lse[rows], O_or, lse_or, f"{name} host {h} sampled ({len(rows)} rows)")
