@@ -38,8 +38,9 @@ constexpr int kABytes = TM * TK * 2;  // 16 KB
 constexpr int kBBytes = TN * TK * 2;  // 32 KB
 constexpr int kOffA = 0;
 constexpr int kOffB = kOffA + STAGES * kABytes;
-constexpr int kOffO = kOffB + STAGES * kBBytes;              // fp32 partial o: [2][kMaxOut][TM]
-constexpr int kOffBar = kOffO + 2 * kMaxOut * TM * 4;
+constexpr int kOffW2 = kOffB + STAGES * kBBytes;            // fp32 W2 slice of one chunk [kMaxOut][TN]
+constexpr int kOffB1 = kOffW2 + kMaxOut * TN * 4;             // fp32 b1 slice [TN]
+constexpr int kOffBar = kOffB1 + TN * 4;
 constexpr int kNumBars = 2 * STAGES + 4;                      // full/empty per stage, acc full/empty x2
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmem = kOffTmem + 16 + 1024;
@@ -57,7 +58,6 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
   auto bAccFull = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
   auto bAccEmpty = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmem);
-  float* opart = reinterpret_cast<float*>(smem + kOffO);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   const int m0 = blockIdx.x * TM;
@@ -130,53 +130,85 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================================================================ epilogue (256 threads)
-    const int wg = warp / 4;          // column half of the chunk
-    const int r = threadIdx.x % 128;  // token row in the tile == TMEM lane
+    // thread = (token row r = TMEM lane, column half wg of each 256-wide chunk); the W2 partial
+    // sums of the row stay in registers, summed in a fixed order (deterministic)
+    const int wg = warp / 4;
+    const int r = threadIdx.x % 128;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    float* my_o = opart + (size_t)wg * kMaxOut * TM;
-    for (int oc = 0; oc < p.n_out; ++oc) my_o[oc * TM + r] = 0.f;
+    float o[kMaxOut];
+#pragma unroll
+    for (int oc = 0; oc < kMaxOut; ++oc) o[oc] = 0.f;
+    float* w2s = reinterpret_cast<float*>(smem + kOffW2);
+    float* b1s = reinterpret_cast<float*>(smem + kOffB1);
     for (int c = 0; c < nchunks; ++c) {
       const int b = c & 1;
+      // this chunk's W2 columns and b1 entries -> shared memory (read back as warp broadcasts)
+      for (int idx = threadIdx.x; idx < p.n_out * (TN / 4); idx += 256) {
+        const int oc = idx / (TN / 4), c4 = idx % (TN / 4);
+        reinterpret_cast<float4*>(w2s + oc * TN)[c4] =
+            __ldg(reinterpret_cast<const float4*>(p.w2 + (size_t)oc * p.d_hidden + c * TN) + c4);
+      }
+      for (int idx = threadIdx.x; idx < TN; idx += 256) b1s[idx] = p.b1 ? __ldg(p.b1 + c * TN + idx) : 0.f;
+      named_bar_sync(1, 256);
       mbar_wait(bAccFull(b), (c >> 1) & 1);
       tc_fence_after();
-      uint32_t zr[128];
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4)
-        tmem_ld32(tmem + lane_base + b * TN + wg * 128 + q4 * 32, *reinterpret_cast<uint32_t(*)[32]>(&zr[q4 * 32]));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bAccEmpty(b));  // TMEM buffer free: the next-but-one chunk may accumulate into it
-      const int u0 = c * TN + wg * 128;
-      float* a = reinterpret_cast<float*>(zr);
-#pragma unroll
-      for (int e = 0; e < 128; ++e) {
-        float z = a[e] + (p.b1 ? __ldg(p.b1 + u0 + e) : 0.f);
-        a[e] = __fdividef(z, 1.f + __expf(-z));  // SiLU
-      }
-      for (int oc = 0; oc < p.n_out; ++oc) {
-        const float4* w = reinterpret_cast<const float4*>(p.w2 + (size_t)oc * p.d_hidden + u0);
-        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-#pragma unroll
-        for (int e4 = 0; e4 < 32; ++e4) {
-          const float4 wv = __ldg(w + e4);
-          acc0 = fmaf(wv.x, a[4 * e4 + 0], acc0);
-          acc1 = fmaf(wv.y, a[4 * e4 + 1], acc1);
-          acc2 = fmaf(wv.z, a[4 * e4 + 2], acc2);
-          acc3 = fmaf(wv.w, a[4 * e4 + 3], acc3);
+      for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t zr[32];
+        tmem_ld32(tmem + lane_base + b * TN + wg * 128 + q4 * 32, zr);
+        tmem_wait_ld();
+        if (q4 == 3) {
+          tc_fence_before();
+          mbar_arrive(bAccEmpty(b));  // TMEM buffer free: the next-but-one chunk may accumulate into it
         }
-        my_o[oc * TM + r] += (acc0 + acc1) + (acc2 + acc3);
+#ifdef APB_DEBUG_SCORE_NO_EPILOGUE
+        continue;  // timing experiment only
+#endif
+        const int cl = wg * 128 + q4 * 32;  // column of this piece inside the chunk
+        float* a = reinterpret_cast<float*>(zr);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float z = a[e] + b1s[cl + e];
+          a[e] = __fdividef(z, 1.f + __expf(-z));  // SiLU
+        }
+#pragma unroll
+        for (int oc = 0; oc < kMaxOut; ++oc) {
+          if (oc < p.n_out) {
+            const float4* w = reinterpret_cast<const float4*>(w2s + oc * TN + cl);
+            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+            for (int e4 = 0; e4 < 8; ++e4) {
+              const float4 wv = w[e4];
+              acc0 = fmaf(wv.x, a[4 * e4 + 0], acc0);
+              acc1 = fmaf(wv.y, a[4 * e4 + 1], acc1);
+              acc2 = fmaf(wv.z, a[4 * e4 + 2], acc2);
+              acc3 = fmaf(wv.w, a[4 * e4 + 3], acc3);
+            }
+            o[oc] += (acc0 + acc1) + (acc2 + acc3);
+          }
+        }
       }
+      named_bar_sync(1, 256);  // the slice is overwritten by the next chunk
+    }
+    // combine the two column halves through the (now idle) stage buffers: every MMA has
+    // completed and every multicast slice has landed (each stage's full barrier was waited on)
+    float* xo = reinterpret_cast<float*>(smem + kOffA);  // [kMaxOut][TM]
+    named_bar_sync(1, 256);
+    if (wg == 1) {
+#pragma unroll
+      for (int oc = 0; oc < kMaxOut; ++oc)
+        if (oc < p.n_out) xo[oc * TM + r] = o[oc];
     }
     named_bar_sync(1, 256);
     if (wg == 0 && m0 + r < p.l_b) {
       const int rr = p.n_out / p.hk;
-      const float* o0 = opart;
-      const float* o1 = opart + (size_t)kMaxOut * TM;
       for (int j = 0; j < p.hk; ++j) {
         float m = -INFINITY;
-        for (int cc = j * rr; cc < (j + 1) * rr; ++cc) {
-          const float o = o0[cc * TM + r] + o1[cc * TM + r] + (p.b2 ? __ldg(p.b2 + cc) : 0.f);
-          m = fmaxf(m, o);
+#pragma unroll
+        for (int oc = 0; oc < kMaxOut; ++oc) {
+          if (oc >= j * rr && oc < (j + 1) * rr) {
+            const float v = o[oc] + xo[oc * TM + r] + (p.b2 ? __ldg(p.b2 + oc) : 0.f);
+            m = fmaxf(m, v);
+          }
         }
         p.scores[(int64_t)j * p.l_b + m0 + r] = m;
       }
