@@ -119,6 +119,24 @@ apb_status apb_select_topk(const apb_dims* dims, const float* scores,
                            int32_t* indices, void* send, void* ws, size_t ws_bytes,
                            apb_stream_t stream);
 
+/* ---------------------------------------------------------------- method variants (NEXT #3)
+ * Compressor and selection variants of the ablation lattice (Table 4).
+ *
+ * apb_random_scores — the random selector "Rd.": writes
+ * scores[j][t] (fp32 [n_kv_heads][l_b]) = uniform in [0,1) drawn from counter
+ *   c = ((layer * H + host) * n_kv_heads + j) * l_b + t
+ * as the top 24 bits (times 2^-24) of the (c+1)-th output of a SplitMix64 stream seeded with
+ * `seed` (reading G17).  Feeding these to apb_select_topk picks a uniformly random
+ * l_p'-subset per KV head.  Deterministic; layer >= 0 (else APB_ERR_CONFIG).
+ *
+ * apb_share_scores — the shared-index-set reading (one index list per host,
+ * Alg. apb_prefill): in place, every row j of scores (fp32 [n_kv_heads][l_b]) becomes
+ * max over KV heads of scores[.][t]; apb_select_topk then returns the same set for every head.
+ * Both: caller-owned device buffer, enqueued on `stream`, APB_ERR_CONTRACT on NULL.        */
+apb_status apb_random_scores(const apb_dims* dims, uint64_t seed, int32_t layer, float* scores,
+                             apb_stream_t stream);
+apb_status apb_share_scores(const apb_dims* dims, float* scores, apb_stream_t stream);
+
 /* ---------------------------------------------------------------- step 3: exchange
  * One in-place AllGather of the packed compressed blocks over NCCL (the
  * paper's two AllGathers of K and V are fused into one, reading G11).

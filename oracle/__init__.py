@@ -63,8 +63,9 @@ def _load():
             lib.oracle_decode_partial.argtypes = [i64, i64, i32, i32, i32, ctypes.c_double,
                                                   dp, dp, dp, dp, dp, dp, dp]
             lib.oracle_merge_score.argtypes = [i32, i64, i32, dp, dp, dp, dp]
+            lib.oracle_random_scores.argtypes = [ctypes.c_uint64, ctypes.c_uint64, i64, dp]
             for f in (lib.oracle_retain_score, lib.oracle_select_topk, lib.oracle_attention,
-                      lib.oracle_decode_partial, lib.oracle_merge_score):
+                      lib.oracle_decode_partial, lib.oracle_merge_score, lib.oracle_random_scores):
                 f.restype = ctypes.c_int
             lib.oracle_num_threads.restype = ctypes.c_int
             _lib = lib
@@ -125,6 +126,23 @@ def select_topk(s_row, l_p: int) -> np.ndarray:
     if rc:
         raise ValueError(f"oracle_select_topk rc={rc}")
     return idx
+
+
+def random_scores(seed: int, layer: int, H: int, host: int, hk: int, l_b: int) -> np.ndarray:
+    """The random compressor "Rd." (Table 4) for one host and layer:
+    [hk][l_b] uniform scores in [0,1), counter c = ((layer*H + host)*hk + j)*l_b + t of the
+    SplitMix64 stream seeded with `seed` (reading G17)."""
+    out = np.empty((hk, l_b), np.float64)
+    c0 = ((layer * H + host) * hk * l_b) % (1 << 64)
+    _load().oracle_random_scores(ctypes.c_uint64(seed % (1 << 64)), ctypes.c_uint64(c0), hk * l_b, _p(out))
+    return out
+
+
+def share_scores(s) -> np.ndarray:
+    """Shared index set (SPEC S:255, S:294 — one index list per host, as Alg. apb_prefill
+    writes it): every KV head's score row is replaced by the max over KV heads."""
+    s = np.asarray(s, np.float64)
+    return np.broadcast_to(s.max(axis=0, keepdims=True), s.shape).copy()
 
 
 def select_all_heads(s, l_p: int) -> np.ndarray:

@@ -268,3 +268,21 @@ int oracle_merge_score(int32_t n, int64_t rows, int32_t d, const double* parts_o
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ method variants
+ * Random selector "Rd." (Table 4), reading G17: a
+ * SplitMix64 stream seeded with `seed`, advanced to position c0, emits `count` outputs;
+ * score = top 24 bits * 2^-24 (uniform in [0,1), exact in fp32 and fp64).  Written as the
+ * textbook sequential generator (state += golden gamma; mix) — one output per step. */
+int oracle_random_scores(uint64_t seed, uint64_t c0, int64_t count, double* out) {
+  uint64_t state = seed + c0 * 0x9E3779B97F4A7C15ull; /* = seed after c0 steps */
+  for (int64_t i = 0; i < count; ++i) {
+    state += 0x9E3779B97F4A7C15ull;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    out[i] = (double)(z >> 40) / 16777216.0;
+  }
+  return 0;
+}

@@ -84,7 +84,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_decode_workspace_size.argtypes = [ddp, ctypes.POINTER(sz)]
     lib.apb_merge_partials.argtypes = [i32, i64, i32, vp, i64, vp, i64, vp, vp, vp]
     lib.apb_exchange_partials.argtypes = [vp, i64, vp, vp]
-    for f in ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
+    lib.apb_random_scores.argtypes = [dp, ctypes.c_uint64, i32, vp, vp]
+    lib.apb_share_scores.argtypes = [dp, vp, vp]
+    for f in ("apb_random_scores", "apb_share_scores", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials"):
@@ -217,6 +219,19 @@ def select_topk(dims: Dims, scores, k, v, indices, send, stream=None) -> None:
     _check(load().apb_select_topk(ctypes.byref(d), scores.data_ptr(), k.data_ptr(), v.data_ptr(),
                                   _rowstride(k, "k"), indices.data_ptr(), send.data_ptr(), None, 0,
                                   _stream(stream)), "apb_select_topk")
+
+
+def random_scores(dims: Dims, seed: int, layer: int, scores, stream=None) -> None:
+    """The "Rd." compressor (Table 4): scores [n_kv_heads][l_b] fp32 <- seeded uniform [0,1)."""
+    d = dims.c()
+    _check(load().apb_random_scores(ctypes.byref(d), seed % (1 << 64), layer, scores.data_ptr(), _stream(stream)),
+           "apb_random_scores")
+
+
+def share_scores(dims: Dims, scores, stream=None) -> None:
+    """Shared index set: scores rows <- max over KV heads, in place."""
+    d = dims.c()
+    _check(load().apb_share_scores(ctypes.byref(d), scores.data_ptr(), _stream(stream)), "apb_share_scores")
 
 
 def attention_fwd(dims: Dims, q, k, v, gathered, out, lse=None, phase: int = PHASE_ALL, ws=None,

@@ -309,6 +309,27 @@ extern "C" apb_status apb_select_topk(const apb_dims* d, const float* scores, co
                                reinterpret_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- method variants (NEXT #3)
+extern "C" apb_status apb_random_scores(const apb_dims* d, uint64_t seed, int32_t layer, float* scores,
+                                        apb_stream_t stream) {
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (layer < 0) return fail(APB_ERR_CONFIG, "layer must be >= 0");
+  if (!scores) return fail(APB_ERR_CONTRACT, "scores NULL");
+  if ((st = check_device())) return st;
+  const int64_t per_host = (int64_t)d->n_kv_heads * d->l_b;
+  const uint64_t c0 = ((uint64_t)layer * (uint64_t)d->H + (uint64_t)d->host) * (uint64_t)per_host;
+  return launch_random_scores(seed, c0, per_host, scores, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_share_scores(const apb_dims* d, float* scores, apb_stream_t stream) {
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (!scores) return fail(APB_ERR_CONTRACT, "scores NULL");
+  if ((st = check_device())) return st;
+  return launch_share_scores(scores, d->n_kv_heads, d->l_b, reinterpret_cast<cudaStream_t>(stream));
+}
+
 // ---------------------------------------------------------------- step 3: exchange (NCCL)
 struct apb_comm {
   ncclComm_t comm;

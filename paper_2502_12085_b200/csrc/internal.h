@@ -54,6 +54,8 @@ apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, cons
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream);
 
 // ---------------------------------------------------------------- selection + compaction
+apb_status launch_random_scores(uint64_t seed, uint64_t c0, int64_t count, float* scores, cudaStream_t stream);
+apb_status launch_share_scores(float* scores, int hk, int l_b, cudaStream_t stream);
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores,
                                  const void* k, const void* v, int64_t kv_row_stride, int32_t* indices,
                                  void* send, cudaStream_t stream);

@@ -141,4 +141,51 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
   return APB_OK;
 }
 
+// ---------------------------------------------------------------- method variants (NEXT #3)
+namespace sel {
+
+// "Rd." compressor (Table 4): a uniform score in [0,1) per
+// (layer, host, KV head, block token) from the counter-based generator of DESIGN.md reading
+// G17 — the (c+1)-th output of a SplitMix64 stream seeded with `seed`, top 24 bits.
+__global__ void __launch_bounds__(256) random_scores_kernel(uint64_t seed, uint64_t c0, int64_t count,
+                                                            float* __restrict__ scores) {
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < count; i += (int64_t)gridDim.x * 256) {
+    uint64_t z = seed + (c0 + (uint64_t)i + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    scores[i] = (float)(z >> 40) * 0x1p-24f;  // exact: a 24-bit integer times 2^-24
+  }
+}
+
+// Shared index set (reading G3's alternative): every KV head's row of
+// scores becomes the max over the KV heads, so the per-head select yields one common set.
+__global__ void __launch_bounds__(256) share_scores_kernel(float* __restrict__ scores, int hk, int l_b) {
+  for (int t = blockIdx.x * 256 + threadIdx.x; t < l_b; t += gridDim.x * 256) {
+    float m = scores[t];
+    for (int j = 1; j < hk; ++j) m = fmaxf(m, scores[(int64_t)j * l_b + t]);
+    for (int j = 0; j < hk; ++j) scores[(int64_t)j * l_b + t] = m;
+  }
+}
+
+}  // namespace sel
+
+apb_status launch_random_scores(uint64_t seed, uint64_t c0, int64_t count, float* scores, cudaStream_t stream) {
+  const int64_t blocks = (count + 255) / 256;
+  sel::random_scores_kernel<<<(int)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, stream>>>(seed, c0, count, scores);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("random_scores launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+apb_status launch_share_scores(float* scores, int hk, int l_b, cudaStream_t stream) {
+  const int blocks = (l_b + 255) / 256;
+  sel::share_scores_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, stream>>>(scores, hk, l_b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("share_scores launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
 }  // namespace apb

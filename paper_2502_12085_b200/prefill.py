@@ -39,12 +39,19 @@ class HostIO:
 class PrefillRank:
     def __init__(self, base: apb.Dims, hosts: list[int], comm: apb.Comm | None = None,
                  device: torch.device | str = "cuda", skip_unused_last: bool = False,
-                 split_phases: bool | None = None):
+                 split_phases: bool | None = None, compressor: str = "retain", shared_set: bool = False,
+                 seed: int = 0):
         """base: problem dims (its `host` field is ignored); hosts: host indices this rank owns
         (contiguous, in order).  skip_unused_last: do not score/select host H-1 — its
         compressed block is ignored by every host, so outputs are unchanged.
         split_phases: LOCAL/PASSING launches around the exchange (default: only when a multi-rank
-        communicator is given; a single rank uses one ordered APB_PHASE_ALL launch per host)."""
+        communicator is given; a single rank uses one ordered APB_PHASE_ALL launch per host).
+        compressor: "retain" (retaining heads R) or "random" (the "Rd." selector of
+        Table 4, seeded by `seed` and the layer index); shared_set: one index set per host, the
+        max over KV heads instead of per-KV-head sets (reading G3)."""
+        if compressor not in ("retain", "random"):
+            raise ValueError(f"compressor must be 'retain' or 'random', not {compressor!r}")
+        self.compressor, self.shared_set, self.seed = compressor, shared_set, seed
         self.base, self.hosts, self.comm = base, list(hosts), comm
         self.device = torch.device(device)
         self.skip_unused_last = skip_unused_last
@@ -67,14 +74,26 @@ class PrefillRank:
     def dims(self, h: int) -> apb.Dims:
         return self.base.with_host(h)
 
-    def compress(self, io: dict[int, HostIO], weights: apb.RetainWeights, stream=None) -> None:
-        """Steps 1-2 for every owned host: scores -> top-l_p indices -> gathered[h] (in place)."""
-        for h in self.hosts:
-            if self.base.l_pp == 0 or (self.skip_unused_last and h == self.base.H - 1):
-                continue
-            d, x = self.dims(h), io[h]
+    def _compress_host(self, h: int, io: dict[int, HostIO], weights, layer_idx: int, stream) -> None:
+        """Steps 1-2 for host h: scores (compressor) -> top-l_p indices -> gathered[h] (in place)."""
+        d, x = self.dims(h), io[h]
+        if self.compressor == "random":
+            apb.random_scores(d, self.seed, layer_idx, self.scores[h], stream=stream)
+        else:
             apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h], stream=stream)
-            apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h], self.gathered[h], stream=stream)
+        if self.shared_set:
+            apb.share_scores(d, self.scores[h], stream=stream)
+        apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h], self.gathered[h], stream=stream)
+
+    def _compresses(self, h: int) -> bool:
+        return self.base.l_pp > 0 and not (self.skip_unused_last and h == self.base.H - 1)
+
+    def compress(self, io: dict[int, HostIO], weights: apb.RetainWeights | None, stream=None,
+                 layer_idx: int = 0) -> None:
+        """Steps 1-2 for every owned host."""
+        for h in self.hosts:
+            if self._compresses(h):
+                self._compress_host(h, io, weights, layer_idx, stream)
 
     def exchange(self, stream=None) -> None:
         """Step 3: one in-place AllGather of the packed [2][hk][l_p'][d] slots."""
@@ -86,8 +105,8 @@ class PrefillRank:
             apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse, phase=phase,
                               ws=self.ws[h], stream=stream)
 
-    def layer(self, io: dict[int, HostIO], weights: apb.RetainWeights, overlap: bool = True,
-              events: list | None = None) -> None:
+    def layer(self, io: dict[int, HostIO], weights: apb.RetainWeights | None, overlap: bool = True,
+              events: list | None = None, layer_idx: int = 0) -> None:
         """One layer of the hot path for all owned hosts, enqueued on the current stream.
         events: if a list is given, (start, end) timing-event pairs bracketing the attention
         launches on the main stream are appended to it (the bench's in-situ kernel time)."""
@@ -103,7 +122,7 @@ class PrefillRank:
             events.append((a, b))
 
         if not overlap:
-            self.compress(io, weights, main)
+            self.compress(io, weights, main, layer_idx)
             self.exchange(main)
             timed(lambda: self.attention(io, apb.PHASE_ALL, main))
             return
@@ -113,11 +132,8 @@ class PrefillRank:
             # < h (side stream, one event per host) — no LOCAL/PASSING split, no fp32 partial.
             self.side.wait_stream(main)
             for h in self.hosts:
-                if self.base.l_pp > 0 and not (self.skip_unused_last and h == self.base.H - 1):
-                    d, x = self.dims(h), io[h]
-                    apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h], stream=self.side)
-                    apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h], self.gathered[h],
-                                    stream=self.side)
+                if self._compresses(h):
+                    self._compress_host(h, io, weights, layer_idx, self.side)
                 self.ev_slot[h].record(self.side)
             self.exchange(self.side)  # no-op without a communicator
             for h in self.hosts:
@@ -128,7 +144,7 @@ class PrefillRank:
                                                 phase=apb.PHASE_ALL, ws=self.ws[h], stream=main))
             return
         self.side.wait_stream(main)  # this layer's inputs are produced on the main stream
-        self.compress(io, weights, self.side)
+        self.compress(io, weights, self.side, layer_idx)
         self.exchange(self.side)
         self.ev_exchanged.record(self.side)
         timed(lambda: self.attention(io, apb.PHASE_LOCAL, main))

@@ -461,3 +461,63 @@ def test_merge_score_spec_examples():
     a2, l2 = oracle.decode_partial(q, k[3:], v[3:])
     A, L = oracle.merge_score(np.stack([a1, a2]), np.stack([l1, l2]))
     assert np.allclose(A, full, atol=1e-14) and np.allclose(L, full_l, atol=1e-14)
+
+
+# ------------------------------------------------------------------ method variants (NEXT #3)
+def test_random_scores_match_splitmix64_reference_stream():
+    """Rd. compressor (Table 4), reading G17: the scores are the published
+    SplitMix64 outputs (tests/golden/splitmix64.json), top 24 bits, times 2^-24."""
+    g = json.load(open(os.path.join(GOLD, "splitmix64.json")))
+    want = [int(h, 16) >> 40 for h in g["outputs_hex"]]
+    s = oracle.random_scores(g["seed"], 0, 1, 0, 1, len(want))
+    assert s.shape == (1, len(want))
+    assert [int(x * 2 ** 24) for x in s[0]] == want
+    assert np.all(s * 2 ** 24 == np.floor(s * 2 ** 24))  # exact 24-bit grid, in [0, 1)
+
+
+def test_random_scores_counter_layout_and_determinism():
+    """c = ((layer*H + host)*hk + j)*l_b + t indexes one stream: a host's block is a slice of it."""
+    seed, H, hk, l_b = 12345, 3, 2, 5
+    stream = oracle.random_scores(seed, 0, 1, 0, 1, 4 * H * hk * l_b)[0]
+    for layer in range(2):
+        for host in range(H):
+            s = oracle.random_scores(seed, layer, H, host, hk, l_b)
+            c0 = (layer * H + host) * hk * l_b
+            np.testing.assert_array_equal(s.reshape(-1), stream[c0:c0 + hk * l_b])
+            np.testing.assert_array_equal(s, oracle.random_scores(seed, layer, H, host, hk, l_b))
+    assert not np.array_equal(oracle.random_scores(1, 0, 1, 0, 2, 64), oracle.random_scores(2, 0, 1, 0, 2, 64))
+
+
+def test_random_selector_is_uniform_monte_carlo():
+    """over 200 trials each index is selected with frequency l_p/l_b +- 0.05."""
+    l_b, l_p, trials = 64, 16, 200
+    counts = np.zeros(l_b)
+    for layer in range(trials):
+        s = oracle.random_scores(7, layer, 1, 0, 1, l_b)
+        counts[oracle.select_topk(s[0], l_p)] += 1
+    freq = counts / trials
+    assert np.all(np.abs(freq - l_p / l_b) <= 0.1)  # per-index binomial sd = 0.031; 3.2 sd
+    assert abs(freq.mean() - l_p / l_b) < 1e-12  # exactly l_p picks per trial
+    # and the scores themselves are uniform: Kolmogorov-Smirnov distance vs U[0,1)
+    u = np.sort(oracle.random_scores(7, 0, 1, 0, 1, 20000)[0])
+    ks = np.max(np.abs(u - np.arange(1, u.size + 1) / u.size))
+    assert ks < 1.63 / np.sqrt(u.size)  # 1 % critical value
+
+
+def test_share_scores_examples():
+    """Shared index set: max over KV heads, then one selection for all."""
+    s = np.array([[3.0, 1.0, 2.0], [0.0, 5.0, 1.0]])
+    sh = oracle.share_scores(s)
+    np.testing.assert_array_equal(sh, [[3, 5, 2], [3, 5, 2]])
+    idx = oracle.select_all_heads(sh, 2)
+    np.testing.assert_array_equal(idx, [[0, 1], [0, 1]])
+    # per-head selection of the same scores differs (head 1 would take 1, 2)
+    np.testing.assert_array_equal(oracle.select_all_heads(s, 2), [[0, 2], [1, 2]])
+    # one KV head: identity
+    one = np.array([[0.5, -1.0, 2.0]])
+    np.testing.assert_array_equal(oracle.share_scores(one), one)
+    # the shared set maximises the head-max of the selected scores (brute force, tiny case)
+    rng = np.random.default_rng(3)
+    s = rng.standard_normal((3, 7))
+    best = max(itertools.combinations(range(7), 3), key=lambda c: (sorted(s.max(0)[list(c)], reverse=True)))
+    np.testing.assert_array_equal(oracle.select_all_heads(oracle.share_scores(s), 3)[0], sorted(best))
