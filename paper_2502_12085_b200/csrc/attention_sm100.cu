@@ -30,7 +30,14 @@ using namespace apb::sm100;
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int KS = 2;  // K and V ring stages
+// K and V tiles share one ring, loaded in consumption order K(0), V(0), K(1), V(1), ...;
+// K(i) is released after S_1(i), V(i) after PV_1(i) — also in sequence order — so a slot is
+// reused exactly kRing loads later.  Load n (= 2i for K(i), 2i+1 for V(i)) uses slot n % kRing.
+#ifndef APB_RING
+#define APB_RING 5
+#endif
+template <int D>
+constexpr int ring_slots() { return D == 128 ? APB_RING : 2 * APB_RING; }
 constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, {TMA, MMA, 2 idle}
 constexpr int kLoadWarp = 10;  // SMSP 2 (warps 0/4 on SMSP 0 would otherwise share with it)
 constexpr int kMmaWarp = 9;
@@ -79,12 +86,12 @@ struct Layout {
   static constexpr int kHalves = D / 64;           // 64-element (128 B) swizzle atoms per row
   static constexpr int kSub = BM * 128;            // bytes of one 128-row x 64-col sub-tile
   static constexpr int kTile = kHalves * kSub;     // bytes of a 128 x D bf16 tile
+  static constexpr int kRing = ring_slots<D>();
   static constexpr int kQ = 0;
-  static constexpr int kK = kQ + 2 * kTile;
-  static constexpr int kV = kK + KS * kTile;
-  static constexpr int kBar = kV + KS * kTile;
-  // barriers: Qfull, Kfull[KS], Kempty[KS], Vfull[KS], Vempty[KS], Sfull[2], Pfull[2][2 halves], Odone[2]
-  static constexpr int kNumBars = 1 + 4 * KS + 8;
+  static constexpr int kR = kQ + 2 * kTile;  // the K/V ring
+  static constexpr int kBar = kR + kRing * kTile;
+  // barriers: Qfull, full[kRing], empty[kRing], Sfull[2], Pfull[2][2 halves], Odone[2]
+  static constexpr int kNumBars = 1 + 2 * kRing + 8;
   static constexpr int kTmemPtr = kBar + kNumBars * 8;
   static constexpr int kUsed = kTmemPtr + 16;
   // keep one CTA per SM (each CTA allocates all 512 TMEM columns)
@@ -182,16 +189,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sQ = sbase + L::kQ, sK = sbase + L::kK, sV = sbase + L::kV;
+  constexpr int NR = L::kRing;
+  const uint32_t sQ = sbase + L::kQ;
   const uint32_t bar0 = sbase + L::kBar;
   const uint32_t bQ = bar0;
-  auto bKf = [&](int s) { return bar0 + 8u * (1 + s); };
-  auto bKe = [&](int s) { return bar0 + 8u * (1 + KS + s); };
-  auto bVf = [&](int s) { return bar0 + 8u * (1 + 2 * KS + s); };
-  auto bVe = [&](int s) { return bar0 + 8u * (1 + 3 * KS + s); };
-  auto bS = [&](int t) { return bar0 + 8u * (1 + 4 * KS + t); };
-  auto bP = [&](int t, int half) { return bar0 + 8u * (3 + 4 * KS + 2 * t + half); };
-  auto bO = [&](int t) { return bar0 + 8u * (7 + 4 * KS + t); };
+  auto sR = [&](int slot) { return sbase + L::kR + slot * L::kTile; };
+  auto bRf = [&](int slot) { return bar0 + 8u * (1 + slot); };
+  auto bRe = [&](int slot) { return bar0 + 8u * (1 + NR + slot); };
+  auto bS = [&](int t) { return bar0 + 8u * (1 + 2 * NR + t); };
+  auto bP = [&](int t, int half) { return bar0 + 8u * (3 + 2 * NR + 2 * t + half); };
+  auto bO = [&](int t) { return bar0 + 8u * (7 + 2 * NR + t); };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtr);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
@@ -199,11 +206,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bQ, 1);
-    for (int s = 0; s < KS; ++s) {
-      mbar_init(bKf(s), 1);
-      mbar_init(bKe(s), 1);
-      mbar_init(bVf(s), 1);
-      mbar_init(bVe(s), 1);
+    for (int r = 0; r < NR; ++r) {
+      mbar_init(bRf(r), 1);
+      mbar_init(bRe(r), 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(bS(t), 1);
@@ -256,40 +261,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       for (int i = 0; i < it.nkv; ++i) {
-        const int s = i % KS;
-        const uint32_t ph = (i / KS) & 1;
         const KvTile kt = kv_tile(p, it, i);
         const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
-        mbar_wait_sleep(bKe(s), ph ^ 1);
-        if (elect_one()) {
-          if ((p.dbg_skip & 1) && i >= KS) {
-            mbar_arrive(bKf(s));
-          } else {
-            mbar_arrive_expect_tx(bKf(s), L::kTile);
-            for (int h = 0; h < L::kHalves; ++h) {
-              if (kt.kind == 1)
-                KV_LOAD4(sK + s * L::kTile + h * L::kSub, &tm_g, bKf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 0);
-              else
-                KV_LOAD3(sK + s * L::kTile + h * L::kSub, &tm_k, bKf(s), h * 64, it.j, row0);
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+          const int n = 2 * i + kv, r = n % NR;
+          mbar_wait_sleep(bRe(r), ((n / NR) & 1) ^ 1);
+          if (elect_one()) {
+            if ((p.dbg_skip & (1 << kv)) && i >= NR) {
+              mbar_arrive(bRf(r));
+            } else {
+              mbar_arrive_expect_tx(bRf(r), L::kTile);
+              for (int h = 0; h < L::kHalves; ++h) {
+                if (kt.kind == 1)
+                  KV_LOAD4(sR(r) + h * L::kSub, &tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv);
+                else
+                  KV_LOAD3(sR(r) + h * L::kSub, kv ? &tm_v : &tm_k, bRf(r), h * 64, it.j, row0);
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
-        mbar_wait_sleep(bVe(s), ph ^ 1);
-        if (elect_one()) {
-          if ((p.dbg_skip & 2) && i >= KS) {
-            mbar_arrive(bVf(s));
-          } else {
-            mbar_arrive_expect_tx(bVf(s), L::kTile);
-            for (int h = 0; h < L::kHalves; ++h) {
-              if (kt.kind == 1)
-                KV_LOAD4(sV + s * L::kTile + h * L::kSub, &tm_g, bVf(s), h * 64, kt.c * BN, it.j, kt.slot * 2 + 1);
-              else
-                KV_LOAD3(sV + s * L::kTile + h * L::kSub, &tm_v, bVf(s), h * 64, it.j, row0);
-            }
-          }
-        }
-        __syncwarp();
       }
     } else if (warp == kMmaWarp) {
       // ============================================================== MMA issuer (warp-converged,
@@ -302,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k / 4) * L::kSub + (k % 4) * 32;
             mma_ss(tmem + t * 128, sdesc_sw128(sQ + t * L::kTile + off, 16, 1024),
-                   sdesc_sw128(sK + s * L::kTile + off, 16, 1024), idS, k > 0);
+                   sdesc_sw128(sR(s) + off, 16, 1024), idS, k > 0);
           }
           mma_commit(bS(t));
         }
@@ -319,14 +311,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_PV = [&](int t, int s, bool acc, uint32_t parity) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
+#ifdef APB_MMA_SPIN
+          mbar_wait(bP(t, half), parity);
+#else
           mbar_wait_sleep(bP(t, half), parity);
+#endif
           TRACE(2 + 2 * t + half, trace_i);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
             for (int k = half * (BN / 32); k < (half + 1) * (BN / 32); ++k) {
               mma_ts(tmem + 256 + t * D, tmem + t * 128 + k * 8,
-                     sdesc_sw128(sV + s * L::kTile + k * 2048, L::kSub, 1024), idPV, (acc || k > 0) ? 1u : 0u);
+                     sdesc_sw128(sR(s) + k * 2048, L::kSub, 1024), idPV, (acc || k > 0) ? 1u : 0u);
             }
           }
           __syncwarp();
@@ -337,34 +333,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       for (int i = 0; i < it.nkv; ++i) {
         trace_i = i;
-        const int s = i % KS;
-        const uint32_t ph = (i / KS) & 1;
+        const int nK = 2 * i, nV = 2 * i + 1, nK1 = 2 * i + 2;  // ring sequence numbers
         if (i == 0) {
-          mbar_wait_sleep(bKf(s), ph);
+          mbar_wait_sleep(bRf(nK % NR), (nK / NR) & 1);
           tc_fence_after();
           for (int t = 0; t < it.ntiles; ++t) {
             TRACE(t, 0);
-            issue_S(t, s);
+            issue_S(t, nK % NR);
           }
-          commit(bKe(s));
+          commit(bRe(nK % NR));
         }
-        mbar_wait_sleep(bVf(s), ph);
+        mbar_wait_sleep(bRf(nV % NR), (nV / NR) & 1);
         TRACE(12, i);
         tc_fence_after();
-        const int s1 = (i + 1) % KS;
-        const uint32_t ph1 = ((i + 1) / KS) & 1;
         for (int t = 0; t < it.ntiles; ++t) {
-          issue_PV(t, s, carry || i > 0, i & 1);
-          if (t == it.ntiles - 1) commit(bVe(s));
+          issue_PV(t, nV % NR, carry || i > 0, i & 1);
+          if (t == it.ntiles - 1) commit(bRe(nV % NR));
           if (i + 1 < it.nkv) {
             if (t == 0) {
-              mbar_wait_sleep(bKf(s1), ph1);
+              mbar_wait_sleep(bRf(nK1 % NR), (nK1 / NR) & 1);
               TRACE(13, i + 1);
               tc_fence_after();
             }
             TRACE(t, i + 1);
-            issue_S(t, s1);
-            if (t == it.ntiles - 1) commit(bKe(s1));
+            issue_S(t, nK1 % NR);
+            if (t == it.ntiles - 1) commit(bRe(nK1 % NR));
           } else {
             commit(bO(t));
           }

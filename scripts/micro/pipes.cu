@@ -20,6 +20,13 @@ __global__ void k(float* out, int iters) {
       if (OP == 6) a[i] = a[i] + 1e-4f;
       if (OP == 7) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u[i]));
       if (OP == 8) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i]));
+      if (OP == 10) { uint32_t r; asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+                      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[(i+1)&7]), "f"(a[(i+2)&7])); u[i] ^= r; }
+      if (OP == 11) { uint32_t r; asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+                      asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(a[(i+1)&7])), "r"(__float_as_uint(a[(i+2)&7]))); u[i] ^= r; }
+      if (OP == 12) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+                      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[i]) : "l"(m), "l"(c)); }
+      if (OP == 13) { uint32_t r; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[(i+1)&7]), "f"(a[(i+2)&7])); u[i] ^= r; }
       if (OP == 9) { uint32_t r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[(i+1)&7])); u[i] ^= r; a[i] += 1e-7f; }
     }
   }
@@ -30,9 +37,9 @@ int main() {
   float* out; cudaMalloc(&out, 4);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  const char* names[] = {"FFMA", "FFMA2", "FADD2", "MUFU.EX2", "F2FP.BF16x2", "FMNMX3", "FADD", "EX2.F16x2", "EX2.BF16x2", "F2FP.F16x2"};
+  const char* names[] = {"FFMA", "FFMA2", "FADD2", "MUFU.EX2", "F2FP.BF16x2", "FMNMX3", "FADD", "EX2.F16x2", "EX2.BF16x2", "F2FP.F16x2", "EX2+F2FP(it)", "EX2+PRMT(it)", "EX2+FFMA2(it)", "F2FP+LOP(it)"};
   const int iters = 4096;
-  for (int op = 0; op < 10; ++op) {
+  for (int op = 3; op < 14; ++op) { if (op > 3 && op < 10) continue;
     for (int warps : {4, 8, 16}) {
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       auto launch = [&]() {
@@ -40,7 +47,9 @@ int main() {
                       case 2: k<2><<<sms, 32*warps>>>(out, iters); break; case 3: k<3><<<sms, 32*warps>>>(out, iters); break;
                       case 4: k<4><<<sms, 32*warps>>>(out, iters); break; case 5: k<5><<<sms, 32*warps>>>(out, iters); break;
                       case 6: k<6><<<sms, 32*warps>>>(out, iters); break; case 7: k<7><<<sms, 32*warps>>>(out, iters); break;
-                      case 8: k<8><<<sms, 32*warps>>>(out, iters); break; case 9: k<9><<<sms, 32*warps>>>(out, iters); break; }
+                      case 8: k<8><<<sms, 32*warps>>>(out, iters); break; case 9: k<9><<<sms, 32*warps>>>(out, iters); break;
+                      case 10: k<10><<<sms, 32*warps>>>(out, iters); break; case 11: k<11><<<sms, 32*warps>>>(out, iters); break;
+                      case 12: k<12><<<sms, 32*warps>>>(out, iters); break; case 13: k<13><<<sms, 32*warps>>>(out, iters); break; }
       };
       launch(); cudaDeviceSynchronize();
       cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
