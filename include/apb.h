@@ -137,6 +137,37 @@ apb_status apb_random_scores(const apb_dims* dims, uint64_t seed, int32_t layer,
                              apb_stream_t stream);
 apb_status apb_share_scores(const apb_dims* dims, float* scores, apb_stream_t stream);
 
+/* ---------------------------------------------------------------- model layer (NEXT #2)
+ * The model steps of Alg. apb_prefill around the hot path: qkv_proj and
+ * FFN of a Llama-style decoder layer (the paper's backbones).  All tensors
+ * are caller-owned bf16 device rows (16-byte aligned, row strides in ELEMENTS, multiples of
+ * 8); element math is fp32 and each output is rounded once to bf16 (reading G9).  rows == 0
+ * is a no-op.  Errors: APB_ERR_CONFIG for bad sizes, APB_ERR_CONTRACT for bad pointers or
+ * strides (both before any launch), APB_ERR_CUDA for launch / cuBLASLt failures.
+ *
+ * apb_rmsnorm — out[r] = x[r] / sqrt(mean(x[r]^2) + eps) * w   (w: bf16 [dim]; dim % 8 == 0).
+ *   x and out may alias (same rows, same stride).
+ * apb_rope — in place on rows of x: for each of the n_heads consecutive heads (head_dim
+ *   elements each) of row r, the pairs (x_i, x_{i+d/2}), i < d/2, are rotated by angle
+ *   pos(r) * theta^(-2i/d) (rotate-half RoPE as in Llama).  pos(r) = positions[r] (int32
+ *   device array) or, if positions == NULL, pos_offset + r (reading G19: the host's local row
+ *   index, so the anchor gets the starting positions 0..l_q+l_a-1 of P:160).  Angles are
+ *   reduced in fp64.  head_dim even and <= 256.
+ * apb_swiglu — out[r][c] = SiLU(gu[r][c]) * gu[r][inter + c]   (inter % 8 == 0).
+ * apb_gemm_bf16 — C[M][N] = A[M][K] W[N][K]^T + beta * C (fp32 accumulate; beta = 1 adds the
+ *   residual in place).  A plain library GEMM (cuBLASLt); ws: optional caller workspace.
+ *   With beta != 0 the result is bf16(beta * C + bf16(A W^T)) — the product is rounded before
+ *   the add, exactly as a bf16 PyTorch residual add (reading G20).                        */
+apb_status apb_rmsnorm(int64_t rows, int32_t dim, const void* x, int64_t x_stride, const void* w, float eps,
+                       void* out, int64_t out_stride, apb_stream_t stream);
+apb_status apb_rope(int64_t rows, int32_t n_heads, int32_t head_dim, void* x, int64_t row_stride,
+                    const int32_t* positions, int64_t pos_offset, float theta, apb_stream_t stream);
+apb_status apb_swiglu(int64_t rows, int32_t inter, const void* gu, int64_t gu_stride, void* out,
+                      int64_t out_stride, apb_stream_t stream);
+apb_status apb_gemm_bf16(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w,
+                         int64_t ldw, void* c, int64_t ldc, float beta, void* ws, size_t ws_bytes,
+                         apb_stream_t stream);
+
 /* ---------------------------------------------------------------- step 3: exchange
  * One in-place AllGather of the packed compressed blocks over NCCL (the
  * paper's two AllGathers of K and V are fused into one, reading G11).

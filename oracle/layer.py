@@ -18,7 +18,9 @@ its index in the host's local sequence, so the anchor gets the starting position
     g|u = RMSNorm(x') * w_ffn_norm  W_gu^T ;  a = SiLU(g) * u
     out = x' + a W_down^T
 
-`rnd=True` rounds to bf16 at the points where the GPU path stores bf16 (reading G9); with
+`rnd=True` rounds to bf16 at the points where the GPU path stores bf16 (readings G9, G20:
+every linear output, norm output, activation and residual sum, as in a bf16 PyTorch Llama
+layer); with
 `rnd=False` every step is exact fp64 (the form pinned against transformers' LlamaDecoderLayer
 in tests/test_oracle_layer.py).
 """
@@ -83,11 +85,13 @@ def attn_out_ffn(x, attn, lw: dict, rnd: bool = True) -> np.ndarray:
     attn: [rows][hq][d] attention output."""
     x = np.asarray(x, np.float64)
     a = np.asarray(attn, np.float64).reshape(x.shape[0], -1)
-    x1 = _r(x + a @ np.asarray(lw["w_o"], np.float64).T, rnd)
+    # reading G20: as in a bf16 PyTorch Llama layer, each projection output is a bf16 tensor
+    # that is then added to the bf16 residual (two roundings per residual add)
+    x1 = _r(x + _r(a @ np.asarray(lw["w_o"], np.float64).T, rnd), rnd)
     h2 = _r(rmsnorm(x1, lw["ffn_norm"], lw["eps"]), rnd)
     gu = _r(h2 @ np.asarray(lw["w_gu"], np.float64).T, rnd)
     act = _r(swiglu(gu, gu.shape[-1] // 2), rnd)
-    return _r(x1 + act @ np.asarray(lw["w_down"], np.float64).T, rnd)
+    return _r(x1 + _r(act @ np.asarray(lw["w_down"], np.float64).T, rnd), rnd)
 
 
 def apb_layer(hosts_x, L_As, lw: dict, retain: dict, l_p: int, hq: int, hk: int, d: int, rnd: bool = True,

@@ -85,8 +85,12 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_merge_partials.argtypes = [i32, i64, i32, vp, i64, vp, i64, vp, vp, vp]
     lib.apb_exchange_partials.argtypes = [vp, i64, vp, vp]
     lib.apb_random_scores.argtypes = [dp, ctypes.c_uint64, i32, vp, vp]
+    lib.apb_rmsnorm.argtypes = [i64, i32, vp, i64, vp, ctypes.c_float, vp, i64, vp]
+    lib.apb_rope.argtypes = [i64, i32, i32, vp, i64, vp, i64, ctypes.c_float, vp]
+    lib.apb_swiglu.argtypes = [i64, i32, vp, i64, vp, i64, vp]
+    lib.apb_gemm_bf16.argtypes = [i64, i32, i32, vp, i64, vp, i64, vp, i64, ctypes.c_float, vp, sz, vp]
     lib.apb_share_scores.argtypes = [dp, vp, vp]
-    for f in ("apb_random_scores", "apb_share_scores", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
+    for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials"):
@@ -241,6 +245,34 @@ def attention_fwd(dims: Dims, q, k, v, gathered, out, lse=None, phase: int = PHA
                                     _rowstride(k, "k"), _ptr(gathered), out.data_ptr(), _rowstride(out, "out"),
                                     _ptr(lse), phase, _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                                     _stream(stream)), "apb_attention_fwd")
+
+
+# ----------------------------------------------------------------------------- model layer (NEXT #2)
+
+def rmsnorm(x, w, eps: float, out, stream=None) -> None:
+    """out = RMSNorm(x) * w over the last dim (x, out: bf16 [rows][dim] row-strided views)."""
+    _check(load().apb_rmsnorm(x.shape[0], x.shape[-1], x.data_ptr(), _rowstride(x, "x"), w.data_ptr(), eps,
+                              out.data_ptr(), _rowstride(out, "out"), _stream(stream)), "apb_rmsnorm")
+
+
+def rope(x, n_heads: int, head_dim: int, theta: float, positions=None, pos_offset: int = 0, stream=None) -> None:
+    """In-place RoPE on the first n_heads heads of every row of x (bf16 [rows][>= n_heads*head_dim])."""
+    _check(load().apb_rope(x.shape[0], n_heads, head_dim, x.data_ptr(), x.stride(0), _ptr(positions), pos_offset,
+                           theta, _stream(stream)), "apb_rope")
+
+
+def swiglu(gu, out, stream=None) -> None:
+    """out = SiLU(gu[:, :I]) * gu[:, I:] with I = out.shape[-1]."""
+    _check(load().apb_swiglu(gu.shape[0], out.shape[-1], gu.data_ptr(), _rowstride(gu, "gu"), out.data_ptr(),
+                             _rowstride(out, "out"), _stream(stream)), "apb_swiglu")
+
+
+def gemm_bf16(a, w, c, beta: float = 0.0, ws=None, stream=None) -> None:
+    """c = a @ w.T (+ beta * c): a bf16 [M][K], w bf16 [N][K], c bf16 [M][N] (row-strided views)."""
+    _check(load().apb_gemm_bf16(a.shape[0], w.shape[0], w.shape[1], a.data_ptr(), _rowstride(a, "a"), w.data_ptr(),
+                                _rowstride(w, "w"), c.data_ptr(), _rowstride(c, "c"), beta, _ptr(ws),
+                                0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+           "apb_gemm_bf16")
 
 
 class Comm:

@@ -33,7 +33,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     if not force and not trace and not _stale():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-ldl"]
+    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-ldl", "-lcublasLt"]
     if trace:
         cmd.insert(1, "-DAPB_TRACE")
     if verbose:

@@ -330,6 +330,68 @@ extern "C" apb_status apb_share_scores(const apb_dims* d, float* scores, apb_str
   return launch_share_scores(scores, d->n_kv_heads, d->l_b, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- model layer (NEXT #2)
+namespace {
+apb_status check_bf16_rows(const void* p, int64_t rows, int64_t stride, int64_t width, const char* what) {
+  if (rows == 0) return APB_OK;
+  if (!p || !aligned16(p)) return fail(APB_ERR_CONTRACT, std::string(what) + " NULL or not 16-byte aligned");
+  if (stride % 8 != 0 || stride < width)
+    return fail(APB_ERR_CONTRACT, std::string(what) + " row stride must be a multiple of 8 elements and >= width");
+  return APB_OK;
+}
+}  // namespace
+
+extern "C" apb_status apb_rmsnorm(int64_t rows, int32_t dim, const void* x, int64_t x_stride, const void* w, float eps,
+                                  void* out, int64_t out_stride, apb_stream_t stream) {
+  if (rows < 0 || dim <= 0 || dim % 8 != 0 || !(eps >= 0.f)) return fail(APB_ERR_CONFIG, "rmsnorm: rows >= 0, dim % 8 == 0, eps >= 0");
+  apb_status st;
+  if ((st = check_bf16_rows(x, rows, x_stride, dim, "x"))) return st;
+  if ((st = check_bf16_rows(out, rows, out_stride, dim, "out"))) return st;
+  if (!w || !aligned16(w)) return fail(APB_ERR_CONTRACT, "w NULL or not 16-byte aligned");
+  if (rows == 0) return APB_OK;
+  if ((st = check_device())) return st;
+  return launch_rmsnorm(rows, dim, x, x_stride, w, eps, out, out_stride, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_rope(int64_t rows, int32_t n_heads, int32_t head_dim, void* x, int64_t row_stride,
+                               const int32_t* positions, int64_t pos_offset, float theta, apb_stream_t stream) {
+  if (rows < 0 || n_heads < 0 || head_dim <= 0 || head_dim % 2 != 0 || head_dim > 256 || !(theta > 0.f))
+    return fail(APB_ERR_CONFIG, "rope: rows, n_heads >= 0, even head_dim <= 256, theta > 0");
+  if (rows == 0 || n_heads == 0) return APB_OK;
+  if (!x) return fail(APB_ERR_CONTRACT, "x NULL");
+  if (row_stride < (int64_t)n_heads * head_dim) return fail(APB_ERR_CONTRACT, "row_stride < n_heads * head_dim");
+  apb_status st;
+  if ((st = check_device())) return st;
+  return launch_rope(rows, n_heads, head_dim, x, row_stride, positions, pos_offset, (double)theta,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_swiglu(int64_t rows, int32_t inter, const void* gu, int64_t gu_stride, void* out,
+                                 int64_t out_stride, apb_stream_t stream) {
+  if (rows < 0 || inter <= 0 || inter % 8 != 0) return fail(APB_ERR_CONFIG, "swiglu: rows >= 0, inter % 8 == 0");
+  apb_status st;
+  if ((st = check_bf16_rows(gu, rows, gu_stride, 2 * (int64_t)inter, "gu"))) return st;
+  if ((st = check_bf16_rows(out, rows, out_stride, inter, "out"))) return st;
+  if (rows == 0) return APB_OK;
+  if ((st = check_device())) return st;
+  return launch_swiglu(rows, inter, gu, gu_stride, out, out_stride, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_gemm_bf16(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w,
+                                    int64_t ldw, void* c, int64_t ldc, float beta, void* ws, size_t ws_bytes,
+                                    apb_stream_t stream) {
+  if (M < 0 || N <= 0 || K <= 0 || N % 8 != 0 || K % 8 != 0)
+    return fail(APB_ERR_CONFIG, "gemm: M >= 0, N and K positive multiples of 8");
+  apb_status st;
+  if ((st = check_bf16_rows(a, M, lda, K, "a"))) return st;
+  if ((st = check_bf16_rows(w, N, ldw, K, "w"))) return st;
+  if ((st = check_bf16_rows(c, M, ldc, N, "c"))) return st;
+  if (ws_bytes && !ws) return fail(APB_ERR_CONTRACT, "ws NULL with ws_bytes > 0");
+  if (M == 0) return APB_OK;
+  if ((st = check_device())) return st;
+  return launch_gemm_bf16(M, N, K, a, lda, w, ldw, c, ldc, beta, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
 // ---------------------------------------------------------------- step 3: exchange (NCCL)
 struct apb_comm {
   ncclComm_t comm;

@@ -1,0 +1,230 @@
+// layer_ops.cu — the model steps of Alg. apb_prefill around the hot path (SURVEY.md 8(f)
+// NEXT #2): qkv_proj and FFN of a Llama-style decoder layer.
+//
+//   rmsnorm_kernel  y = x / sqrt(mean(x^2) + eps) * w          HBM-bound: 4*dim B per row
+//   rope_kernel     in-place rotate-half RoPE on the Q and K heads of each qkv row (reading
+//                   G19: position = caller array, or pos_offset + row)   HBM-bound
+//   swiglu_kernel   a = SiLU(g) * u for [g | u] rows                      HBM-bound
+//   apb_gemm_bf16   C = A W^T (+ beta C): cuBLASLt, bf16 in / fp32 accumulate / bf16 out — a
+//                   plain library GEMM (the projections carry no APB-specific structure)
+//
+// All element math is fp32; every output is rounded once to bf16 (reading G9).
+#include <cublasLt.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace apb {
+namespace layer {
+
+__device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
+__device__ __forceinline__ uint16_t f2bf(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = static_cast<uint32_t>(f2bf(f[2 * i])) | (static_cast<uint32_t>(f2bf(f[2 * i + 1])) << 16);
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// One 256-thread CTA per row; dim % 8 == 0.  Sum of squares in fp32 (fixed-order warp + CTA
+// reduction), then the row is re-read (L1/L2-hot) and normalised.
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const uint16_t* __restrict__ x, int64_t xs,
+                                                      const uint16_t* __restrict__ w, int dim, float eps,
+                                                      uint16_t* __restrict__ y, int64_t ys) {
+  const int64_t row = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * xs);
+  const int nv = dim / 8;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < nv; i += 256) {
+    float f[8];
+    unpack8(__ldg(xr + i), f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  __shared__ float part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) tot += part[i];
+  const float inv = rsqrtf(tot / static_cast<float>(dim) + eps);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * ys);
+  for (int i = threadIdx.x; i < nv; i += 256) {
+    float f[8], g[8];
+    unpack8(__ldg(xr + i), f);
+    unpack8(__ldg(wr + i), g);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = f[e] * inv * g[e];
+    yr[i] = pack8(f);
+  }
+}
+
+// One CTA per row: the d/2 angles pos * theta^(-2i/d) are formed and reduced mod 2*pi in fp64
+// (positions reach 10^6: fp32 angles would be off by O(0.1) rad), then sin/cos in fp32; every
+// thread rotates pairs (x_i, x_{i+d/2}) of all n_heads heads with the shared table.
+__global__ void __launch_bounds__(256) rope_kernel(uint16_t* __restrict__ x, int64_t row_stride, int n_heads, int d,
+                                                   const int32_t* __restrict__ positions, int64_t pos_offset,
+                                                   double log2_theta) {
+  __shared__ float cs[2][128];
+  const int64_t row = blockIdx.x;
+  const int half = d / 2;
+  const double pos = positions ? static_cast<double>(positions[row]) : static_cast<double>(pos_offset + row);
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const double inv = exp2(-log2_theta * (2.0 * i) / d);
+    double a = pos * inv;
+    a -= rint(a * 0.15915494309189535) * 6.283185307179586;  // |a| <= pi
+    float s, c;
+    sincosf(static_cast<float>(a), &s, &c);
+    cs[0][i] = c;
+    cs[1][i] = s;
+  }
+  __syncthreads();
+  uint16_t* xr = x + row * row_stride;
+  for (int t = threadIdx.x; t < n_heads * half; t += blockDim.x) {
+    const int h = t / half, i = t % half;
+    uint16_t* p = xr + h * d;
+    const float x1 = bf2f(p[i]), x2 = bf2f(p[i + half]);
+    const float c = cs[0][i], s = cs[1][i];
+    p[i] = f2bf(x1 * c - x2 * s);
+    p[i + half] = f2bf(x2 * c + x1 * s);
+  }
+}
+
+// a = SiLU(g) * u, 8 elements per thread; inter % 8 == 0.
+__global__ void __launch_bounds__(256) swiglu_kernel(const uint16_t* __restrict__ gu, int64_t gs, int inter,
+                                                     uint16_t* __restrict__ out, int64_t os, int64_t rows) {
+  const int nv = inter / 8;
+  const int64_t total = rows * nv;
+  for (int64_t t = blockIdx.x * 256ll + threadIdx.x; t < total; t += (int64_t)gridDim.x * 256) {
+    const int64_t r = t / nv;
+    const int c = static_cast<int>(t % nv);
+    const uint4* g = reinterpret_cast<const uint4*>(gu + r * gs);
+    float fg[8], fu[8];
+    unpack8(__ldg(g + c), fg);
+    unpack8(__ldg(g + nv + c), fu);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) fg[e] = fg[e] / (1.f + __expf(-fg[e])) * fu[e];
+    reinterpret_cast<uint4*>(out + r * os)[c] = pack8(fg);
+  }
+}
+
+}  // namespace layer
+
+apb_status launch_rmsnorm(int64_t rows, int dim, const void* x, int64_t xs, const void* w, float eps, void* y,
+                          int64_t ys, cudaStream_t stream) {
+  layer::rmsnorm_kernel<<<(unsigned)rows, 256, 0, stream>>>(static_cast<const uint16_t*>(x), xs,
+                                                           static_cast<const uint16_t*>(w), dim, eps,
+                                                           static_cast<uint16_t*>(y), ys);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("rmsnorm launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+apb_status launch_rope(int64_t rows, int n_heads, int d, void* x, int64_t row_stride, const int32_t* positions,
+                       int64_t pos_offset, double theta, cudaStream_t stream) {
+  layer::rope_kernel<<<(unsigned)rows, 256, 0, stream>>>(static_cast<uint16_t*>(x), row_stride, n_heads, d, positions,
+                                                        pos_offset, log2(theta));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("rope launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+apb_status launch_swiglu(int64_t rows, int inter, const void* gu, int64_t gs, void* out, int64_t os,
+                         cudaStream_t stream) {
+  const int64_t work = rows * (inter / 8);
+  int64_t blocks = (work + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  layer::swiglu_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(gu), gs, inter,
+                                                            static_cast<uint16_t*>(out), os, rows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("swiglu launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+// ---------------------------------------------------------------- cuBLASLt GEMM
+namespace {
+struct GemmKey {
+  int64_t M, lda, ldw, ldc;
+  int32_t N, K;
+  bool beta;
+  size_t ws;
+  bool operator==(const GemmKey& o) const {
+    return M == o.M && lda == o.lda && ldw == o.ldw && ldc == o.ldc && N == o.N && K == o.K && beta == o.beta &&
+           ws == o.ws;
+  }
+};
+struct GemmKeyHash {
+  size_t operator()(const GemmKey& k) const {
+    size_t h = std::hash<int64_t>()(k.M);
+    for (int64_t v : {k.lda, k.ldw, k.ldc, (int64_t)k.N, (int64_t)k.K, (int64_t)k.beta, (int64_t)k.ws})
+      h = h * 1000003u ^ std::hash<int64_t>()(v);
+    return h;
+  }
+};
+struct GemmPlan {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  cublasLtMatmulAlgo_t algo;
+};
+std::mutex g_gemm_mu;
+cublasLtHandle_t g_lt = nullptr;
+std::unordered_map<GemmKey, GemmPlan, GemmKeyHash> g_plans;
+}  // namespace
+
+apb_status launch_gemm_bf16(int64_t M, int N, int K, const void* a, int64_t lda, const void* w, int64_t ldw, void* c,
+                            int64_t ldc, float beta, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  // Row-major C[M][N] = A[M][K] W[N][K]^T  <=>  column-major C^T (N x M) = W^T(op T on the
+  // K x N column-major view of W) * A (K x M column-major view of A).
+  std::lock_guard<std::mutex> lock(g_gemm_mu);
+  if (!g_lt && cublasLtCreate(&g_lt) != CUBLAS_STATUS_SUCCESS) return fail(APB_ERR_CUDA, "cublasLtCreate failed");
+  const GemmKey key{M, lda, ldw, ldc, N, K, beta != 0.f, ws_bytes};
+  auto it = g_plans.find(key);
+  if (it == g_plans.end()) {
+    GemmPlan pl;
+    bool ok = cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS;
+    const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+    ok = ok && cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)) == CUBLAS_STATUS_SUCCESS;
+    ok = ok && cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)) == CUBLAS_STATUS_SUCCESS;
+    ok = ok && cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_16BF, K, N, ldw) == CUBLAS_STATUS_SUCCESS;
+    ok = ok && cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_16BF, K, M, lda) == CUBLAS_STATUS_SUCCESS;
+    ok = ok && cublasLtMatrixLayoutCreate(&pl.c, CUDA_R_16BF, N, M, ldc) == CUBLAS_STATUS_SUCCESS;
+    cublasLtMatmulPreference_t pref = nullptr;
+    ok = ok && cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS;
+    ok = ok && cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes,
+                                                    sizeof(ws_bytes)) == CUBLAS_STATUS_SUCCESS;
+    cublasLtMatmulHeuristicResult_t res;
+    int n = 0;
+    ok = ok && cublasLtMatmulAlgoGetHeuristic(g_lt, pl.op, pl.a, pl.b, pl.c, pl.c, pref, 1, &res, &n) ==
+                   CUBLAS_STATUS_SUCCESS && n > 0;
+    if (pref) cublasLtMatmulPreferenceDestroy(pref);
+    if (!ok) return fail(APB_ERR_CUDA, "cuBLASLt: no bf16 GEMM algorithm for this shape");
+    pl.algo = res.algo;
+    it = g_plans.emplace(key, pl).first;
+  }
+  const GemmPlan& pl = it->second;
+  const float alpha = 1.f;
+  cublasStatus_t st = cublasLtMatmul(g_lt, pl.op, &alpha, w, pl.a, a, pl.b, &beta, c, pl.c, c, pl.c, &pl.algo, ws,
+                                     ws_bytes, stream);
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(APB_ERR_CUDA, "cublasLtMatmul failed: status " + std::to_string((int)st));
+  count_launch();
+  return APB_OK;
+}
+
+}  // namespace apb

@@ -142,6 +142,7 @@ class PrefillRank:
                 x = io[h]
                 timed(lambda: apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse,
                                                 phase=apb.PHASE_ALL, ws=self.ws[h], stream=main))
+            main.wait_stream(self.side)  # the last host's compression still reads io[h].k/v
             return
         self.side.wait_stream(main)  # this layer's inputs are produced on the main stream
         self.compress(io, weights, self.side, layer_idx)
@@ -151,7 +152,9 @@ class PrefillRank:
         main.wait_event(self.ev_exchanged)
         timed(lambda: self.attention(io, apb.PHASE_PASSING, main))
         # the side stream's buffers (scores, gathered) are reused next layer only after main
-        # has consumed them: next layer's side.wait_stream(main) orders that.
+        # has consumed them: next layer's side.wait_stream(main) orders that.  Conversely the
+        # caller may overwrite io's Q/K/V once main is past this point.
+        main.wait_stream(self.side)
 
 
 def hosts_of_rank(H: int, world: int, rank: int) -> list[int]:

@@ -228,3 +228,46 @@ def random_scores(cfg: Config, layer: int, host: int, ties: bool = False) -> np.
     if ties:
         s = np.round(s * 4.0).astype(np.float32) / 4.0
     return s
+
+
+# ----------------------------------------------------------------------------- model layer (NEXT #2)
+_T_HID, _T_QHID, _T_MW = 40, 41, 50  # hidden rows, query hidden rows, model weights (+0..5)
+
+
+def model_weights(cfg: Config, layer: int, hidden: int, inter: int) -> dict:
+    """Random-init Llama-style decoder-layer weights (bf16 bits, nn.Linear layout [out][in]):
+    projections ~ N(0, 1/fan_in) so activations stay O(1); norm weights ~ 1 + N(0, 0.1^2)."""
+    hq, hk, d = cfg.hq, cfg.hk, cfg.d
+
+    def lin(k, n_out, n_in):
+        w = _rng(cfg, layer, _T_MW + k, 0).standard_normal((n_out, n_in), dtype=np.float32) / np.sqrt(n_in)
+        return f32_to_bf16_bits(w)
+
+    def norm(k):
+        return f32_to_bf16_bits(1.0 + 0.1 * _rng(cfg, layer, _T_MW + k, 0).standard_normal(hidden, dtype=np.float32))
+
+    return {"attn_norm": norm(0), "w_qkv": lin(1, (hq + 2 * hk) * d, hidden), "w_o": lin(2, hidden, hq * d),
+            "ffn_norm": norm(3), "w_gu": lin(4, 2 * inter, hidden), "w_down": lin(5, hidden, inter)}
+
+
+def host_hidden(cfg: Config, host: int, hidden: int) -> np.ndarray:
+    """bf16 bits [L_A + l_b][hidden] of host `host`'s input hidden states [A; B_h] (the layout of
+    host_qkv: anchor = query rows then the document's first l_a rows, block = its document
+    block).  Document and query rows ~ N(0, 1), chunked by CHUNK rows like doc_rows."""
+    L_A = cfg.L_A(host)
+
+    def doc(r0, r1):
+        out = np.empty((r1 - r0, hidden), np.float32)
+        for c in range(r0 // CHUNK, (r1 - 1) // CHUNK + 1 if r1 > r0 else 0):
+            g = _rng(cfg, 0, _T_HID, c).standard_normal((CHUNK, hidden), dtype=np.float32)
+            lo, hi = max(r0, c * CHUNK), min(r1, (c + 1) * CHUNK)
+            out[lo - r0:hi - r0] = g[lo - c * CHUNK:hi - c * CHUNK]
+        return out
+
+    parts = []
+    if L_A:
+        if cfg.l_q:
+            parts.append(_rng(cfg, 0, _T_QHID, 0).standard_normal((cfg.l_q, hidden), dtype=np.float32))
+        parts.append(doc(0, cfg.l_a))
+    parts.append(doc(host * cfg.l_b, (host + 1) * cfg.l_b))
+    return f32_to_bf16_bits(np.concatenate(parts))
