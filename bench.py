@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["apb", "reference"], default="apb")
+    ap.add_argument("--workload", choices=["hotpath", "model"], default="hotpath",
+                    help="model: the full decoder stack around the hot path (bench_model.py, NEXT #2)")
     ap.add_argument("--config", default="llama8b-128k")
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (default: the model's)")
     ap.add_argument("--hosts", type=int, default=None, help="override H (default: the paper's 8)")
@@ -206,6 +208,10 @@ def workload_config(cfg, H, layers, n_gpus):
 
 def main():
     args = parse()
+    if args.workload == "model":
+        import bench_model
+        bench_model.main(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -324,7 +330,8 @@ def main():
         traffic = json.load(open(tpath)).get(args.config, {}).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
-                "kernel": "apb_attention_kernel<128> (LOCAL + PASSING launches)",
+                "kernel": "apb_attention_kernel<128> (" + ("LOCAL + PASSING launches" if pr.split_phases
+                                                           else "one ordered PHASE_ALL launch per host") + ")",
                 "peak_source": f"bf16_tflops_sustained, {peak_src}",
                 "flops_per_step": flops_rank * layers,
                 "attn_ms_per_step": round(attn_ms / args.steps, 3)}
