@@ -124,9 +124,18 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int w) {
     it.seg = 0;
     nrt = p.nA_rt;
   }
+  const int units = nrt * p.g;
+#ifdef APB_HEAD_MINOR
   it.j = w % p.hk;
   const int pidx = w / p.hk;
-  const int units = nrt * p.g;
+#else
+  // KV-head-major order (heaviest row tiles first within a head): the CTAs resident at any
+  // time share one or two KV heads, so the K/V tiles they walk stay L2-resident instead of
+  // every head's K/V (> L2 at 128K) streaming from HBM once per item
+  const int per_head = (units + 1) / 2;
+  it.j = w / per_head;
+  const int pidx = w % per_head;
+#endif
   it.ntiles = 0;
   for (int t = 0; t < 2; ++t) {
     const int u = 2 * pidx + t;

@@ -9,3 +9,5 @@ timeout -k 10 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun
 timeout -k 10 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s_launches.csv python bench.py --layers 2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/s_ncu_list.log 2>&1; echo "NCU1 $?"
 timeout -k 10 900 ncu --set full --clock-control none --import-source on -k regex:apb_attention -c 15 -o gpurun_out/s_attn_full python bench.py --layers 1 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/s_ncu_full.log 2>&1; echo "NCU2 $?"
 timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:"retain|select|compact" -c 3 -o gpurun_out/s_aux_full python bench.py --layers 1 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/s_ncu_aux.log 2>&1; echo "NCU3 $?"
+timeout -k 10 900 python bench.py --workload model > gpurun_out/s_bench_model.json 2> gpurun_out/s_bench_model.err; echo "MODEL $?"
+timeout -k 10 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s_model_launches.csv python bench.py --workload model --layers 2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/s_ncu_model.log 2>&1; echo "NCU4 $?"

@@ -22,10 +22,11 @@ def launches(path):
             continue
         name = r[ki].split("(")[0]
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+              "second": 1e6, "s": 1e6}.get(r[ui], 1.0)
         agg[name][0] += 1
         agg[name][1] += v
-    ours = {k: v for k, v in agg.items() if any(s in k for s in ("apb", "attn::", "score::", "sel::"))}
+    ours = {k: v for k, v in agg.items() if any(s in k for s in ("apb", "attn::", "score::", "sel::", "layer::", "dec::"))}
     tot = sum(v for _, v in agg.values())
     tot_ours = sum(v for _, v in ours.values())
     print(f"# ncu launch list ({path}); gpu__time_duration.sum, --clock-control none, serialised + cold-cache")

@@ -190,3 +190,25 @@ def test_shared_index_set_layer(compressor):
         O_or, lse_or = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv)
         check_attention(io[h].out.float().cpu().double().numpy(), io[h].lse.cpu().double().numpy().T,
                         O_or, lse_or, f"shared {compressor} host {h}")
+
+
+# ----------------------------------------------------------------------------- comparison systems
+
+@pytest.mark.parametrize("mode", ["ordered", "split"])
+def test_ring_mapping_equals_full_causal(mode):
+    """RingAttn as APB parameters (scripts/method_table.py, NEXT #4): with no anchor and
+    l_p = l_b every earlier block passes whole and in order, so host h's rows equal rows
+    [h l_b, (h+1) l_b) of plain causal attention over the whole document — the selection,
+    compaction, exchange and masked attention all run."""
+    cfg = synth.Config("ring", 22, n=1024, H=4, l_a=0, l_p=256, hq=4, hk=2, d=64, d_hidden=1024)
+    hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    w = synth.retain_weights(cfg, 0)
+    rank, io = _run_layer(cfg, hosts, "retain", False, mode, w)
+    full = {k: np.concatenate([hh[k] for hh in hosts]) for k in ("q", "k", "v")}
+    empty = np.zeros((0, cfg.hk, cfg.d), np.uint16)
+    for h in range(cfg.H):
+        assert np.array_equal(rank.indices[h].cpu().numpy(), np.tile(np.arange(cfg.l_b), (cfg.hk, 1)))
+        rows = np.arange(h * cfg.l_b, (h + 1) * cfg.l_b)
+        O_or, lse_or = oracle.attention(full["q"], full["k"], full["v"], 0, empty, empty, rows=rows)
+        check_attention(io[h].out.float().cpu().double().numpy(), io[h].lse.cpu().double().numpy().T, O_or, lse_or,
+                        f"ring host {h}")
