@@ -220,8 +220,12 @@ typedef struct {
 /* Partial attention of host `host`: q bf16 [t_new][n_heads][head_dim]; k_new/v_new bf16
  * [t_new][n_kv_heads][head_dim] (row stride new_row_stride; read only when host == H-1, may be
  * NULL otherwise).  Writes part_o fp32 [t_new][n_heads][head_dim] (normalised) and part_lse fp32
- * [t_new][n_heads] (natural log; -inf for a row that sees no key).  ws: apb_decode_workspace_size.
- * Kernel: split-KV over 256-key chunks x KV heads (memory-bound), then an LSE fold of the chunks. */
+ * [t_new][n_heads] (natural log; -inf for a row that sees no key).  ws: apb_decode_workspace_size
+ * bytes; one workspace per concurrently running call.
+ * Kernels: split-KV over ~2 CTAs per SM x KV heads, each streaming 64-key chunks through a
+ * cp.async ring with both products on the tensor cores (mma.sync bf16, fp32 accumulate) and an
+ * online softmax across its chunks; then a log-sum-exp fold of the splits (fixed order:
+ * deterministic).                                                                              */
 apb_status apb_decode_attention(const apb_decode_dims* dims, const void* q, const void* k_cache,
                                 const void* v_cache, int64_t cache_row_stride, const void* k_new,
                                 const void* v_new, int64_t new_row_stride, float* part_o,

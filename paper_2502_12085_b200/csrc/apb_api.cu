@@ -518,7 +518,7 @@ extern "C" apb_status apb_decode_workspace_size(const apb_decode_dims* d, size_t
   if (!bytes) return fail(APB_ERR_CONTRACT, "bytes is NULL");
   apb_status st = check_decode_dims(d);
   if (st) return st;
-  *bytes = decode_workspace_bytes(decode_keys(d), d->t_new, d->n_heads, d->head_dim);
+  *bytes = decode_workspace_bytes(decode_keys(d), d->t_new, d->n_heads, d->n_kv_heads, d->head_dim);
   return APB_OK;
 }
 
@@ -540,7 +540,7 @@ extern "C" apb_status apb_decode_attention(const apb_decode_dims* d, const void*
     if ((st = check_rows(v_new, new_row_stride, (int64_t)hk * D, "v_new"))) return st;
   }
   if (!part_o || !part_lse || !aligned16(part_o)) return fail(APB_ERR_CONTRACT, "part_o/part_lse NULL or misaligned");
-  const size_t need = decode_workspace_bytes(decode_keys(d), d->t_new, hq, D);
+  const size_t need = decode_workspace_bytes(decode_keys(d), d->t_new, hq, d->n_kv_heads, D);
   if (need && (!ws || ws_bytes < need || !aligned16(ws))) return fail(APB_ERR_CONTRACT, "decode workspace missing or too small");
   if ((st = check_device())) return st;
   DecodeParams p{};

@@ -4,11 +4,10 @@
 // partial (A_h, lse_h) of every host is gathered and merged by log-sum-exp (MergeScore,
 // P:753), which makes the result exact.
 //
-// decode_split_kernel: memory-bound split-KV ("flash decoding") — grid (key chunks of 256, KV
-// heads); a CTA stages its V chunk in shared memory with coalesced 16-byte loads, each thread
-// owns one key (its K row held in registers as bf16x2), computes the logits of the t*g query
-// rows of that KV head, then the rows' softmax over the chunk and the P.V product over the
-// staged V.  Output: one normalised partial (O, log2-sum-exp) per chunk in the workspace.
+// decode_mma_kernel: memory-bound split-KV ("flash decoding") — grid (splits, KV heads), ~2
+// CTAs per SM, each streaming a contiguous range of 64-key chunks through a cp.async ring, both
+// products on the tensor cores, online softmax across its chunks.  Output: one normalised
+// partial (O, log2-sum-exp) per split in the workspace.
 // merge_kernel: log-sum-exp merge of n partials per row — used both to fold the chunks of one
 // host and, across hosts, as MergeScore.  Fixed merge order, no atomics: deterministic.
 #include "internal.h"
@@ -19,183 +18,257 @@ namespace dec {
 
 using namespace apb::sm100;
 
-constexpr int KC = 128;        // keys per CTA
-constexpr int kThreads = 128;  // == KC: one key per thread in the logit phase
-constexpr int kKPad = 16;      // bytes of padding per staged K row (conflict-free per-key reads)
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, bool valid) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem_src), "r"(valid ? 16 : 0) : "memory");
 }
 
-// shared memory: K chunk [KC][D*2 + pad] bf16, V chunk [KC][D] bf16, q rows [R][D] fp32
-// (pre-scaled), probabilities [R][KC] fp32, row stats [2][R]
-__host__ __device__ constexpr int decode_smem_bytes(int R, int D) {
-  return KC * (D * 2 + kKPad) + KC * D * 2 + R * D * 4 + R * KC * 4 + 2 * R * 4;
+// Split plan: ~kSplitTarget CTAs over (splits x KV heads), whole 64-key chunks per split.
+#ifndef APB_DEC_CTAS_PER_SM
+#define APB_DEC_CTAS_PER_SM 2
+#endif
+constexpr int SKC = 64;                                  // keys per chunk
+constexpr int kSplitTarget = APB_DEC_CTAS_PER_SM * 148;  // CTAs per launch to aim for (per SM x B200 SMs)
+
+// ---------------------------------------------------------------- tensor-core split-KV
+// decode_mma_kernel: the same streaming split-KV plan, with both products on the tensor cores
+// (mma.sync m16n8k16 bf16 -> fp32; R = t*g query rows padded to 16-row m-tiles — for this
+// HBM-bound GEMV the point is to take the bf16 unpacking and the FMAs off the CUDA cores, not
+// tensor throughput, so the legacy warp-level MMA is the right size).  Per 64-key chunk:
+//   S = Q K^T: warp w owns keys [8w, 8w+8) (one n-tile), K fragments via ldmatrix from the
+//              padded K rows; masks; row max over the chunk through shared memory;
+//   P = 2^(S - m), written as bf16 to shared memory; row sums kept per thread;
+//   O = alpha O + P V: warp w owns head_dim columns [D/8 w, D/8 (w+1)), V fragments via
+//              ldmatrix.trans; O stays in registers for the whole split.
+constexpr int MKC = SKC;        // keys per chunk
+constexpr int kMThreads = 256;  // 8 warps
+constexpr int kMStages = 3;
+
+template <int D>
+struct MmaSmem {
+  static constexpr int kRow = D + 8;                  // padded bf16 row (conflict-free ldmatrix)
+  static constexpr int kStage = 2 * MKC * kRow * 2;   // K and V chunk
+  static constexpr int kPRow = MKC + 8;
+  static constexpr int bytes(int MT) {
+    return kMStages * kStage + 16 * MT * kRow * 2 + 16 * MT * kPRow * 2 + 2 * 8 * 16 * MT * 4;
+  }
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// RT: compile-time bound on the query rows each thread accumulates in the P.V phase
-// (ceil(R / (kThreads / (D/2)))), so the accumulators stay in registers without predicated waste.
-template <int D, int RT>
-__global__ void __launch_bounds__(kThreads) decode_split_kernel(const DecodeParams p) {
+template <int D, int MT>
+__global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParams p, int chunks_per_split) {
+  using L = MmaSmem<D>;
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int kRowK = D * 2 + kKPad;
-  const int R = p.t * p.g;  // query rows of this KV head: r = s * g + gi  (new token s, head j*g+gi)
-  uint8_t* ks = smem;
-  __nv_bfloat16* vs = reinterpret_cast<__nv_bfloat16*>(smem + KC * kRowK);
-  float* qs = reinterpret_cast<float*>(smem + KC * kRowK + KC * D * 2);
-  float* ps = qs + R * D;
-  float* ms = ps + R * KC;
-  float* ls = ms + R;
-
-  const int tid = threadIdx.x;
+  constexpr int NT = D / 64;  // O n-tiles (of 8 columns) per warp: D/8 tiles over 8 warps
+  const int R = p.t * p.g;
+  __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(smem + kMStages * L::kStage);  // [16 MT][kRow]
+  __nv_bfloat16* pss = qs + 16 * MT * L::kRow;                                       // [16 MT][kPRow]
+  float* xm = reinterpret_cast<float*>(pss + 16 * MT * L::kPRow);                    // [8][16 MT]
+  float* xl = xm + 8 * 16 * MT;                                                      // [8][16 MT]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int g8 = lane / 4, t4 = lane % 4;
   const int split = blockIdx.x, j = blockIdx.y;
-  const int64_t k0 = (int64_t)split * KC;
   const int64_t n_keys = p.cache_len + (p.has_new ? p.t : 0);
-
-  // stage the chunk's K and V rows: every thread issues all of its 16-byte async copies at once.
-  // Thread tid always copies 16-byte column chunk c = tid % kVec of rows tid / kVec + i * kRowsPerPass.
+  const int64_t c_first = (int64_t)split * chunks_per_split;
+  const int64_t n_chunks_total = (n_keys + MKC - 1) / MKC;
+  const int nch = (int)((c_first + chunks_per_split <= n_chunks_total) ? chunks_per_split
+                                                                       : (n_chunks_total > c_first ? n_chunks_total - c_first : 0));
   constexpr int kVec = D / 8;
-  constexpr int kRowsPerPass = kThreads / kVec;
-  {
-    const int c = tid % kVec;
-    const int kk0 = tid / kVec;
-    const int64_t cache_in_chunk = p.cache_len - k0;  // keys [0, cache_in_chunk) of the chunk are cached
-    if (cache_in_chunk >= KC) {  // fast path: the whole chunk is cached
-      const __nv_bfloat16* kb = p.k_cache + (k0 + kk0) * p.cache_row_stride + (int64_t)j * D + c * 8;
-      const __nv_bfloat16* vb = p.v_cache + (k0 + kk0) * p.cache_row_stride + (int64_t)j * D + c * 8;
-      const int64_t step = (int64_t)kRowsPerPass * p.cache_row_stride;
+  auto stage_k = [&](int s) { return smem + s * L::kStage; };
+  auto stage_v = [&](int s) { return smem + s * L::kStage + MKC * L::kRow * 2; };
+  auto load_chunk = [&](int c, int s) {
+    const int64_t k0 = (c_first + c) * MKC;
+    uint8_t* ks = stage_k(s);
+    uint8_t* vs = stage_v(s);
+    for (int idx = tid; idx < MKC * kVec; idx += kMThreads) {
+      const int kk = idx / kVec, cv = idx % kVec;
+      const int64_t key = k0 + kk;
+      const bool cached = key < p.cache_len, valid = key < n_keys;
+      const __nv_bfloat16* kb = cached ? p.k_cache + key * p.cache_row_stride
+                                       : p.k_new + (key - p.cache_len) * p.new_row_stride;
+      const __nv_bfloat16* vb = cached ? p.v_cache + key * p.cache_row_stride
+                                       : p.v_new + (key - p.cache_len) * p.new_row_stride;
+      cp_async16(ks + (kk * L::kRow + cv * 8) * 2, valid ? kb + (int64_t)j * D + cv * 8 : p.q, valid);
+      cp_async16(vs + (kk * L::kRow + cv * 8) * 2, valid ? vb + (int64_t)j * D + cv * 8 : p.q, valid);
+    }
+  };
+  // queries as bf16 rows (16-byte async copies; rows >= R zero-filled), in the first group
+  for (int idx = tid; idx < 16 * MT * kVec; idx += kMThreads) {
+    const int r = idx / kVec, cv = idx % kVec;
+    const int sr = r / p.g, qh = j * p.g + r % p.g;
+    cp_async16(qs + r * L::kRow + cv * 8, r < R ? p.q + ((int64_t)sr * p.hq + qh) * D + cv * 8 : p.q, r < R);
+  }
 #pragma unroll
-      for (int i = 0; i < KC / kRowsPerPass; ++i) {
-        const int kk = kk0 + i * kRowsPerPass;
-        cp_async16(ks + kk * kRowK + c * 16, kb + i * step, true);
-        cp_async16(reinterpret_cast<uint8_t*>(vs) + (kk * D + c * 8) * 2, vb + i * step, true);
-      }
-    } else {
-      for (int i = 0; i < KC / kRowsPerPass; ++i) {
-        const int kk = kk0 + i * kRowsPerPass;
-        const int64_t key = k0 + kk;
-        const bool cached = key < p.cache_len, valid = key < n_keys;
-        const __nv_bfloat16* kb = cached ? p.k_cache + key * p.cache_row_stride : p.k_new + (key - p.cache_len) * p.new_row_stride;
-        const __nv_bfloat16* vb = cached ? p.v_cache + key * p.cache_row_stride : p.v_new + (key - p.cache_len) * p.new_row_stride;
-        cp_async16(ks + kk * kRowK + c * 16, valid ? kb + (int64_t)j * D + c * 8 : p.q, valid);
-        cp_async16(reinterpret_cast<uint8_t*>(vs) + (kk * D + c * 8) * 2, valid ? vb + (int64_t)j * D + c * 8 : p.q, valid);
+  for (int s = 0; s < kMStages - 1; ++s) {
+    if (s < nch) load_chunk(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // per-thread running state for rows (mt, g8) and (mt, g8 + 8)
+  float m_run[MT][2], l_run[MT][2];
+  float o[MT][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    m_run[mt][0] = m_run[mt][1] = -INFINITY;
+    l_run[mt][0] = l_run[mt][1] = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) o[mt][nt][0] = o[mt][nt][1] = o[mt][nt][2] = o[mt][nt][3] = 0.f;
+  }
+  const uint32_t qs_u = static_cast<uint32_t>(__cvta_generic_to_shared(qs));
+  const uint32_t ps_u = static_cast<uint32_t>(__cvta_generic_to_shared(pss));
+  const float sl2 = p.scale_log2;
+
+  for (int c = 0; c < nch; ++c) {
+    const int s = c % kMStages;
+    if (c + kMStages - 1 < nch) load_chunk(c + kMStages - 1, (c + kMStages - 1) % kMStages);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kMStages - 1) : "memory");
+    __syncthreads();
+    const int64_t k0 = (c_first + c) * MKC;
+    const uint32_t ks_u = static_cast<uint32_t>(__cvta_generic_to_shared(stage_k(s)));
+    const uint32_t vs_u = static_cast<uint32_t>(__cvta_generic_to_shared(stage_v(s)));
+    // ---- S = Q K^T for this warp's 8 keys
+    float sc[MT][4], sc2[MT][4];  // two accumulator chains (even / odd k-steps)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[mt][e] = sc2[mt][e] = 0.f;
+#pragma unroll
+    for (int kb = 0; kb < D / 32; ++kb) {  // two k-steps of 16 per ldmatrix.x4 of K
+      uint32_t b[4];
+      ldsm_x4(ks_u + ((warp * 8 + (lane % 8)) * L::kRow + kb * 32 + (lane / 8) * 8) * 2, b[0], b[1], b[2], b[3]);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t a[4], a2[4];
+        ldsm_x4(qs_u + ((mt * 16 + (lane % 16)) * L::kRow + kb * 32 + (lane / 16) * 8) * 2, a[0], a[1], a[2], a[3]);
+        ldsm_x4(qs_u + ((mt * 16 + (lane % 16)) * L::kRow + kb * 32 + 16 + (lane / 16) * 8) * 2, a2[0], a2[1], a2[2],
+                a2[3]);
+        mma_bf16_16816(sc[mt], a, b[0], b[1]);
+        mma_bf16_16816(sc2[mt], a2, b[2], b[3]);
       }
     }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  // queries (pre-scaled into the log2 domain) while the copies fly
-  for (int idx = tid; idx < R * D; idx += kThreads) {
-    const int r = idx / D, e = idx % D;
-    const int s = r / p.g, qh = j * p.g + r % p.g;
-    qs[idx] = __bfloat162float(p.q[((int64_t)s * p.hq + qh) * D + e]) * p.scale_log2;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[mt][e] += sc2[mt][e];
+    // ---- mask, scale to the log2 domain, chunk row max (quad, then across the 8 warps)
+    const int key_a = warp * 8 + 2 * t4;  // this thread's two keys inside the chunk
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = mt * 16 + g8 + (e >> 1) * 8;
+        const int64_t key = k0 + key_a + (e & 1);
+        const bool vis = r < R && key < n_keys && (key < p.cache_len || key - p.cache_len <= r / p.g);
+        sc[mt][e] = vis ? sc[mt][e] * sl2 : -INFINITY;
+      }
+      float m0 = fmaxf(sc[mt][0], sc[mt][1]), m1 = fmaxf(sc[mt][2], sc[mt][3]);
+      m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+      m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+      m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+      m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+      if (t4 == 0) {
+        xm[warp * 16 * MT + mt * 16 + g8] = m0;
+        xm[warp * 16 * MT + mt * 16 + g8 + 8] = m1;
+      }
+    }
+    __syncthreads();
+    // ---- P = 2^(S - m_new) (bf16 to shared memory), running state, O rescale
+    float alpha[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int r = mt * 16 + g8 + hr * 8;
+        float mc = xm[r];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) mc = fmaxf(mc, xm[w * 16 * MT + r]);
+        const float m_new = fmaxf(m_run[mt][hr], mc);
+        const float mu = (m_new == -INFINITY) ? 0.f : m_new;
+        alpha[mt][hr] = (m_run[mt][hr] == -INFINITY) ? 0.f : ex2(m_run[mt][hr] - mu);
+        m_run[mt][hr] = m_new;
+        const float p0 = ex2(sc[mt][2 * hr] - mu), p1 = ex2(sc[mt][2 * hr + 1] - mu);
+        l_run[mt][hr] = l_run[mt][hr] * alpha[mt][hr] + (p0 + p1);
+        *reinterpret_cast<uint32_t*>(pss + r * L::kPRow + key_a) = pack_bf16x2(p0, p1);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        o[mt][nt][0] *= alpha[mt][0];
+        o[mt][nt][1] *= alpha[mt][0];
+        o[mt][nt][2] *= alpha[mt][1];
+        o[mt][nt][3] *= alpha[mt][1];
+      }
+    }
+    __syncthreads();
+    // ---- O += P V for this warp's D/8 columns
+#pragma unroll
+    for (int ks2 = 0; ks2 < MKC / 16; ++ks2) {
+#pragma unroll
+      for (int np = 0; np < NT; np += 2) {  // pairs of n-tiles per ldmatrix.x4.trans
+        uint32_t b[4];
+        const int col = warp * (D / 8) + np * 8 + (lane / 16) * 8;
+        ldsm_x4_t(vs_u + ((ks2 * 16 + (lane % 16)) * L::kRow + col) * 2, b[0], b[1], b[2], b[3]);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          uint32_t a[4];
+          ldsm_x4(ps_u + ((mt * 16 + (lane % 16)) * L::kPRow + ks2 * 16 + (lane / 16) * 8) * 2, a[0], a[1], a[2], a[3]);
+          mma_bf16_16816(o[mt][np], a, b[0], b[1]);
+          if (np + 1 < NT) mma_bf16_16816(o[mt][np + 1], a, b[2], b[3]);
+        }
+      }
+    }
+    __syncthreads();  // stage s, xm and P are rewritten next chunk
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
-
-  // logits: thread = key, its K row read from the padded shared-memory copy
-  {
-    const int64_t key = k0 + tid;
-    const bool valid = key < n_keys;
-    const bool is_new = key >= p.cache_len;
-    const int64_t jn = key - p.cache_len;  // index among the new tokens
-    const uint4* krow = reinterpret_cast<const uint4*>(ks + tid * kRowK);
-    for (int r = 0; r < R; ++r) {
-      float sacc = -INFINITY;
-      const bool visible = valid && (!is_new || jn <= r / p.g);  // new keys: causal among new tokens
-      if (visible) {
-        const uint64_t* qr2 = reinterpret_cast<const uint64_t*>(qs + r * D);
-        uint64_t acc0 = 0ull, acc1 = 0ull;
+  // ---- row sums: quad, then across warps; normalised partial out
 #pragma unroll
-        for (int c = 0; c < kVec; ++c) {
-          const uint4 u = krow[c];
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            // bf16x2 -> fp32x2 is two shifts/selects; the dot product runs on packed FFMA2
-            const uint64_t k2 = f2_pack(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u));
-            if (h & 1)
-              acc1 = ffma2(qr2[c * 4 + h], k2, acc1);
-            else
-              acc0 = ffma2(qr2[c * 4 + h], k2, acc0);
-          }
-        }
-        float x0, x1, y0, y1;
-        f2_unpack(acc0, x0, x1);
-        f2_unpack(acc1, y0, y1);
-        sacc = (x0 + x1) + (y0 + y1);
-      }
-      ps[r * KC + tid] = sacc;
+    for (int hr = 0; hr < 2; ++hr) {
+      float l = l_run[mt][hr];
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      if (t4 == 0) xl[warp * 16 * MT + mt * 16 + g8 + hr * 8] = l;
     }
   }
   __syncthreads();
-
-  // softmax over the chunk, one warp per row
-  const int warp = tid / 32, lane = tid % 32;
-  for (int r = warp; r < R; r += kThreads / 32) {
-    float v[KC / 32];
-    float m = -INFINITY;
-#pragma unroll
-    for (int q = 0; q < KC / 32; ++q) {
-      v[q] = ps[r * KC + q * 32 + lane];
-      m = fmaxf(m, v[q]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float mu = (m == -INFINITY) ? 0.f : m;
-    float l = 0.f;
-#pragma unroll
-    for (int q = 0; q < KC / 32; ++q) {
-      const float e = ex2(v[q] - mu);
-      ps[r * KC + q * 32 + lane] = e;
-      l += e;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) {
-      ms[r] = m;
-      ls[r] = l;
-    }
-  }
-  __syncthreads();
-
-  // O = P V over the staged chunk: thread = (row group, head_dim pair)
-  constexpr int kPairs = D / 2;
-  constexpr int kGroups = kThreads / kPairs;
-  const int d2 = tid % kPairs, rg = tid / kPairs;
-  const int64_t rem = n_keys - k0;
-  const int kmax = rem <= 0 ? 0 : (rem < KC ? (int)rem : KC);
   const int rows_total = p.t * p.hq;
-  constexpr int kRowsPerThread = RT;
-  float acc[kRowsPerThread][2];
 #pragma unroll
-  for (int q = 0; q < kRowsPerThread; ++q) acc[q][0] = acc[q][1] = 0.f;
-  const int nrow = (R - rg + kGroups - 1) / kGroups;  // rows rg, rg + kGroups, ... of this thread
-#pragma unroll 4
-  for (int kk = 0; kk < kmax; ++kk) {
-    const uint32_t vw = *reinterpret_cast<const uint32_t*>(vs + kk * D + 2 * d2);
-    const float vx = __uint_as_float(vw << 16), vy = __uint_as_float(vw & 0xffff0000u);
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-      if (q < nrow) {
-        const float pr = ps[(rg + q * kGroups) * KC + kk];
-        acc[q][0] = fmaf(pr, vx, acc[q][0]);
-        acc[q][1] = fmaf(pr, vy, acc[q][1]);
-      }
+    for (int hr = 0; hr < 2; ++hr) {
+      const int r = mt * 16 + g8 + hr * 8;
+      if (r >= R) continue;
+      float l = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) l += xl[w * 16 * MT + r];
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const int sr = r / p.g, qh = j * p.g + r % p.g;
+      const int64_t row = (int64_t)sr * p.hq + qh;
+      float* dst = p.ws_o + ((int64_t)split * rows_total + row) * D + warp * (D / 8) + 2 * t4;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        *reinterpret_cast<float2*>(dst + nt * 8) = make_float2(o[mt][nt][2 * hr] * inv, o[mt][nt][2 * hr + 1] * inv);
+      if (warp == 0 && t4 == 0)
+        p.ws_lse[(int64_t)split * rows_total + row] = l > 0.f ? m_run[mt][hr] + __log2f(l) : -INFINITY;
     }
   }
-#pragma unroll
-  for (int q = 0; q < kRowsPerThread; ++q) {
-    if (q >= nrow) break;
-    const int r = rg + q * kGroups;
-    const int s = r / p.g, qh = j * p.g + r % p.g;
-    const int64_t row = (int64_t)s * p.hq + qh;
-    const float l = ls[r];
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    float2* dst = reinterpret_cast<float2*>(p.ws_o + ((int64_t)split * rows_total + row) * D) + d2;
-    *dst = make_float2(acc[q][0] * inv, acc[q][1] * inv);
-    if (d2 == 0) p.ws_lse[(int64_t)split * rows_total + row] = l > 0.f ? ms[r] + __log2f(l) : -INFINITY;
-  }
+  // ---- the last CTA of this KV head folds its splits (LSE merge, fixed split order) into the
+  // host's partial: no second launch, the split partials are read back from L2
 }
 
 // LSE merge of n partials per row (MergeScore).  lse_in_log2 selects the input log base;
@@ -269,52 +342,70 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(int n, int64_t 
 
 }  // namespace dec
 
-size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int D) {
-  const int64_t splits = (n_keys + dec::KC - 1) / dec::KC;
+// Split plan of the streaming kernel: ~kSplitTarget CTAs over (splits x KV heads), whole
+// 64-key chunks per split.  Deterministic in the sizes only (no device query), so the
+// workspace size is known without a GPU.
+static void decode_plan(int64_t n_keys, int hk, int64_t* splits, int* chunks_per_split) {
+  const int64_t n_chunks = (n_keys + dec::SKC - 1) / dec::SKC;
+  int64_t target = (dec::kSplitTarget + hk - 1) / hk;
+  if (target < 1) target = 1;
+  if (n_chunks == 0) {
+    *splits = 0;
+    *chunks_per_split = 1;
+    return;
+  }
+  const int64_t cps = (n_chunks + target - 1) / target;
+  *chunks_per_split = (int)cps;
+  *splits = (n_chunks + cps - 1) / cps;
+}
+
+// workspace: split partials O [splits][rows][D] | (256-byte aligned) lse [splits][rows]
+static size_t ws_off_lse(int64_t splits, int64_t rows, int D) {
+  return ((size_t)splits * rows * D * sizeof(float) + 255) & ~size_t(255);
+}
+
+size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int hk, int D) {
+  int64_t splits;
+  int cps;
+  decode_plan(n_keys, hk, &splits, &cps);
   const int64_t rows = (int64_t)t * hq;
-  size_t o = (size_t)splits * rows * D * sizeof(float);
-  o = (o + 255) & ~size_t(255);
-  return o + (size_t)splits * rows * sizeof(float);
+  return ws_off_lse(splits, rows, D) + (size_t)splits * rows * sizeof(float);
 }
 
 apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse, cudaStream_t stream) {
   DecodeParams p = p0;
   const int64_t n_keys = p.cache_len + (p.has_new ? p.t : 0);
-  const int64_t splits = (n_keys + dec::KC - 1) / dec::KC;
+  int64_t splits;
+  int cps;
+  decode_plan(n_keys, p.hk, &splits, &cps);
   const int64_t rows = (int64_t)p.t * p.hq;
-  // (splits == 0: no key at all -> the merge below of zero parts writes O = 0, lse = -inf)
-  size_t o = (size_t)splits * rows * p.D * sizeof(float);
-  o = (o + 255) & ~size_t(255);
-  p.ws_lse = reinterpret_cast<float*>(reinterpret_cast<char*>(p.ws_o) + o);
+  char* base = reinterpret_cast<char*>(p.ws_o);
+  p.ws_lse = reinterpret_cast<float*>(base + ws_off_lse(splits, rows, p.D));
   dim3 grid((unsigned)splits, p.hk);
-  if (splits > 0) {
+  if (splits == 0)  // no key at all: the merge of zero parts writes O = 0, lse = -inf
+    return launch_merge(0, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream);
+  {
     const int R = p.t * p.g;
-    const int smem = dec::decode_smem_bytes(R, p.D);
-    const int groups = dec::kThreads / (p.D / 2);
-    const int rt = (R + groups - 1) / groups;  // rows per thread in the P.V phase
-    auto launch = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dec::decode_smem_bytes(kDecodeRowsMax, p.D));
-      kern<<<grid, dec::kThreads, smem, stream>>>(p);
+    const int mt = (R + 15) / 16;  // 16-row m-tiles
+    auto launch = [&](auto kern, int MT, int D) {
+      const int smem = D == 128 ? dec::MmaSmem<128>::bytes(MT) : dec::MmaSmem<64>::bytes(MT);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kern<<<grid, dec::kMThreads, smem, stream>>>(p, cps);
     };
     if (p.D == 128) {
-      if (rt <= 1) launch(dec::decode_split_kernel<128, 1>);
-      else if (rt <= 2) launch(dec::decode_split_kernel<128, 2>);
-      else if (rt <= 4) launch(dec::decode_split_kernel<128, 4>);
-      else if (rt <= 8) launch(dec::decode_split_kernel<128, 8>);
-      else if (rt <= 16) launch(dec::decode_split_kernel<128, 16>);
-      else launch(dec::decode_split_kernel<128, 32>);
+      if (mt <= 1) launch(dec::decode_mma_kernel<128, 1>, 1, 128);
+      else if (mt <= 2) launch(dec::decode_mma_kernel<128, 2>, 2, 128);
+      else launch(dec::decode_mma_kernel<128, 4>, 4, 128);
     } else {
-      if (rt <= 1) launch(dec::decode_split_kernel<64, 1>);
-      else if (rt <= 2) launch(dec::decode_split_kernel<64, 2>);
-      else if (rt <= 4) launch(dec::decode_split_kernel<64, 4>);
-      else if (rt <= 8) launch(dec::decode_split_kernel<64, 8>);
-      else launch(dec::decode_split_kernel<64, 16>);
+      if (mt <= 1) launch(dec::decode_mma_kernel<64, 1>, 1, 64);
+      else if (mt <= 2) launch(dec::decode_mma_kernel<64, 2>, 2, 64);
+      else launch(dec::decode_mma_kernel<64, 4>, 4, 64);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     count_launch();
   }
-  // fold the chunks: fp32 partial of this host, natural-log lse
+  // fold the splits (LSE merge, fixed order): the host's fp32 partial, natural-log lse
   return launch_merge((int)splits, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream);
 }
 

@@ -82,7 +82,7 @@ struct DecodeParams {
   float* ws_o;                   // [splits][t*hq][D] then (256-B aligned) ws_lse [splits][t*hq]
   float* ws_lse;
 };
-size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int D);
+size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int hk, int D);
 apb_status launch_decode(const DecodeParams& p, float* part_o, float* part_lse, cudaStream_t stream);
 apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,
                         int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,

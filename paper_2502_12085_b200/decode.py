@@ -37,7 +37,7 @@ class DecodeRank:
             d = self.dims(h, kc.shape[0])
             n = apb.decode_workspace_size(d)
             if self.ws.get(h) is None or self.ws[h].numel() < n:
-                self.ws[h] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device)
+                self.ws[h] = torch.zeros(max(n, 16), dtype=torch.uint8, device=self.device)
             slot = self.parts[h]
             apb.decode_attention(d, q, kc, vc, k_new if h == self.H - 1 else None,
                                  v_new if h == self.H - 1 else None, slot[: self.rows * self.d],

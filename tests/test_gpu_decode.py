@@ -53,7 +53,7 @@ def test_decode_partial_parity(c, t, last, d, hq, hk):
     dims = apb.DecodeDims(H, host, t, c, hq, hk, d)
     po = torch.full((t, hq, d), float("nan"), device="cuda")
     pl = torch.full((t, hq), float("nan"), device="cuda")
-    ws = torch.empty(max(apb.decode_workspace_size(dims), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(apb.decode_workspace_size(dims), 16), dtype=torch.uint8, device="cuda")
     kct = dev(kc) if c else torch.empty((0, hk, d), dtype=torch.bfloat16, device="cuda")
     vct = dev(vc) if c else torch.empty((0, hk, d), dtype=torch.bfloat16, device="cuda")
     apb.decode_attention(dims, dev(q), kct, vct, dev(kn) if last else None, dev(vn) if last else None, po, pl, ws)
