@@ -43,7 +43,17 @@ def test_binary_is_sm100a_with_tcgen05_and_tma(lib):
     assert "UTCHMMA" in sass  # tcgen05.mma
     assert "UTMALDG" in sass  # TMA loads
     assert "LDTM" in sass and "STTM" in sass  # TMEM <-> registers
-    assert "HMMA" not in re.sub(r"UTCHMMA", "", sass)  # no legacy mma.sync path
+    # per function: the prefill kernels (attention, retaining heads) use tcgen05 only; the legacy
+    # warp-level mma.sync appears only in the decode GEMV kernel (DESIGN 7b: M = t*g <= 16 rows)
+    funcs = re.split(r"\n\s*Function : ", sass)[1:]
+    assert funcs
+    for f in funcs:
+        name, body = f.split("\n", 1)
+        legacy = "HMMA" in re.sub(r"UTCHMMA", "", body)
+        if "attention_kernel" in name or "retain_score_kernel" in name:
+            assert "UTCHMMA" in body and not legacy, name
+        elif legacy:
+            assert "decode_mma_kernel" in name, name
 
 
 def _dims(**kw):
