@@ -60,11 +60,13 @@ def _load():
             lib.oracle_select_topk.argtypes = [i64, i64, dp, ip]
             lib.oracle_attention.argtypes = [i64, i64, i64, i32, i32, i32, ctypes.c_double,
                                              dp, dp, dp, i64, lp, dp, dp]
+            lib.oracle_attention_ex.argtypes = [i64, i64, i64, i32, i32, i32, ctypes.c_double,
+                                                dp, dp, dp, i64, lp, dp, dp, ctypes.c_int]
             lib.oracle_decode_partial.argtypes = [i64, i64, i32, i32, i32, ctypes.c_double,
                                                   dp, dp, dp, dp, dp, dp, dp]
             lib.oracle_merge_score.argtypes = [i32, i64, i32, dp, dp, dp, dp]
             lib.oracle_random_scores.argtypes = [ctypes.c_uint64, ctypes.c_uint64, i64, dp]
-            for f in (lib.oracle_retain_score, lib.oracle_select_topk, lib.oracle_attention,
+            for f in (lib.oracle_retain_score, lib.oracle_select_topk, lib.oracle_attention, lib.oracle_attention_ex,
                       lib.oracle_decode_partial, lib.oracle_merge_score, lib.oracle_random_scores):
                 f.restype = ctypes.c_int
             lib.oracle_num_threads.restype = ctypes.c_int
@@ -181,15 +183,22 @@ def passing(gathered, host: int):
     return pk, pv
 
 
-def attention(q, k, v, L_A: int, pk, pv, scale: float | None = None, rows=None):
+def attention(q, k, v, L_A: int, pk, pv, scale: float | None = None, rows=None, q_subset: bool = False):
     """[A_a, A_h] = softmax(M' . Q K^T / sqrt(d_m)) V  (eq:apb).
 
     q: [L_A+l_b][hq][d]; k, v: [L_A+l_b][hk][d]; pk, pv: [P][hk][d].
     Key sequence: [K_a ; K_p ; K_h].  rows: optional query-row subset.
+    q_subset: q holds only the rows listed in `rows`, in that order (same arithmetic; for
+    sampled checks at sizes whose full Q does not fit in host memory as fp64).
     Returns (O [rows][hq][d] fp64, lse [rows][hq] fp64)."""
     q, k, v = _as_f64(q), _as_f64(k), _as_f64(v)
     pk, pv = _as_f64(pk), _as_f64(pv)
-    n_q, hq, d = q.shape
+    _, hq, d = q.shape
+    n_q = k.shape[0]
+    if not q_subset and q.shape[0] != n_q:
+        raise ValueError("q and k must have the same number of rows")
+    if q_subset and (rows is None or len(rows) != q.shape[0]):
+        raise ValueError("q_subset needs rows with one entry per q row")
     hk = k.shape[1]
     l_b = n_q - L_A
     P = pk.shape[0]
@@ -205,9 +214,9 @@ def attention(q, k, v, L_A: int, pk, pv, scale: float | None = None, rows=None):
         n_rows = rp.shape[0]
     O = np.empty((n_rows, hq, d), np.float64)
     lse = np.empty((n_rows, hq), np.float64)
-    rc = _load().oracle_attention(L_A, P, l_b, hq, hk, d, float(scale), _p(q), _p(kseq), _p(vseq),
-                                  n_rows, _p(rp, ctypes.c_int64) if rp is not None else None,
-                                  _p(O), _p(lse))
+    rc = _load().oracle_attention_ex(L_A, P, l_b, hq, hk, d, float(scale), _p(q), _p(kseq), _p(vseq),
+                                     n_rows, _p(rp, ctypes.c_int64) if rp is not None else None,
+                                     _p(O), _p(lse), int(q_subset))
     if rc:
         raise ValueError(f"oracle_attention rc={rc}")
     return O, lse

@@ -117,13 +117,17 @@ int oracle_select_topk(int64_t l_b, int64_t l_p, const double* s, int32_t* idx) 
  *              and local keys L_A + P + m with m <= i    (causal over the local block)
  * Query head qh reads KV head qh / (hq / hk) (GQA).
  */
-int oracle_attention(int64_t L_A, int64_t P, int64_t l_b, int32_t hq, int32_t hk, int32_t d,
-                     double scale, const double* Q, const double* K, const double* V,
-                     int64_t n_rows, const int64_t* rows, double* O, double* lse) {
+/* q_subset != 0: Q holds only the requested rows, in the order of `rows` (row x of Q is query
+ * row rows[x]) — for sampled checks at sizes whose full Q would not fit in host memory as fp64.
+ * The arithmetic is identical. */
+int oracle_attention_ex(int64_t L_A, int64_t P, int64_t l_b, int32_t hq, int32_t hk, int32_t d,
+                        double scale, const double* Q, const double* K, const double* V,
+                        int64_t n_rows, const int64_t* rows, double* O, double* lse, int q_subset) {
     if (L_A < 0 || P < 0 || l_b < 0 || hq <= 0 || hk <= 0 || hq % hk || d <= 0) return 1;
     const int64_t n_q = L_A + l_b, n_k = L_A + P + l_b;
     const int32_t g = hq / hk;
     if (!rows) n_rows = n_q;
+    if (q_subset && !rows) return 3;
     for (int64_t x = 0; x < n_rows; ++x) {
         int64_t r = rows ? rows[x] : x;
         if (r < 0 || r >= n_q) return 2;
@@ -133,7 +137,7 @@ int oracle_attention(int64_t L_A, int64_t P, int64_t l_b, int32_t hq, int32_t hk
         for (int32_t qh = 0; qh < hq; ++qh) {
             const int64_t r = rows ? rows[x] : x;
             const int32_t j = qh / g;
-            const double* q = Q + (r * hq + qh) * (int64_t)d;
+            const double* q = Q + ((q_subset ? x : r) * hq + qh) * (int64_t)d;
             double* logit = (double*)malloc(sizeof(double) * (size_t)(n_k > 0 ? n_k : 1));
             unsigned char* vis = (unsigned char*)malloc((size_t)(n_k > 0 ? n_k : 1));
             for (int64_t k = 0; k < n_k; ++k) {
@@ -174,6 +178,12 @@ int oracle_attention(int64_t L_A, int64_t P, int64_t l_b, int32_t hq, int32_t hk
         }
     }
     return 0;
+}
+
+int oracle_attention(int64_t L_A, int64_t P, int64_t l_b, int32_t hq, int32_t hk, int32_t d,
+                     double scale, const double* Q, const double* K, const double* V,
+                     int64_t n_rows, const int64_t* rows, double* O, double* lse) {
+    return oracle_attention_ex(L_A, P, l_b, hq, hk, d, scale, Q, K, V, n_rows, rows, O, lse, 0);
 }
 
 int oracle_num_threads(void) {

@@ -190,7 +190,8 @@ def test_select_compact_bit_exact(name, ties):
         assert np.array_equal(send, oracle.compact(x["k"], x["v"], x["L_A"], idx_or))
 
 
-@pytest.mark.parametrize("lp,l_b", [(1, 300), (300, 300), (500, 300), (129, 1000), (4096, 70000)])
+@pytest.mark.parametrize("lp,l_b", [(1, 300), (300, 300), (500, 300), (129, 1000), (4096, 70000), (8192, 65536),
+                                    (2048, 131072)])
 def test_select_sizes(lp, l_b):
     cfg = synth.Config("sel", 17, n=l_b * 2, H=2, l_a=8, l_p=lp, hq=2, hk=2, d=64, d_hidden=256)
     x = synth.host_qkv(cfg, 0, 1)
@@ -321,6 +322,47 @@ def test_full_size_llama8b_128k_sampled():
             O = io[h].out[rows].float().cpu().double().numpy()
             lse = io[h].lse[:, rows].cpu().double().numpy().T
             check_attention(O, lse, O_or, lse_or, f"L8-128K host {h} LOCAL+PASSING sampled")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["llama8b-512k", "llama8b-1m"])
+def test_full_size_max_sampled(name):
+    """Maximum sizes (512K with l_a = l_p = 8K, and 1M tokens; H = 8): the
+    critical host's attention (135K-rows Q, 150K-key sequences, 64-bit offsets) in the ordered
+    one-launch form and as the LOCAL / PASSING pair, on sampled rows (boundaries of every
+    segment + random) against the oracle.  Inputs: seeded N(0,1) on the device; the passing
+    buffer is random too (attention is exact for any passing keys)."""
+    from paper_2502_12085_b200 import apb
+    cfg = synth.CONFIGS[name]
+    h = cfg.H - 1
+    d = dims_of(cfg, h)
+    n = d.rows
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1 + cfg.cfg_id)
+    rnd = lambda *shape: torch.randn(*shape, generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+    q, k, v = rnd(n, cfg.hq, cfg.d), rnd(n, cfg.hk, cfg.d), rnd(n, cfg.hk, cfg.d)
+    gathered = rnd(cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)
+    ws = torch.empty(max(apb.workspace_size(d, apb.WS_ATTENTION), 16), dtype=torch.uint8, device="cuda")
+    L_A, l_b = d.L_A, cfg.l_b
+    rng = np.random.default_rng(cfg.cfg_id)
+    rows = sorted({0, L_A - 1, L_A, L_A + 1, L_A + 127, L_A + 128, n - 129, n - 1}
+                  | set(rng.choice(n, 8, replace=False).tolist()))
+    kb, vb, gb = to_bits(k), to_bits(v), to_bits(gathered)
+    pk, pv = oracle.passing(gb, h)
+    O_or, lse_or = oracle.attention(to_bits(q[rows]), kb, vb, L_A, pk, pv, rows=rows, q_subset=True)
+    for split in (False, True):
+        out = torch.full_like(q, float("nan"))
+        lse = torch.full((cfg.hq, n), float("nan"), device="cuda")
+        if split:
+            apb.attention_fwd(d, q, k, v, gathered, out, lse, phase=apb.PHASE_LOCAL, ws=ws)
+            apb.attention_fwd(d, q, k, v, gathered, out, lse, phase=apb.PHASE_PASSING, ws=ws)
+        else:
+            apb.attention_fwd(d, q, k, v, gathered, out, lse, phase=apb.PHASE_ALL, ws=ws)
+        torch.cuda.synchronize()
+        O = out[rows].float().cpu().double().numpy()
+        L = lse[:, rows].cpu().double().numpy().T
+        check_attention(O, L, O_or, lse_or, f"{name} host {h} {'split' if split else 'ordered'} ({len(rows)} rows)")
+        assert torch.isfinite(out.float()).all()
 
 
 def test_nccl_unique_id_and_single_rank_comm():

@@ -521,3 +521,18 @@ def test_share_scores_examples():
     s = rng.standard_normal((3, 7))
     best = max(itertools.combinations(range(7), 3), key=lambda c: (sorted(s.max(0)[list(c)], reverse=True)))
     np.testing.assert_array_equal(oracle.select_all_heads(oracle.share_scores(s), 3)[0], sorted(best))
+
+
+def test_attention_q_subset_equals_full_rows():
+    """The q_subset indexing option (sampled checks at maximum sizes) returns exactly the rows of
+    the full-Q call."""
+    rng = np.random.default_rng(11)
+    L_A, P, l_b, hq, hk, d = 5, 3, 9, 4, 2, 8
+    q = rng.standard_normal((L_A + l_b, hq, d))
+    k, v = rng.standard_normal((L_A + l_b, hk, d)), rng.standard_normal((L_A + l_b, hk, d))
+    pk, pv = rng.standard_normal((P, hk, d)), rng.standard_normal((P, hk, d))
+    rows = np.array([13, 0, 6, 4, 5])
+    O, lse = oracle.attention(q, k, v, L_A, pk, pv, rows=rows)
+    O2, lse2 = oracle.attention(q[rows], k, v, L_A, pk, pv, rows=rows, q_subset=True)
+    np.testing.assert_array_equal(O, O2)
+    np.testing.assert_array_equal(lse, lse2)
