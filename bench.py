@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["apb", "reference"], default="apb")
+    ap.add_argument("--compressor", choices=["retain", "random"], default="retain",
+                    help="Table 4 compressor: retaining heads R (default) or the random selector Rd.")
+    ap.add_argument("--shared-set", action="store_true", help="one index set per host (SPEC S:294 reading)")
     ap.add_argument("--workload", choices=["hotpath", "model"], default="hotpath",
                     help="model: the full decoder stack around the hot path (bench_model.py, NEXT #2)")
     ap.add_argument("--config", default="llama8b-128k")
@@ -195,8 +198,8 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg, H, layers, n_gpus):
-    return {"workload": f"{cfg.name}: APB prefill hot path, Llama-3.1-8B-shaped layer stack "
+def workload_config(cfg, H, layers, n_gpus, variant=""):
+    return {"workload": f"{cfg.name}{variant}: APB prefill hot path, Llama-3.1-8B-shaped layer stack "
                         f"(hq={cfg.hq}, hk={cfg.hk}, d={cfg.d}), n={cfg.n}, H={H} hosts over {n_gpus} GPU(s), "
                         f"l_a={cfg.l_a}, l_p={cfg.l_p}, {layers} layers, retaining head d_R={cfg.d_hidden}",
             "n": cfg.n, "H": H, "l_a": cfg.l_a, "l_p": cfg.l_p, "layers": layers, "hq": cfg.hq, "hk": cfg.hk,
@@ -249,7 +252,8 @@ def main():
     split = None if args.schedule == "auto" else (args.schedule == "split")
     if args.same_device and world > 1 and split is None:
         split = True  # the multi-rank schedule (the exchange itself is skipped in this mode)
-    pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True, split_phases=split)
+    pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True, split_phases=split,
+                     compressor=args.compressor, shared_set=args.shared_set, seed=2502)
 
     # ---- synthetic inputs: D1 N(0,1) Q/K/V (the paper's timing input is synthetic random
     # input), two alternating layer buffer sets, random-init retaining heads.
@@ -285,7 +289,7 @@ def main():
     def step(timed=False):
         for l in range(layers):
             pr.layer(sets[l % 2], weights[l], overlap=not args.no_overlap,
-                     events=attn_events if timed else None)
+                     events=attn_events if timed else None, layer_idx=l)
 
     def barrier():
         torch.cuda.synchronize()
@@ -351,7 +355,9 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) Q/K/V, random-init retaining heads)",
-                "config": workload_config(cfg, H, layers, world),
+                "config": workload_config(cfg, H, layers, world,
+                                          ("" if args.compressor == "retain" else " [compressor Rd.]")
+                                          + (" [shared index set]" if args.shared_set else "")),
                 "attn_peak_frac": {"critical_host": round(crit * layers / (ms_per_step / 1e3) / 1e12 / peak_tf, 4)
                                    if world == H else None,
                                    "aggregate": round(flops_all * layers / (ms_per_step / 1e3) / 1e12 / (peak_tf * world), 4)},
@@ -397,7 +403,7 @@ def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank,
             if l + 1 < layers:
                 upload((l + 1) % 2)
             main.wait_event(copied[s])
-            pr.layer(sets[s], weights[l], overlap=not args.no_overlap)
+            pr.layer(sets[s], weights[l], overlap=not args.no_overlap, layer_idx=l)
             done[s].record(main)
         for h in hosts:
             out_host[h].copy_(sets[(layers - 1) % 2][h].out, non_blocking=True)
