@@ -93,6 +93,9 @@ CASES = {
     "d128-sink": synth.Config("d128-sink", 14, n=2048, H=4, l_a=256, l_p=128, hq=4, hk=2, d=128, d_hidden=256,
                               dist="D3"),
     "lq": synth.Config("lq", 15, n=1024, H=2, l_a=100, l_p=64, hq=4, hk=2, d=64, d_hidden=256, l_q=37),
+    # MHA (g = 1: one query head per KV head, odd unit count per KV head) and g = 8 (Llama-70B ratio)
+    "mha": synth.Config("mha", 16, n=1152, H=3, l_a=70, l_p=40, hq=3, hk=3, d=128, d_hidden=256),
+    "gqa8": synth.Config("gqa8", 17, n=768, H=2, l_a=130, l_p=96, hq=16, hk=2, d=64, d_hidden=256),
 }
 
 
