@@ -26,7 +26,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src,
 
 // Split plan: ~kSplitTarget CTAs over (splits x KV heads), whole 64-key chunks per split.
 #ifndef APB_DEC_CTAS_PER_SM
-#define APB_DEC_CTAS_PER_SM 2
+#define APB_DEC_CTAS_PER_SM 3
 #endif
 constexpr int SKC = 64;                                  // keys per chunk
 constexpr int kSplitTarget = APB_DEC_CTAS_PER_SM * 148;  // CTAs per launch to aim for (per SM x B200 SMs)
@@ -43,12 +43,16 @@ constexpr int kSplitTarget = APB_DEC_CTAS_PER_SM * 148;  // CTAs per launch to a
 //              ldmatrix.trans; O stays in registers for the whole split.
 constexpr int MKC = SKC;        // keys per chunk
 constexpr int kMThreads = 256;  // 8 warps
-constexpr int kMStages = 3;
+#ifndef APB_DEC_STAGES
+#define APB_DEC_STAGES 2
+#endif
+constexpr int kMStages = APB_DEC_STAGES;
 
 template <int D>
 struct MmaSmem {
-  static constexpr int kRow = D + 8;                  // padded bf16 row (conflict-free ldmatrix)
-  static constexpr int kStage = 2 * MKC * kRow * 2;   // K and V chunk
+  static constexpr int kRow = D + 8;                  // padded bf16 row (Q, conflict-free ldmatrix)
+  static constexpr int kKV = D * 2;                   // K / V chunk row: dense, 16-byte chunks XOR-swizzled
+  static constexpr int kStage = 2 * MKC * kKV;        // K and V chunk
   static constexpr int kPRow = MKC + 8;
   static constexpr int bytes(int MT) {
     return kMStages * kStage + 16 * MT * kRow * 2 + 16 * MT * kPRow * 2 + 2 * 8 * 16 * MT * 4;
@@ -68,6 +72,13 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
                "{%0,%1,%2,%3};"
                : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// byte offset of 16-byte chunk c of row r in a dense K / V chunk: chunk index XOR (r & 7), so the
+// 8 rows an ldmatrix 8x8 reads hit 8 different bank groups
+template <int D>
+__device__ __forceinline__ uint32_t kv_off(int r, int c) {
+  return static_cast<uint32_t>(r * (D * 2) + ((c ^ (r & 7)) << 4));
 }
 
 template <int D, int MT>
@@ -90,7 +101,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
                                                                        : (n_chunks_total > c_first ? n_chunks_total - c_first : 0));
   constexpr int kVec = D / 8;
   auto stage_k = [&](int s) { return smem + s * L::kStage; };
-  auto stage_v = [&](int s) { return smem + s * L::kStage + MKC * L::kRow * 2; };
+  auto stage_v = [&](int s) { return smem + s * L::kStage + MKC * L::kKV; };
   auto load_chunk = [&](int c, int s) {
     const int64_t k0 = (c_first + c) * MKC;
     uint8_t* ks = stage_k(s);
@@ -103,8 +114,8 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
                                        : p.k_new + (key - p.cache_len) * p.new_row_stride;
       const __nv_bfloat16* vb = cached ? p.v_cache + key * p.cache_row_stride
                                        : p.v_new + (key - p.cache_len) * p.new_row_stride;
-      cp_async16(ks + (kk * L::kRow + cv * 8) * 2, valid ? kb + (int64_t)j * D + cv * 8 : p.q, valid);
-      cp_async16(vs + (kk * L::kRow + cv * 8) * 2, valid ? vb + (int64_t)j * D + cv * 8 : p.q, valid);
+      cp_async16(ks + kv_off<D>(kk, cv), valid ? kb + (int64_t)j * D + cv * 8 : p.q, valid);
+      cp_async16(vs + kv_off<D>(kk, cv), valid ? vb + (int64_t)j * D + cv * 8 : p.q, valid);
     }
   };
   // queries as bf16 rows (16-byte async copies; rows >= R zero-filled), in the first group
@@ -150,7 +161,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
 #pragma unroll
     for (int kb = 0; kb < D / 32; ++kb) {  // two k-steps of 16 per ldmatrix.x4 of K
       uint32_t b[4];
-      ldsm_x4(ks_u + ((warp * 8 + (lane % 8)) * L::kRow + kb * 32 + (lane / 8) * 8) * 2, b[0], b[1], b[2], b[3]);
+      ldsm_x4(ks_u + kv_off<D>(warp * 8 + (lane % 8), kb * 4 + lane / 8), b[0], b[1], b[2], b[3]);
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         uint32_t a[4], a2[4];
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
       for (int np = 0; np < NT; np += 2) {  // pairs of n-tiles per ldmatrix.x4.trans
         uint32_t b[4];
         const int col = warp * (D / 8) + np * 8 + (lane / 16) * 8;
-        ldsm_x4_t(vs_u + ((ks2 * 16 + (lane % 16)) * L::kRow + col) * 2, b[0], b[1], b[2], b[3]);
+        ldsm_x4_t(vs_u + kv_off<D>(ks2 * 16 + (lane % 16), col / 8), b[0], b[1], b[2], b[3]);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           uint32_t a[4];

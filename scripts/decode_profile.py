@@ -22,8 +22,16 @@ def main():
     ap.add_argument("--config", default="llama8b-128k")
     ap.add_argument("--t", type=int, default=1)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--hq", type=int, default=None, help="override query heads (layout experiments)")
+    ap.add_argument("--hk", type=int, default=None, help="override KV heads")
+    ap.add_argument("--lb", type=int, default=None, help="override cache rows per host")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
+    over = {k: v for k, v in (("hq", a.hq), ("hk", a.hk)) if v is not None}
+    if a.lb is not None:
+        over["n"] = a.lb * cfg.H
+    if over:
+        cfg = cfg.replace(**over)
     dev = torch.device("cuda")
     caches = {h: (torch.randn((cfg.l_b, cfg.hk, cfg.d), device=dev).bfloat16(),
                   torch.randn((cfg.l_b, cfg.hk, cfg.d), device=dev).bfloat16()) for h in range(cfg.H)}
@@ -48,7 +56,7 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     gbs = cache_bytes / (ms / 1e3) / 1e9
-    print(json.dumps({"config": a.config, "t_new": a.t, "hosts": cfg.H, "cache_rows_per_host": cfg.l_b,
+    print(json.dumps({"config": a.config, "hq": cfg.hq, "hk": cfg.hk, "t_new": a.t, "hosts": cfg.H, "cache_rows_per_host": cfg.l_b,
                       "ms_per_layer_step": round(ms, 4), "cache_bytes": cache_bytes, "achieved_gbs": round(gbs, 1),
                       "hbm_peak_gbs": peaks["hbm_gbs"], "frac": round(gbs / peaks["hbm_gbs"], 3)}))
 
