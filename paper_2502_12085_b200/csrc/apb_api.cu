@@ -64,6 +64,18 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t
 // ---------------------------------------------------------------- validation helpers
 static int64_t L_A_of(const apb_dims* d) { return d->host == 0 ? 0 : (int64_t)d->l_q + d->l_a; }
 static int64_t lpp_of(const apb_dims* d) { return d->l_p < d->l_b ? d->l_p : d->l_b; }
+apb_status set_max_smem_once(const void* func, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return APB_OK;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return APB_OK;
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 static apb_status check_dims(const apb_dims* d) {

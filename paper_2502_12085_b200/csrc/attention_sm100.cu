@@ -614,12 +614,9 @@ static apb_status launch_impl(const AttnParams& p, const CUtensorMap& tq, const 
   using L = Layout<D>;
   const int grid = p.n_local_items + p.n_anchor_items;
   if (grid == 0) return APB_OK;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(apb_attention_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
-    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(apb_attention_kernel<D>), L::kAlloc, smem_set))
+    return st;
   apb_attention_kernel<D><<<grid, kThreads, L::kAlloc, stream>>>(tq, tk, tv, tg, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));

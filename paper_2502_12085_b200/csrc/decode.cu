@@ -398,10 +398,14 @@ apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse,
   {
     const int R = p.t * p.g;
     const int mt = (R + 15) / 16;  // 16-row m-tiles
+    apb_status st = APB_OK;
     auto launch = [&](auto kern, int MT, int D) {
+      // one set-once device mask per kernel instantiation (D, MT)
       const int smem = D == 128 ? dec::MmaSmem<128>::bytes(MT) : dec::MmaSmem<64>::bytes(MT);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      kern<<<grid, dec::kMThreads, smem, stream>>>(p, cps);
+      static std::atomic<uint64_t> smem_set[2][3];
+      const int di = D == 128 ? 0 : 1, mi = MT <= 1 ? 0 : (MT <= 2 ? 1 : 2);
+      st = set_max_smem_once(reinterpret_cast<const void*>(kern), smem, smem_set[di][mi]);
+      if (st == APB_OK) kern<<<grid, dec::kMThreads, smem, stream>>>(p, cps);
     };
     if (p.D == 128) {
       if (mt <= 1) launch(dec::decode_mma_kernel<128, 1>, 1, 128);
@@ -412,6 +416,7 @@ apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse,
       else if (mt <= 2) launch(dec::decode_mma_kernel<64, 2>, 2, 64);
       else launch(dec::decode_mma_kernel<64, 4>, 4, 64);
     }
+    if (st) return st;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     count_launch();

@@ -1,5 +1,6 @@
 // internal.h — declarations shared by libapb's translation units (not part of the ABI).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cstddef>
 #include <string>
@@ -14,6 +15,11 @@ namespace apb {
 void set_error(const std::string& msg);
 apb_status fail(apb_status s, const std::string& msg);
 void count_launch(int n = 1);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (call site, device): the attribute
+// is per device, so a process that drives several GPUs needs it on each.  `done` is a per-call-
+// site bitmask of devices already configured.
+apb_status set_max_smem_once(const void* func, int bytes, std::atomic<uint64_t>& done);
 
 // TMA descriptor encoding through the driver entry point (no -lcuda at link time).
 // Returns false (and sets the error) if the driver call fails.

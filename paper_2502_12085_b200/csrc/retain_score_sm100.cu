@@ -228,13 +228,9 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
 
 apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(score::retain_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         score::kSmem);
-    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(score::retain_score_kernel), score::kSmem, smem_set))
+    return st;
   int grid = (p.l_b + score::TM - 1) / score::TM;
   grid = (grid + score::kCluster - 1) / score::kCluster * score::kCluster;  // whole clusters
   score::retain_score_kernel<<<grid, score::kThreads, score::kSmem, stream>>>(tq, tk, tv, tw1, p);
