@@ -251,3 +251,69 @@ def test_apb_layer_random_compressor_runs():
     s = oracle.random_scores(5, 2, cfg.H, 1, cfg.hk, cfg.l_b)
     assert np.array_equal(idx, oracle.select_all_heads(s, cfg.l_p))
     assert all(torch.isfinite(x.float()).all() for x in xs.values())
+
+
+@pytest.mark.slow
+def test_full_size_llama8b_layer_sampled():
+    """NEXT #2 at the bench's size and launch configuration (bench_model.py: Llama-3.1-8B shape,
+    hidden 4096 / FFN 14336, n = 128K, H = 8 hosts on one GPU, ordered schedule): one layer,
+    every step checked on sampled rows of the critical host (and host 1) — the row-local steps
+    (RMSNorm, QKV projection, RoPE; O projection + FFN) against the oracle fed the GPU's inputs of
+    that step, attention against the oracle over the GPU's own Q/K/V and gathered buffer."""
+    from paper_2502_12085_b200 import apb
+    from paper_2502_12085_b200.model import ApbModelRank, LayerWeights, ModelShape
+    cfg = synth.CONFIGS["llama8b-128k"]
+    hidden, inter = 4096, 14336
+    shape = ModelShape(hidden=hidden, inter=inter, n_heads=cfg.hq, n_kv_heads=cfg.hk, head_dim=cfg.d)
+    base = apb.Dims(n=cfg.n, H=cfg.H, host=0, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
+                    head_dim=cfg.d)
+    rank = ApbModelRank(base, shape, list(range(cfg.H)))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(12085)
+    rnd = lambda *s, scale=1.0, mean=0.0: (torch.randn(*s, generator=g, device="cuda") * scale + mean).to(torch.bfloat16)
+    lw = LayerWeights(attn_norm=rnd(hidden, scale=0.1, mean=1.0),
+                      w_qkv=rnd((cfg.hq + 2 * cfg.hk) * cfg.d, hidden, scale=hidden ** -0.5),
+                      w_o=rnd(hidden, cfg.hq * cfg.d, scale=(cfg.hq * cfg.d) ** -0.5),
+                      ffn_norm=rnd(hidden, scale=0.1, mean=1.0), w_gu=rnd(2 * inter, hidden, scale=hidden ** -0.5),
+                      w_down=rnd(hidden, inter, scale=inter ** -0.5),
+                      retain=apb.RetainWeights(w1=rnd(cfg.d_hidden, cfg.d_in, scale=cfg.d_in ** -0.5),
+                                               w2=torch.randn(cfg.hq, cfg.d_hidden, generator=g, device="cuda")
+                                               * cfg.d_hidden ** -0.5,
+                                               b1=torch.zeros(cfg.d_hidden, device="cuda"),
+                                               b2=torch.zeros(cfg.hq, device="cuda")))
+    xs = {h: rnd(rank.rows[h], hidden) for h in range(cfg.H)}
+    x_in = {h: xs[h].clone() for h in (1, cfg.H - 1)}
+    rank.layer(xs, lw)
+    torch.cuda.synchronize()
+    W = {k: f64(getattr(lw, k)) for k in ("attn_norm", "w_qkv", "w_o", "ffn_norm", "w_gu", "w_down")}
+    W.update(eps=shape.eps, theta=shape.theta)
+    gathered = rank.hot.gathered.view(torch.int16).cpu().numpy().view(np.uint16)
+    rng = np.random.default_rng(3)
+    for h in (1, cfg.H - 1):
+        L_A = rank.hot.dims(h).L_A
+        n = rank.rows[h]
+        rows = sorted({0, L_A - 1, L_A, n - 1} | set(rng.choice(n, 6, replace=False).tolist()))
+        x = f64(x_in[h][rows])
+        # pre-attention, row-local: RMSNorm -> QKV -> RoPE at the row's position (G19)
+        hb = OL.bf16(OL.rmsnorm(x, W["attn_norm"], shape.eps))
+        qkv_lin = hb @ W["w_qkv"].T
+        ref = np.concatenate([OL.rope(OL.bf16(qkv_lin).reshape(len(rows), -1, cfg.d)[:, :cfg.hq + cfg.hk],
+                                      np.array(rows), shape.theta),
+                              qkv_lin.reshape(len(rows), -1, cfg.d)[:, cfg.hq + cfg.hk:]], axis=1)
+        got = f64(rank.qkv[h][rows])
+        err = np.abs(got - ref)
+        assert err.max() <= 4 * ULP * np.abs(ref).max() + 1e-2, (h, err.max())
+        # attention over the GPU's Q/K/V and gathered buffer
+        qkv_bits = rank.qkv[h].view(torch.int16).cpu().numpy().view(np.uint16)
+        q, k, v = qkv_bits[:, :cfg.hq], qkv_bits[:, cfg.hq:cfg.hq + cfg.hk], qkv_bits[:, cfg.hq + cfg.hk:]
+        pk, pv = oracle.passing(gathered, h)
+        O_or, _ = oracle.attention(q[rows], k, v, L_A, pk, pv, rows=rows, q_subset=True)
+        e2 = np.abs(f64(rank.attn[h][rows]) - O_or)
+        assert e2.max() <= 2e-2 and e2.mean() <= 2e-3, (h, e2.max(), e2.mean())
+        # O projection + FFN, row-local, from the GPU's attention output
+        ref_out = OL.attn_out_ffn(x, f64(rank.attn[h][rows]), W, rnd=True)
+        x1 = OL.bf16(x + OL.bf16(f64(rank.attn[h][rows]).reshape(len(rows), -1) @ W["w_o"].T))
+        h2 = OL.bf16(OL.rmsnorm(x1, W["ffn_norm"], shape.eps))
+        act = OL.bf16(OL.swiglu(OL.bf16(h2 @ W["w_gu"].T), inter))
+        terms = np.abs(x) + np.abs(x1 - x) + np.abs(ref_out - x1) + np.abs(act) @ np.abs(W["w_down"]).T
+        check(f64(xs[h][rows]), ref_out, f"L8 layer host {h} out ({len(rows)} rows)", rel=2 * ULP, scale=4 * ULP * terms)
