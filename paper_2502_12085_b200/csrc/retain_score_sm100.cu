@@ -170,20 +170,25 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
           const float z = a[e] + b1s[cl + e];
           a[e] = __fdividef(z, 1.f + __expf(-z));  // SiLU
         }
+        // W2 dot on packed FFMA2 (two columns per instruction; half the issue slots of FFMA)
+        uint64_t a2[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) a2[e] = f2_pack(a[2 * e], a[2 * e + 1]);
 #pragma unroll
         for (int oc = 0; oc < kMaxOut; ++oc) {
           if (oc < p.n_out) {
-            const float4* w = reinterpret_cast<const float4*>(w2s + oc * TN + cl);
-            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+            const ulonglong2* w = reinterpret_cast<const ulonglong2*>(w2s + oc * TN + cl);
+            uint64_t acc01 = 0ull, acc23 = 0ull;
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
-              const float4 wv = w[e4];
-              acc0 = fmaf(wv.x, a[4 * e4 + 0], acc0);
-              acc1 = fmaf(wv.y, a[4 * e4 + 1], acc1);
-              acc2 = fmaf(wv.z, a[4 * e4 + 2], acc2);
-              acc3 = fmaf(wv.w, a[4 * e4 + 3], acc3);
+              const ulonglong2 wv = w[e4];
+              acc01 = ffma2(wv.x, a2[2 * e4], acc01);
+              acc23 = ffma2(wv.y, a2[2 * e4 + 1], acc23);
             }
-            o[oc] += (acc0 + acc1) + (acc2 + acc3);
+            float x0, x1, y0, y1;
+            f2_unpack(acc01, x0, x1);
+            f2_unpack(acc23, y0, y1);
+            o[oc] += (x0 + x1) + (y0 + y1);
           }
         }
       }
