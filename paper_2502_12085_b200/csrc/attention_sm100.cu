@@ -77,7 +77,18 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
 __device__ unsigned long long g_trace[64 * 32];
 __device__ int g_trace_block = 0;
 #define TRACE(slot, i) do { if (blockIdx.x == g_trace_block && (i) < 64) g_trace[(i) * 32 + (slot)] = clock64(); } while (0)
+// per-CTA timeline of the last launch: [start globaltimer ns, end ns, smid] for blockIdx < 65536
+__device__ unsigned long long g_cta_time[3 * 65536];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_TIME(k) do { if (threadIdx.x == 0 && blockIdx.x < 65536) { \
+    unsigned int sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); \
+    g_cta_time[3 * blockIdx.x + (k)] = gtimer(); g_cta_time[3 * blockIdx.x + 2] = sm; } } while (0)
 #else
+#define CTA_TIME(k) do {} while (0)
 #define TRACE(slot, i) do {} while (0)
 #endif
 
@@ -212,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   const Item it = decode_item(p, blockIdx.x);
+  CTA_TIME(0);
 
   if (threadIdx.x == 0) {
     mbar_init(bQ, 1);
@@ -602,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  CTA_TIME(1);
   if (warp == kLoadWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -632,6 +645,10 @@ extern "C" int apb_debug_trace(unsigned long long* out, int n, int block) {
     return cudaMemcpyToSymbol(attn::g_trace_block, &block, sizeof(int)) == cudaSuccess ? 0 : 1;
   }
   return cudaMemcpyFromSymbol(out, attn::g_trace, sizeof(unsigned long long) * (n < 2048 ? n : 2048)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int apb_debug_cta_times(unsigned long long* out, int n_ctas) {
+  const int n = 3 * (n_ctas < 65536 ? n_ctas : 65536);
+  return cudaMemcpyFromSymbol(out, attn::g_cta_time, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
 }
 #endif
 

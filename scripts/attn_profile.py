@@ -25,7 +25,13 @@ def main():
     ap.add_argument("--config", default="llama8b-128k")
     ap.add_argument("--score", action="store_true", help="profile apb_retain_score instead")
     ap.add_argument("--trace", type=int, default=None, help="CTA index to trace (uses libapb_trace.so)")
+    ap.add_argument("--ctatimes", action="store_true", help="per-CTA timeline of the last launch (libapb_trace.so): "
+                    "SM utilisation, tail, gaps between CTAs on one SM")
+    ap.add_argument("--clock", type=int, default=0, help="N extra launches with NVML SM-clock sampling: "
+                    "prints the median clock and the fraction of the tensor peak at that clock")
     a = ap.parse_args()
+    if a.ctatimes and a.trace is None:
+        a.trace = 0
     if a.trace is not None:
         import ctypes
         lib = apb.load(apb.LIB_PATH.replace("libapb.so", "libapb_trace.so"))
@@ -65,6 +71,64 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         print(f"iter {i}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
+    if a.clock:
+        import threading
+        import pynvml
+        pynvml.nvmlInit()
+        hdl = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        mhz, stop = [], threading.Event()
+
+        def sample():
+            while not stop.is_set():
+                mhz.append(pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM))
+                stop.wait(0.005)
+        th = threading.Thread(target=sample)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        th.start()
+        e0.record()
+        for _ in range(a.clock):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        stop.set()
+        th.join()
+        ms = e0.elapsed_time(e1) / a.clock
+        f = sorted(mhz)[len(mhz) // 2]
+        tf = flops / ms / 1e9
+        # dense bf16 tcgen05 rate: 8192 FLOP/clk/SM (M=128, N=128, K=16 in 64 cycles) x 148 SMs
+        peak = 148 * 8192 * f * 1e6 / 1e12
+        print(f"clock: {ms:.3f} ms/launch  {tf:.1f} TFLOP/s  SM {f} MHz ({len(mhz)} samples)  "
+              f"tensor peak at that clock {peak:.0f} TF/s -> {tf / peak:.3f}")
+    if a.ctatimes:
+        import numpy as np
+        g_ = cfg.hq // cfg.hk
+        nB, nA = -(-d.l_b // 128), -(-(d.rows - d.l_b) // 128)
+        n_loc = (nB * g_ + 1) // 2 * cfg.hk
+        n_anc = 0 if a.phase == "passing" else (nA * g_ + 1) // 2 * cfg.hk
+        n = n_loc + n_anc
+        buf = (ctypes.c_ulonglong * (3 * n))()
+        lib.apb_debug_cta_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.apb_debug_cta_times(buf, n)
+        t = np.array(list(buf), dtype=np.int64).reshape(n, 3)
+        t0 = t[:, 0].min()
+        st, en, sm = t[:, 0] - t0, t[:, 1] - t0, t[:, 2]
+        span = en.max()
+        busy = (en - st).sum()
+        nsm = 148
+        last = np.array([en[sm == s_].max() for s_ in range(nsm) if (sm == s_).any()])
+        gaps = []
+        for s_ in range(nsm):
+            idx = np.where(sm == s_)[0]
+            o = idx[np.argsort(st[idx])]
+            gaps += list(st[o][1:] - en[o][:-1])
+        gaps = np.array(gaps)
+        dur = en - st
+        print(f"ctas {n} (local {n_loc}, anchor {n_anc}); span {span / 1e3:.1f} us; SM util {busy / (nsm * span):.3f}; "
+              f"SM last-finish p10/p50/p90 {np.percentile(last, 10) / span:.3f}/{np.percentile(last, 50) / span:.3f}/"
+              f"{np.percentile(last, 90) / span:.3f}; gap between CTAs on an SM mean {gaps.mean():.0f} ns "
+              f"p90 {np.percentile(gaps, 90):.0f} ns; CTA us local mean {dur[:n_loc].mean() / 1e3:.1f} max "
+              f"{dur[:n_loc].max() / 1e3:.1f} min {dur[:n_loc].min() / 1e3:.1f}"
+              + (f"; anchor mean {dur[n_loc:].mean() / 1e3:.1f}" if n_anc else ""))
     if a.trace is not None:
         import numpy as np
         buf = (ctypes.c_ulonglong * 2048)()

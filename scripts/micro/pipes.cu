@@ -39,7 +39,7 @@ int main() {
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const char* names[] = {"FFMA", "FFMA2", "FADD2", "MUFU.EX2", "F2FP.BF16x2", "FMNMX3", "FADD", "EX2.F16x2", "EX2.BF16x2", "F2FP.F16x2", "EX2+F2FP(it)", "EX2+PRMT(it)", "EX2+FFMA2(it)", "F2FP+LOP(it)"};
   const int iters = 4096;
-  for (int op = 3; op < 14; ++op) { if (op > 3 && op < 10) continue;
+  for (int op = 0; op < 14; ++op) {
     for (int warps : {4, 8, 16}) {
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       auto launch = [&]() {
