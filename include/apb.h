@@ -232,6 +232,25 @@ apb_status apb_decode_attention(const apb_decode_dims* dims, const void* q, cons
                                 float* part_lse, void* ws, size_t ws_bytes, apb_stream_t stream);
 apb_status apb_decode_workspace_size(const apb_decode_dims* dims, size_t* bytes);
 
+/* The partials of the n_hosts consecutive hosts one rank owns (dims->host .. dims->host +
+ * n_hosts - 1; N < H ranks emulate several hosts per GPU), in ONE launch of the streaming kernel
+ * and ONE fold launch instead of n_hosts of each.  Host i has its own cache k_caches[i] /
+ * v_caches[i] of cache_lens[i] rows (row stride cache_row_stride; dims->cache_len is ignored);
+ * the host with index H-1, if in range, also attends to k_new/v_new.  Host i's partial is
+ * written to parts + i*part_stride: O fp32 [t_new][n_heads][head_dim] at float offset 0 and lse
+ * fp32 [t_new][n_heads] (natural log) at float offset lse_offset.  k_caches, v_caches and
+ * cache_lens are HOST arrays of n_hosts entries, 1 <= n_hosts <= 16 (else APB_ERR_CONFIG);
+ * ws: apb_decode_hosts_workspace_size bytes.  Same partials as n_hosts calls of
+ * apb_decode_attention up to the split plan (the fp32 summation order).                       */
+apb_status apb_decode_attention_hosts(const apb_decode_dims* dims, int32_t n_hosts, const int64_t* cache_lens,
+                                      const void* const* k_caches, const void* const* v_caches,
+                                      int64_t cache_row_stride, const void* q, const void* k_new,
+                                      const void* v_new, int64_t new_row_stride, float* parts,
+                                      int64_t part_stride, int64_t lse_offset, void* ws, size_t ws_bytes,
+                                      apb_stream_t stream);
+apb_status apb_decode_hosts_workspace_size(const apb_decode_dims* dims, int32_t n_hosts, const int64_t* cache_lens,
+                                           size_t* bytes);
+
 /* MergeScore: out[r] = sum_h parts_o[h][r] * exp(parts_lse[h][r] - L[r]),
  * L[r] = log sum_h exp(parts_lse[h][r]).  parts_o fp32 with part stride part_stride_o floats
  * (rows x head_dim each), parts_lse fp32 with part stride part_stride_lse; out bf16 [rows][head_dim];

@@ -28,7 +28,8 @@ WS_RETAIN, WS_SELECT, WS_ATTENTION = 0, 1, 2
 EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
             "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
             "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count",
-            "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials")
+            "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
+            "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size")
 
 
 class ApbError(RuntimeError):
@@ -82,6 +83,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     ddp = ctypes.POINTER(_DecodeDims)
     lib.apb_decode_attention.argtypes = [ddp, vp, vp, vp, i64, vp, vp, i64, vp, vp, vp, sz, vp]
     lib.apb_decode_workspace_size.argtypes = [ddp, ctypes.POINTER(sz)]
+    lib.apb_decode_attention_hosts.argtypes = [ddp, i32, vp, vp, vp, i64, vp, vp, vp, i64, vp, i64, i64, vp, sz, vp]
+    lib.apb_decode_hosts_workspace_size.argtypes = [ddp, i32, vp, ctypes.POINTER(sz)]
     lib.apb_merge_partials.argtypes = [i32, i64, i32, vp, i64, vp, i64, vp, vp, vp]
     lib.apb_exchange_partials.argtypes = [vp, i64, vp, vp]
     lib.apb_random_scores.argtypes = [dp, ctypes.c_uint64, i32, vp, vp]
@@ -93,7 +96,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
-              "apb_exchange_partials"):
+              "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -350,6 +353,42 @@ def decode_attention(dims: DecodeDims, q, k_cache, v_cache, k_new, v_new, part_o
                                        _ptr(k_new), _ptr(v_new), ns, part_o.data_ptr(), part_lse.data_ptr(),
                                        _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                                        _stream(stream)), "apb_decode_attention")
+
+
+def _host_arrays(cache_lens, k_caches, v_caches):
+    n = len(cache_lens)
+    lens = (ctypes.c_int64 * n)(*cache_lens)
+    kp = (ctypes.c_void_p * n)(*[_ptr(k) for k in k_caches]) if k_caches is not None else None
+    vp = (ctypes.c_void_p * n)(*[_ptr(v) for v in v_caches]) if v_caches is not None else None
+    return n, lens, kp, vp
+
+
+def decode_hosts_workspace_size(dims: DecodeDims, cache_lens: list[int]) -> int:
+    out = ctypes.c_size_t(0)
+    d = dims.c()
+    n, lens, _, _ = _host_arrays(cache_lens, None, None)
+    _check(load().apb_decode_hosts_workspace_size(ctypes.byref(d), n, lens, ctypes.byref(out)),
+           "apb_decode_hosts_workspace_size")
+    return out.value
+
+
+def decode_attention_hosts(dims: DecodeDims, q, k_caches: list, v_caches: list, k_new, v_new, parts,
+                           lse_offset: int, ws=None, stream=None) -> None:
+    """Partials of hosts dims.host .. dims.host + len(k_caches) - 1 in one launch (+ one fold):
+    host i's O at parts[i][:lse_offset], its lse at parts[i][lse_offset:] (parts fp32 [n][stride])."""
+    lens = [k.shape[0] for k in k_caches]
+    nz = [k for k in k_caches if k.numel()]
+    cs = _rowstride(nz[0], "k_cache") if nz else 0
+    for t in list(k_caches) + list(v_caches):
+        if t.numel() and _rowstride(t, "cache") != cs:
+            raise ValueError("all caches of one call must share a row stride")
+    ns = _rowstride(k_new, "k_new") if k_new is not None else 0
+    n, lp, kp, vp = _host_arrays(lens, k_caches, v_caches)
+    d = dims.c()
+    _check(load().apb_decode_attention_hosts(ctypes.byref(d), n, lp, kp, vp, cs, q.data_ptr(), _ptr(k_new),
+                                             _ptr(v_new), ns, parts.data_ptr(), parts.stride(0), lse_offset,
+                                             _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                                             _stream(stream)), "apb_decode_attention_hosts")
 
 
 def merge_partials(n_parts: int, rows: int, head_dim: int, parts_o, stride_o: int, parts_lse, stride_lse: int,

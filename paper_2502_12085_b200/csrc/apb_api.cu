@@ -576,6 +576,85 @@ extern "C" apb_status apb_decode_attention(const apb_decode_dims* d, const void*
   return launch_decode(p, part_o, part_lse, reinterpret_cast<cudaStream_t>(stream));
 }
 
+static apb_status check_decode_hosts(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens) {
+  apb_status st = check_decode_dims(d);
+  if (st) return st;
+  if (n < 1 || n > kDecMaxHosts || d->host + n > d->H) return fail(APB_ERR_CONFIG, "n_hosts must be in [1, 16] and host + n_hosts <= H");
+  if (!cache_lens) return fail(APB_ERR_CONTRACT, "cache_lens is NULL");
+  for (int i = 0; i < n; ++i)
+    if (cache_lens[i] < 0) return fail(APB_ERR_CONFIG, "cache_lens[i] >= 0 required");
+  return APB_OK;
+}
+
+static void decode_hosts_keys(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens, int64_t* keys) {
+  for (int i = 0; i < n; ++i) keys[i] = cache_lens[i] + (d->host + i == d->H - 1 ? d->t_new : 0);
+}
+
+extern "C" apb_status apb_decode_hosts_workspace_size(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens,
+                                                      size_t* bytes) {
+  if (!bytes) return fail(APB_ERR_CONTRACT, "bytes is NULL");
+  apb_status st = check_decode_hosts(d, n, cache_lens);
+  if (st) return st;
+  int64_t keys[kDecMaxHosts];
+  decode_hosts_keys(d, n, cache_lens, keys);
+  *bytes = decode_hosts_workspace_bytes(n, keys, d->t_new, d->n_heads, d->n_kv_heads, d->head_dim);
+  return APB_OK;
+}
+
+extern "C" apb_status apb_decode_attention_hosts(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens,
+                                                 const void* const* k_caches, const void* const* v_caches,
+                                                 int64_t cache_row_stride, const void* q, const void* k_new,
+                                                 const void* v_new, int64_t new_row_stride, float* parts,
+                                                 int64_t part_stride, int64_t lse_offset, void* ws, size_t ws_bytes,
+                                                 apb_stream_t stream) {
+  apb_status st = check_decode_hosts(d, n, cache_lens);
+  if (st) return st;
+  const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
+  if (!q || !aligned16(q)) return fail(APB_ERR_CONTRACT, "q NULL or misaligned");
+  if (!k_caches || !v_caches) return fail(APB_ERR_CONTRACT, "k_caches/v_caches is NULL");
+  DecodeHosts hb{};
+  hb.n = n;
+  hb.new_host = -1;
+  for (int i = 0; i < n; ++i) {
+    if (cache_lens[i] > 0) {
+      if ((st = check_rows(k_caches[i], cache_row_stride, (int64_t)hk * D, "k_caches[i]"))) return st;
+      if ((st = check_rows(v_caches[i], cache_row_stride, (int64_t)hk * D, "v_caches[i]"))) return st;
+    }
+    hb.cache_len[i] = cache_lens[i];
+    hb.k_cache[i] = static_cast<const __nv_bfloat16*>(k_caches[i]);
+    hb.v_cache[i] = static_cast<const __nv_bfloat16*>(v_caches[i]);
+    if (d->host + i == d->H - 1) hb.new_host = i;
+  }
+  if (hb.new_host >= 0) {
+    if ((st = check_rows(k_new, new_row_stride, (int64_t)hk * D, "k_new"))) return st;
+    if ((st = check_rows(v_new, new_row_stride, (int64_t)hk * D, "v_new"))) return st;
+  }
+  const int64_t rows = (int64_t)d->t_new * hq;
+  if (!parts || !aligned16(parts)) return fail(APB_ERR_CONTRACT, "parts NULL or misaligned");
+  if (part_stride < rows * D + rows || lse_offset < rows * D || lse_offset + rows > part_stride)
+    return fail(APB_ERR_CONTRACT, "part_stride / lse_offset do not hold O [rows][head_dim] and lse [rows]");
+  int64_t keys[kDecMaxHosts];
+  decode_hosts_keys(d, n, cache_lens, keys);
+  const size_t need = decode_hosts_workspace_bytes(n, keys, d->t_new, hq, hk, D);
+  if (need && (!ws || ws_bytes < need || !aligned16(ws))) return fail(APB_ERR_CONTRACT, "decode workspace missing or too small");
+  if ((st = check_device())) return st;
+  DecodeParams p{};
+  p.t = d->t_new;
+  p.hq = hq;
+  p.hk = hk;
+  p.g = hq / hk;
+  p.D = D;
+  p.cache_row_stride = cache_row_stride;
+  p.new_row_stride = new_row_stride;
+  const float scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)D);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  p.ws_o = static_cast<float*>(ws);
+  return launch_decode_hosts(p, hb, keys, parts, part_stride, lse_offset, reinterpret_cast<cudaStream_t>(stream));
+}
+
 extern "C" apb_status apb_merge_partials(int32_t n_parts, int64_t rows, int32_t head_dim, const float* parts_o,
                                          int64_t part_stride_o, const float* parts_lse, int64_t part_stride_lse,
                                          void* out, float* out_lse, apb_stream_t stream) {

@@ -30,6 +30,13 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src,
 #endif
 constexpr int SKC = 64;                                  // keys per chunk
 constexpr int kSplitTarget = APB_DEC_CTAS_PER_SM * 148;  // CTAs per launch to aim for (per SM x B200 SMs)
+// The multi-host launch streams longer ranges per split; it runs faster over-subscribed (more
+// CTAs than fit at once; per L8 step: 3 x 148 0.148 ms, 4 x 0.142, 5 x 0.132, 6 x 0.124, 8 x 0.124,
+// 12 x 0.133 ms).
+#ifndef APB_DEC_HOSTS_CTAS_PER_SM
+#define APB_DEC_HOSTS_CTAS_PER_SM 6
+#endif
+constexpr int kHostsSplitTarget = APB_DEC_HOSTS_CTAS_PER_SM * 148;
 
 // ---------------------------------------------------------------- tensor-core split-KV
 // decode_mma_kernel: the same streaming split-KV plan, with both products on the tensor cores
@@ -82,7 +89,8 @@ __device__ __forceinline__ uint32_t kv_off(int r, int c) {
 }
 
 template <int D, int MT>
-__global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParams p, int chunks_per_split) {
+__global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParams p, const DecodeHosts hb,
+                                                                 int chunks_per_split) {
   using L = MmaSmem<D>;
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int NT = D / 64;  // O n-tiles (of 8 columns) per warp: D/8 tiles over 8 warps
@@ -93,9 +101,24 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
   float* xl = xm + 8 * 16 * MT;                                                      // [8][16 MT]
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int g8 = lane / 4, t4 = lane % 4;
-  const int split = blockIdx.x, j = blockIdx.y;
-  const int64_t n_keys = p.cache_len + (p.has_new ? p.t : 0);
-  const int64_t c_first = (int64_t)split * chunks_per_split;
+  const int split = blockIdx.x, j = blockIdx.y;  // split: index into the workspace partials
+  // multi-host launch: this split's host (its cache, length, whether it sees the new tokens)
+  int split_local = split;
+  const __nv_bfloat16* k_cache = p.k_cache;
+  const __nv_bfloat16* v_cache = p.v_cache;
+  int64_t cache_len = p.cache_len;
+  int has_new = p.has_new;
+  if (hb.n > 0) {
+    int i = 0;
+    while (i + 1 < hb.n && split >= hb.split_begin[i + 1]) ++i;
+    split_local = split - hb.split_begin[i];
+    k_cache = hb.k_cache[i];
+    v_cache = hb.v_cache[i];
+    cache_len = hb.cache_len[i];
+    has_new = (i == hb.new_host) ? 1 : 0;
+  }
+  const int64_t n_keys = cache_len + (has_new ? p.t : 0);
+  const int64_t c_first = (int64_t)split_local * chunks_per_split;
   const int64_t n_chunks_total = (n_keys + MKC - 1) / MKC;
   const int nch = (int)((c_first + chunks_per_split <= n_chunks_total) ? chunks_per_split
                                                                        : (n_chunks_total > c_first ? n_chunks_total - c_first : 0));
@@ -109,11 +132,11 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
     for (int idx = tid; idx < MKC * kVec; idx += kMThreads) {
       const int kk = idx / kVec, cv = idx % kVec;
       const int64_t key = k0 + kk;
-      const bool cached = key < p.cache_len, valid = key < n_keys;
-      const __nv_bfloat16* kb = cached ? p.k_cache + key * p.cache_row_stride
-                                       : p.k_new + (key - p.cache_len) * p.new_row_stride;
-      const __nv_bfloat16* vb = cached ? p.v_cache + key * p.cache_row_stride
-                                       : p.v_new + (key - p.cache_len) * p.new_row_stride;
+      const bool cached = key < cache_len, valid = key < n_keys;
+      const __nv_bfloat16* kb = cached ? k_cache + key * p.cache_row_stride
+                                       : p.k_new + (key - cache_len) * p.new_row_stride;
+      const __nv_bfloat16* vb = cached ? v_cache + key * p.cache_row_stride
+                                       : p.v_new + (key - cache_len) * p.new_row_stride;
       cp_async16(ks + kv_off<D>(kk, cv), valid ? kb + (int64_t)j * D + cv * 8 : p.q, valid);
       cp_async16(vs + kv_off<D>(kk, cv), valid ? vb + (int64_t)j * D + cv * 8 : p.q, valid);
     }
@@ -184,7 +207,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
       for (int e = 0; e < 4; ++e) {
         const int r = mt * 16 + g8 + (e >> 1) * 8;
         const int64_t key = k0 + key_a + (e & 1);
-        const bool vis = r < R && key < n_keys && (key < p.cache_len || key - p.cache_len <= r / p.g);
+        const bool vis = r < R && key < n_keys && (key < cache_len || key - cache_len <= r / p.g);
         sc[mt][e] = vis ? sc[mt][e] * sl2 : -INFINITY;
       }
       float m0 = fmaxf(sc[mt][0], sc[mt][1]), m1 = fmaxf(sc[mt][2], sc[mt][3]);
@@ -288,14 +311,12 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
 // head_dim, coalesced), and the 8 warp partials are added in a fixed order — deterministic.
 constexpr int kMergeWarps = 8;
 template <int D, typename OutT>
-__global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(int n, int64_t rows, const float* __restrict__ parts_o,
-                                                                 const float* __restrict__ parts_lse, int64_t stride_o,
-                                                                 int64_t stride_lse, int lse_in_log2,
-                                                                 OutT* __restrict__ out, float* __restrict__ out_lse) {
+__device__ __forceinline__ void merge_row(int64_t row, int n, const float* __restrict__ parts_o,
+                                          const float* __restrict__ parts_lse, int64_t stride_o, int64_t stride_lse,
+                                          int lse_in_log2, OutT* __restrict__ out, float* __restrict__ out_lse) {
   extern __shared__ float wsm[];  // [n] weights
   __shared__ float red[kMergeWarps];
   __shared__ float part[kMergeWarps][D];
-  const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const float to2 = lse_in_log2 ? 1.f : 1.4426950408889634f;  // convert to the log2 domain
   float m = -INFINITY;
@@ -351,6 +372,28 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(int n, int64_t 
   if (tid == 0 && out_lse) out_lse[row] = (z > 0.f) ? (m + __log2f(z)) * 0.69314718055994530942f : -INFINITY;
 }
 
+template <int D, typename OutT>
+__global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(int n, int64_t rows, const float* __restrict__ parts_o,
+                                                                 const float* __restrict__ parts_lse, int64_t stride_o,
+                                                                 int64_t stride_lse, int lse_in_log2,
+                                                                 OutT* __restrict__ out, float* __restrict__ out_lse) {
+  merge_row<D, OutT>(blockIdx.x, n, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, out, out_lse);
+}
+
+// Fold of a multi-host launch: CTA (row, host i) merges host i's splits (log2 lse in the
+// workspace) into its partial at parts + i*part_stride (O) and + lse_offset (natural lse).
+template <int D>
+__global__ void __launch_bounds__(kMergeWarps * 32) fold_hosts_kernel(const DecodeHosts hb, int64_t rows,
+                                                                      const float* __restrict__ ws_o,
+                                                                      const float* __restrict__ ws_lse,
+                                                                      float* __restrict__ parts, int64_t part_stride,
+                                                                      int64_t lse_offset) {
+  const int i = blockIdx.y, s0 = hb.split_begin[i];
+  float* dst = parts + (int64_t)i * part_stride;
+  merge_row<D, float>(blockIdx.x, hb.split_begin[i + 1] - s0, ws_o + (int64_t)s0 * rows * D, ws_lse + (int64_t)s0 * rows,
+                      rows * D, rows, 1, dst, dst + lse_offset);
+}
+
 }  // namespace dec
 
 // Split plan of the streaming kernel: ~kSplitTarget CTAs over (splits x KV heads), whole
@@ -383,6 +426,63 @@ size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int hk, int D) {
   return ws_off_lse(splits, rows, D) + (size_t)splits * rows * sizeof(float);
 }
 
+// Multi-host split plan: one chunk size (chunks per split) for all hosts, from the total chunk
+// count and the launch's CTA target, so every split streams the same number of chunks.
+static int64_t decode_hosts_plan(int n, const int64_t* n_keys, int hk, int* split_begin, int* chunks_per_split) {
+  int64_t total_chunks = 0;
+  for (int i = 0; i < n; ++i) total_chunks += (n_keys[i] + dec::SKC - 1) / dec::SKC;
+  int64_t target = (dec::kHostsSplitTarget + hk - 1) / hk;
+  if (target < 1) target = 1;
+  const int64_t cps = total_chunks > 0 ? (total_chunks + target - 1) / target : 1;
+  *chunks_per_split = (int)cps;
+  int64_t acc = 0;
+  for (int i = 0; i < n; ++i) {
+    split_begin[i] = (int)acc;
+    acc += ((n_keys[i] + dec::SKC - 1) / dec::SKC + cps - 1) / cps;
+  }
+  split_begin[n] = (int)acc;
+  return acc;
+}
+
+size_t decode_hosts_workspace_bytes(int n, const int64_t* n_keys, int t, int hq, int hk, int D) {
+  int sb[kDecMaxHosts + 1];
+  int cps;
+  const int64_t splits = decode_hosts_plan(n, n_keys, hk, sb, &cps);
+  const int64_t rows = (int64_t)t * hq;
+  return ws_off_lse(splits, rows, D) + (size_t)splits * rows * sizeof(float);
+}
+
+// the streaming kernel over `splits` x KV heads (hb.n == 0: one host, all of p)
+static apb_status launch_partials(const DecodeParams& p, const DecodeHosts& hb, int64_t splits, int cps,
+                                  cudaStream_t stream) {
+  dim3 grid((unsigned)splits, p.hk);
+  const int R = p.t * p.g;
+  const int mt = (R + 15) / 16;  // 16-row m-tiles
+  apb_status st = APB_OK;
+  auto launch = [&](auto kern, int MT, int D) {
+    // one set-once device mask per kernel instantiation (D, MT)
+    const int smem = D == 128 ? dec::MmaSmem<128>::bytes(MT) : dec::MmaSmem<64>::bytes(MT);
+    static std::atomic<uint64_t> smem_set[2][3];
+    const int di = D == 128 ? 0 : 1, mi = MT <= 1 ? 0 : (MT <= 2 ? 1 : 2);
+    st = set_max_smem_once(reinterpret_cast<const void*>(kern), smem, smem_set[di][mi]);
+    if (st == APB_OK) kern<<<grid, dec::kMThreads, smem, stream>>>(p, hb, cps);
+  };
+  if (p.D == 128) {
+    if (mt <= 1) launch(dec::decode_mma_kernel<128, 1>, 1, 128);
+    else if (mt <= 2) launch(dec::decode_mma_kernel<128, 2>, 2, 128);
+    else launch(dec::decode_mma_kernel<128, 4>, 4, 128);
+  } else {
+    if (mt <= 1) launch(dec::decode_mma_kernel<64, 1>, 1, 64);
+    else if (mt <= 2) launch(dec::decode_mma_kernel<64, 2>, 2, 64);
+    else launch(dec::decode_mma_kernel<64, 4>, 4, 64);
+  }
+  if (st) return st;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
 apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse, cudaStream_t stream) {
   DecodeParams p = p0;
   const int64_t n_keys = p.cache_len + (p.has_new ? p.t : 0);
@@ -392,37 +492,43 @@ apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse,
   const int64_t rows = (int64_t)p.t * p.hq;
   char* base = reinterpret_cast<char*>(p.ws_o);
   p.ws_lse = reinterpret_cast<float*>(base + ws_off_lse(splits, rows, p.D));
-  dim3 grid((unsigned)splits, p.hk);
   if (splits == 0)  // no key at all: the merge of zero parts writes O = 0, lse = -inf
     return launch_merge(0, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream);
-  {
-    const int R = p.t * p.g;
-    const int mt = (R + 15) / 16;  // 16-row m-tiles
-    apb_status st = APB_OK;
-    auto launch = [&](auto kern, int MT, int D) {
-      // one set-once device mask per kernel instantiation (D, MT)
-      const int smem = D == 128 ? dec::MmaSmem<128>::bytes(MT) : dec::MmaSmem<64>::bytes(MT);
-      static std::atomic<uint64_t> smem_set[2][3];
-      const int di = D == 128 ? 0 : 1, mi = MT <= 1 ? 0 : (MT <= 2 ? 1 : 2);
-      st = set_max_smem_once(reinterpret_cast<const void*>(kern), smem, smem_set[di][mi]);
-      if (st == APB_OK) kern<<<grid, dec::kMThreads, smem, stream>>>(p, cps);
-    };
-    if (p.D == 128) {
-      if (mt <= 1) launch(dec::decode_mma_kernel<128, 1>, 1, 128);
-      else if (mt <= 2) launch(dec::decode_mma_kernel<128, 2>, 2, 128);
-      else launch(dec::decode_mma_kernel<128, 4>, 4, 128);
-    } else {
-      if (mt <= 1) launch(dec::decode_mma_kernel<64, 1>, 1, 64);
-      else if (mt <= 2) launch(dec::decode_mma_kernel<64, 2>, 2, 64);
-      else launch(dec::decode_mma_kernel<64, 4>, 4, 64);
-    }
-    if (st) return st;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
-    count_launch();
-  }
+  DecodeHosts hb{};
+  hb.n = 0;
+  hb.new_host = -1;
+  if (apb_status st = launch_partials(p, hb, splits, cps, stream)) return st;
   // fold the splits (LSE merge, fixed order): the host's fp32 partial, natural-log lse
   return launch_merge((int)splits, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream);
+}
+
+apb_status launch_decode_hosts(const DecodeParams& p0, DecodeHosts hb, const int64_t* n_keys, float* parts,
+                               int64_t part_stride, int64_t lse_offset, cudaStream_t stream) {
+  DecodeParams p = p0;
+  int cps;
+  const int64_t splits = decode_hosts_plan(hb.n, n_keys, p.hk, hb.split_begin, &cps);
+  const int64_t rows = (int64_t)p.t * p.hq;
+  char* base = reinterpret_cast<char*>(p.ws_o);
+  p.ws_lse = reinterpret_cast<float*>(base + ws_off_lse(splits, rows, p.D));
+  if (splits > 0)
+    if (apb_status st = launch_partials(p, hb, splits, cps, stream)) return st;
+  if (rows == 0) return APB_OK;
+  const dim3 grid((unsigned)rows, (unsigned)hb.n);
+  size_t smem = 0;
+  for (int i = 0; i < hb.n; ++i) {
+    const size_t b = (size_t)(hb.split_begin[i + 1] - hb.split_begin[i]) * sizeof(float);
+    smem = b > smem ? b : smem;
+  }
+  if (p.D == 128)
+    dec::fold_hosts_kernel<128><<<grid, dec::kMergeWarps * 32, smem, stream>>>(hb, rows, p.ws_o, p.ws_lse, parts,
+                                                                                part_stride, lse_offset);
+  else
+    dec::fold_hosts_kernel<64><<<grid, dec::kMergeWarps * 32, smem, stream>>>(hb, rows, p.ws_o, p.ws_lse, parts,
+                                                                               part_stride, lse_offset);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("fold launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
 }
 
 apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,

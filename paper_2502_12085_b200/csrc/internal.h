@@ -88,8 +88,24 @@ struct DecodeParams {
   float* ws_o;                   // [splits][t*hq][D] then (256-B aligned) ws_lse [splits][t*hq]
   float* ws_lse;
 };
+// Several hosts' partials in one launch (the hosts one rank owns): per-host cache pointers and
+// lengths; host i's splits are [split_begin[i], split_begin[i+1]) of the launch's split axis.
+constexpr int kDecMaxHosts = 16;
+struct DecodeHosts {
+  int n;         // 0: single-host launch (DecodeParams alone)
+  int new_host;  // index i of the host that also attends to the new tokens (-1: none)
+  int split_begin[kDecMaxHosts + 1];
+  int64_t cache_len[kDecMaxHosts];
+  const __nv_bfloat16* k_cache[kDecMaxHosts];
+  const __nv_bfloat16* v_cache[kDecMaxHosts];
+};
 size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int hk, int D);
+size_t decode_hosts_workspace_bytes(int n, const int64_t* n_keys, int t, int hq, int hk, int D);
 apb_status launch_decode(const DecodeParams& p, float* part_o, float* part_lse, cudaStream_t stream);
+// p: common fields (q, k_new/v_new, strides, scale, ws); n hosts with keys n_keys[i] (cache plus
+// the new tokens for hb.new_host); host i's partial -> parts + i*part_stride (O), + lse_offset (lse)
+apb_status launch_decode_hosts(const DecodeParams& p, DecodeHosts hb, const int64_t* n_keys, float* parts,
+                               int64_t part_stride, int64_t lse_offset, cudaStream_t stream);
 apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,
                         int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,
                         cudaStream_t stream);

@@ -15,10 +15,13 @@ from . import apb
 
 class DecodeRank:
     def __init__(self, H: int, hosts: list[int], t_new: int, n_heads: int, n_kv_heads: int, head_dim: int,
-                 comm: apb.Comm | None = None, device="cuda", softmax_scale: float = 0.0):
+                 comm: apb.Comm | None = None, device="cuda", softmax_scale: float = 0.0,
+                 batch_hosts: bool = True):
+        """batch_hosts: with several owned hosts, one apb_decode_attention_hosts call (one
+        streaming launch + one fold) instead of one apb_decode_attention per host."""
         self.H, self.hosts, self.t = H, list(hosts), t_new
         self.hq, self.hk, self.d = n_heads, n_kv_heads, head_dim
-        self.comm, self.scale = comm, softmax_scale
+        self.comm, self.scale, self.batch_hosts = comm, softmax_scale, batch_hosts
         self.device = torch.device(device)
         self.rows = t_new * n_heads
         # floats per host: O [rows][d] then lse [rows], padded to 16 B so every slot stays aligned
@@ -32,16 +35,30 @@ class DecodeRank:
     def step(self, q, caches: dict, k_new, v_new, out, out_lse=None, stream=None) -> None:
         """q: [t][hq][d] bf16 (same on every host); caches: {host: (k_cache, v_cache)} for the owned
         hosts ([c_h][hk][d] bf16); k_new/v_new: [t][hk][d] bf16; out: [t][hq][d] bf16."""
-        for h in self.hosts:
-            kc, vc = caches[h]
-            d = self.dims(h, kc.shape[0])
-            n = apb.decode_workspace_size(d)
-            if self.ws.get(h) is None or self.ws[h].numel() < n:
-                self.ws[h] = torch.zeros(max(n, 16), dtype=torch.uint8, device=self.device)
-            slot = self.parts[h]
-            apb.decode_attention(d, q, kc, vc, k_new if h == self.H - 1 else None,
-                                 v_new if h == self.H - 1 else None, slot[: self.rows * self.d],
-                                 slot[self.rows * self.d:], self.ws[h], stream=stream)
+        if len(self.hosts) > 1 and self.batch_hosts:
+            # every owned host's partial in one streaming launch + one fold (same partials up to
+            # the split plan's fp32 summation order)
+            h0 = self.hosts[0]
+            kcs, vcs = [caches[h][0] for h in self.hosts], [caches[h][1] for h in self.hosts]
+            d = self.dims(h0, 0)
+            n = apb.decode_hosts_workspace_size(d, [k.shape[0] for k in kcs])
+            if self.ws.get("batch") is None or self.ws["batch"].numel() < n:
+                self.ws["batch"] = torch.zeros(max(n, 16), dtype=torch.uint8, device=self.device)
+            last_owned = self.H - 1 in self.hosts
+            apb.decode_attention_hosts(d, q, kcs, vcs, k_new if last_owned else None, v_new if last_owned else None,
+                                       self.parts[h0: h0 + len(self.hosts)], self.rows * self.d, self.ws["batch"],
+                                       stream=stream)
+        else:
+            for h in self.hosts:
+                kc, vc = caches[h]
+                d = self.dims(h, kc.shape[0])
+                n = apb.decode_workspace_size(d)
+                if self.ws.get(h) is None or self.ws[h].numel() < n:
+                    self.ws[h] = torch.zeros(max(n, 16), dtype=torch.uint8, device=self.device)
+                slot = self.parts[h]
+                apb.decode_attention(d, q, kc, vc, k_new if h == self.H - 1 else None,
+                                     v_new if h == self.H - 1 else None, slot[: self.rows * self.d],
+                                     slot[self.rows * self.d:], self.ws[h], stream=stream)
         per_rank = self.slot * (self.H // (self.comm.nranks if self.comm else 1))
         apb.exchange_partials(self.comm, per_rank, self.parts, stream=stream)
         apb.merge_partials(self.H, self.rows, self.d, self.parts, self.slot, self.parts[:, self.rows * self.d:],

@@ -62,6 +62,38 @@ def test_decode_partial_parity(c, t, last, d, hq, hk):
     _check(po.cpu().double().numpy(), pl.cpu().double().numpy(), O_or, l_or, f"partial c={c} t={t} last={last}")
 
 
+@pytest.mark.parametrize("lens,host0,H", [([0, 1, 255, 257, 1000], 0, 5), ([64, 0, 130], 2, 5), ([300], 3, 4),
+                                           ([513, 70, 0, 2000, 5, 128, 64, 9], 0, 8)])
+@pytest.mark.parametrize("t", [1, 4])
+@pytest.mark.parametrize("d,hq,hk", [(128, 8, 2), (64, 6, 2)])
+def test_decode_hosts_partials_parity(lens, host0, H, t, d, hq, hk):
+    """apb_decode_attention_hosts (one launch for the hosts a rank owns): every host's partial vs
+    the oracle, ragged cache lengths (empty, chunk boundaries), with and without the last host."""
+    from paper_2502_12085_b200 import apb
+    rng = np.random.default_rng(sum(lens) + 7 * t + d)
+    q = _bits((t, hq, d), rng, 1.5)
+    kn, vn = _bits((t, hk, d), rng, 1.5), _bits((t, hk, d), rng)
+    caches = [(_bits((c, hk, d), rng, 1.5), _bits((c, hk, d), rng)) for c in lens]
+    n, rows = len(lens), t * hq
+    stride = (rows * d + rows + 3) // 4 * 4 + 4  # a padded part stride: exercises part_stride != rows*(d+1)
+    parts = torch.full((n, stride), float("nan"), device="cuda")
+    dims = apb.DecodeDims(H, host0, t, 0, hq, hk, d)
+    ws = torch.zeros(max(apb.decode_hosts_workspace_size(dims, lens), 16), dtype=torch.uint8, device="cuda")
+    kcs = [dev(k) if c else torch.empty((0, hk, d), dtype=torch.bfloat16, device="cuda") for (k, _), c in zip(caches, lens)]
+    vcs = [dev(v) if c else torch.empty((0, hk, d), dtype=torch.bfloat16, device="cuda") for (_, v), c in zip(caches, lens)]
+    last = host0 + n == H
+    apb.decode_attention_hosts(dims, dev(q), kcs, vcs, dev(kn) if last else None, dev(vn) if last else None,
+                               parts, rows * d, ws)
+    torch.cuda.synchronize()
+    P = parts.cpu().double().numpy()
+    for i in range(n):
+        is_last = host0 + i == H - 1
+        O_or, l_or = oracle.decode_partial(q, caches[i][0], caches[i][1], kn if is_last else None,
+                                           vn if is_last else None)
+        _check(P[i, : rows * d].reshape(t, hq, d), P[i, rows * d: rows * d + rows].reshape(t, hq), O_or, l_or,
+               f"hosts partial {host0 + i} c={lens[i]} t={t}")
+
+
 def test_merge_partials_parity():
     from paper_2502_12085_b200 import apb
     rng = np.random.default_rng(3)
@@ -83,8 +115,9 @@ def test_merge_partials_parity():
     assert np.isneginf(ol.cpu().numpy()[7])
 
 
+@pytest.mark.parametrize("batch", [True, False])
 @pytest.mark.parametrize("name,t", [("toy", 1), ("toy", 3), ("gqa3", 2)])
-def test_decode_step_end_to_end(name, t):
+def test_decode_step_end_to_end(name, t, batch):
     """All hosts on one GPU through DecodeRank: partials -> (in-place) gather -> MergeScore, vs the
     oracle's decode step AND vs exact attention over [B_1 .. B_H | new] (the step is exact)."""
     from paper_2502_12085_b200.decode import DecodeRank
@@ -95,7 +128,7 @@ def test_decode_step_end_to_end(name, t):
     caches = [(x["k"][x["L_A"]:], x["v"][x["L_A"]:]) for x in hosts]  # block KV cache
     q = _bits((t, cfg.hq, cfg.d), rng)
     kn, vn = _bits((t, cfg.hk, cfg.d), rng), _bits((t, cfg.hk, cfg.d), rng)
-    dr = DecodeRank(cfg.H, list(range(cfg.H)), t, cfg.hq, cfg.hk, cfg.d)
+    dr = DecodeRank(cfg.H, list(range(cfg.H)), t, cfg.hq, cfg.hk, cfg.d, batch_hosts=batch)
     out = torch.empty((t, cfg.hq, cfg.d), dtype=torch.bfloat16, device="cuda")
     ol = torch.empty((t, cfg.hq), device="cuda")
     dr.step(dev(q), {h: (dev(kc), dev(vc)) for h, (kc, vc) in enumerate(caches)}, dev(kn), dev(vn), out, ol)
