@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", default="llama8b-128k")
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (default: the model's)")
     ap.add_argument("--hosts", type=int, default=None, help="override H (default: the paper's 8)")
+    ap.add_argument("--host-layout", choices=["cyclic", "block"], default="cyclic",
+                    help="host ownership when N < H ranks: cyclic r, r+N, ... (work-balanced) or contiguous blocks")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -243,7 +245,7 @@ def main():
     layers = args.layers or cfg.layers
     base = apb.Dims(n=cfg.n, H=H, host=0, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
                     head_dim=cfg.d, l_q=cfg.l_q)
-    hosts = hosts_of_rank(H, world, rank)
+    hosts = hosts_of_rank(H, world, rank, args.host_layout)
     comm = None
     if world > 1 and not args.same_device:
         uid = [apb.Comm.unique_id() if rank == 0 else None]
@@ -355,9 +357,11 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) Q/K/V, random-init retaining heads)",
-                "config": workload_config(cfg, H, layers, world,
+                "config": dict(workload_config(cfg, H, layers, world,
                                           ("" if args.compressor == "retain" else " [compressor Rd.]")
                                           + (" [shared index set]" if args.shared_set else "")),
+                               host_layout=("all hosts on one GPU" if world == 1 else
+                                            args.host_layout if world < H else "one host per GPU")),
                 "attn_peak_frac": {"critical_host": round(crit * layers / (ms_per_step / 1e3) / 1e12 / peak_tf, 4)
                                    if world == H else None,
                                    "aggregate": round(flops_all * layers / (ms_per_step / 1e3) / 1e12 / (peak_tf * world), 4)},

@@ -181,6 +181,13 @@ apb_status apb_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, ap
 apb_status apb_comm_destroy(apb_comm* comm);
 apb_status apb_exchange_passing(apb_comm* comm, const apb_dims* dims, void* gathered,
                                 apb_stream_t stream);
+/* The same exchange for CYCLIC host ownership (N < H ranks, work-balanced: the later hosts carry
+ * more passing keys, so rank r owning hosts r, r+N, r+2N, ... levels the per-rank attention
+ * work that contiguous blocks skew towards the last rank).  H/N in-place AllGathers, round k
+ * gathering slots [k*N, (k+1)*N) in host order.  Same buffer, same result; equal to
+ * apb_exchange_passing when N == H.                                                      */
+apb_status apb_exchange_passing_cyclic(apb_comm* comm, const apb_dims* dims, void* gathered,
+                                       apb_stream_t stream);
 
 /* ---------------------------------------------------------------- step 4: masked attention
  * eq:apb: for query head qh and query row r in [0, L_A + l_b), with the key

@@ -29,7 +29,7 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
             "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count",
             "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
-            "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size")
+            "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic")
 
 
 class ApbError(RuntimeError):
@@ -74,6 +74,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_retain_score.argtypes = [dp, ctypes.POINTER(_Weights), vp, vp, vp, i64, i64, vp, vp, sz, vp]
     lib.apb_select_topk.argtypes = [dp, vp, vp, vp, i64, vp, vp, vp, sz, vp]
     lib.apb_exchange_passing.argtypes = [vp, dp, vp, vp]
+    lib.apb_exchange_passing_cyclic.argtypes = [vp, dp, vp, vp]
     lib.apb_attention_fwd.argtypes = [dp, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.c_int, vp, sz, vp]
     lib.apb_comm_get_unique_id.argtypes = [ctypes.c_char_p]
     lib.apb_comm_init.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
@@ -96,7 +97,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
-              "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size"):
+              "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size",
+              "apb_exchange_passing_cyclic"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -303,10 +305,12 @@ class Comm:
             self._h = ctypes.c_void_p()
 
 
-def exchange_passing(comm: Comm | None, dims: Dims, gathered, stream=None) -> None:
+def exchange_passing(comm: Comm | None, dims: Dims, gathered, stream=None, cyclic: bool = False) -> None:
+    """cyclic: rank r owns hosts r, r+N, ... (apb_exchange_passing_cyclic), else contiguous blocks."""
     d = dims.c()
-    _check(load().apb_exchange_passing(comm.handle if comm is not None else None, ctypes.byref(d),
-                                       gathered.data_ptr(), _stream(stream)), "apb_exchange_passing")
+    fn = "apb_exchange_passing_cyclic" if cyclic else "apb_exchange_passing"
+    _check(getattr(load(), fn)(comm.handle if comm is not None else None, ctypes.byref(d),
+                               gathered.data_ptr(), _stream(stream)), fn)
 
 
 def launch_count() -> int:

@@ -509,6 +509,28 @@ extern "C" apb_status apb_exchange_passing(apb_comm* c, const apb_dims* d, void*
   return APB_OK;
 }
 
+extern "C" apb_status apb_exchange_passing_cyclic(apb_comm* c, const apb_dims* d, void* gathered,
+                                                  apb_stream_t stream) {
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (!c || c->nranks == 1) return APB_OK;
+  const int64_t lpp = lpp_of(d);
+  if (lpp == 0) return APB_OK;
+  if (!gathered || !aligned16(gathered)) return fail(APB_ERR_CONTRACT, "gathered NULL or misaligned");
+  if (d->H % c->nranks) return fail(APB_ERR_CONFIG, "comm nranks must divide H");
+  NcclApi* api = nccl();
+  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+  const size_t slot = (size_t)2 * d->n_kv_heads * lpp * d->head_dim;  // bf16 elements per host slot
+  char* base = static_cast<char*>(gathered);
+  for (int k = 0; k < d->H / c->nranks; ++k) {  // round k: hosts k*N .. k*N+N-1, one per rank
+    char* round = base + (size_t)k * c->nranks * slot * 2;
+    ncclResult_t r = api->allGather(round + (size_t)c->rank * slot * 2, round, slot, ncclBfloat16, c->comm,
+                                    reinterpret_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather (cyclic round)");
+  }
+  return APB_OK;
+}
+
 // ---------------------------------------------------------------- decode step (NEXT #1)
 static apb_status check_decode_dims(const apb_decode_dims* d) {
   if (!d) return fail(APB_ERR_CONTRACT, "dims is NULL");

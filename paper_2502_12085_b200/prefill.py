@@ -12,8 +12,9 @@ Alg. apb_prefill per layer, for every host h this rank owns:
 With a single rank (all hosts on this GPU) the exchange is just the slot layout, so each host
 runs one APB_PHASE_ALL launch as soon as the side stream has compressed hosts < h.
 
-With H hosts over N ranks, rank r owns hosts [r*H/N, (r+1)*H/N) (N = H is the paper's
-deployment, one host per GPU; N < H emulates several hosts per GPU).  Everything numeric runs
+With H hosts over N ranks (N = H is the paper's deployment, one host per GPU; N < H emulates
+several hosts per GPU) rank r owns either the contiguous block [r*H/N, (r+1)*H/N) or, work-balanced,
+the cyclic set r, r+N, r+2N, ... (hosts_of_rank); the exchange follows the ownership.  Everything numeric runs
 in libapb; this module only allocates buffers and orders launches.
 """
 from __future__ import annotations
@@ -56,6 +57,10 @@ class PrefillRank:
         self.device = torch.device(device)
         self.skip_unused_last = skip_unused_last
         self.split_phases = (comm is not None and comm.nranks > 1) if split_phases is None else split_phases
+        nr = comm.nranks if comm is not None else 1
+        self.cyclic = nr > 1 and nr < base.H and self.hosts == list(range(self.hosts[0], base.H, nr))
+        if nr > 1 and not self.cyclic and self.hosts != list(range(self.hosts[0], self.hosts[0] + len(self.hosts))):
+            raise ValueError("owned hosts must be a contiguous block or the cyclic set r, r+N, ...")
         b = base
         lpp, hk, hq, d = b.l_pp, b.n_kv_heads, b.n_heads, b.head_dim
         self.gathered = torch.zeros((b.H, 2, hk, lpp, d), dtype=torch.bfloat16, device=self.device)
@@ -96,8 +101,8 @@ class PrefillRank:
                 self._compress_host(h, io, weights, layer_idx, stream)
 
     def exchange(self, stream=None) -> None:
-        """Step 3: one in-place AllGather of the packed [2][hk][l_p'][d] slots."""
-        apb.exchange_passing(self.comm, self.base, self.gathered, stream=stream)
+        """Step 3: in-place AllGather(s) of the packed [2][hk][l_p'][d] slots."""
+        apb.exchange_passing(self.comm, self.base, self.gathered, stream=stream, cyclic=self.cyclic)
 
     def attention(self, io: dict[int, HostIO], phase: int, stream=None) -> None:
         for h in self.hosts:
@@ -157,8 +162,16 @@ class PrefillRank:
         main.wait_stream(self.side)
 
 
-def hosts_of_rank(H: int, world: int, rank: int) -> list[int]:
+def hosts_of_rank(H: int, world: int, rank: int, layout: str = "block") -> list[int]:
+    """Hosts rank `rank` of `world` owns: "block" = [rank*H/world, (rank+1)*H/world); "cyclic" =
+    rank, rank+world, ... — balances the per-rank attention work, which grows with the host index
+    (host h attends to h*l_p' passing keys), e.g. L8-128K, N = 2: 22.5 vs 25.8 TFLOP per layer on
+    the busiest rank; N = 4: 12.4 vs 14.0."""
     if H % world:
         raise ValueError(f"world size {world} must divide H={H}")
+    if layout == "cyclic":
+        return list(range(rank, H, world))
+    if layout != "block":
+        raise ValueError(f"layout must be 'block' or 'cyclic', not {layout!r}")
     per = H // world
     return list(range(rank * per, (rank + 1) * per))

@@ -21,8 +21,29 @@ def test_hosts_of_rank():
     assert hosts_of_rank(8, 1, 0) == list(range(8))
     assert hosts_of_rank(8, 2, 1) == [4, 5, 6, 7]
     assert hosts_of_rank(8, 8, 3) == [3]
+    assert hosts_of_rank(8, 2, 1, "cyclic") == [1, 3, 5, 7]
+    assert hosts_of_rank(8, 4, 2, "cyclic") == [2, 6]
+    assert hosts_of_rank(8, 8, 3, "cyclic") == [3]
+    assert hosts_of_rank(8, 1, 0, "cyclic") == list(range(8))
     with pytest.raises(ValueError):
         hosts_of_rank(8, 3, 0)
+    with pytest.raises(ValueError):
+        hosts_of_rank(8, 2, 0, "snake")
+
+
+def test_cyclic_layout_balances_work():
+    """The per-rank attention work (mask-counted FLOPs, Appendix A) of the busiest rank is lower
+    with cyclic ownership than with contiguous blocks, and every host is owned exactly once."""
+    from paper_2502_12085_b200 import workload
+    c = synth.CONFIGS["llama8b-128k"]
+    f = [workload.attention_flops(c.n, c.H, h, c.l_a, c.l_p, c.hq, c.d, c.l_q) for h in range(c.H)]
+    for world in (2, 4):
+        for layout in ("block", "cyclic"):
+            owned = sorted(h for r in range(world) for h in hosts_of_rank(c.H, world, r, layout))
+            assert owned == list(range(c.H))
+        busiest = {lay: max(sum(f[h] for h in hosts_of_rank(c.H, world, r, lay)) for r in range(world))
+                   for lay in ("block", "cyclic")}
+        assert busiest["cyclic"] < 0.9 * busiest["block"], (world, busiest)
 
 
 def _free_port():
@@ -37,7 +58,7 @@ def _cfg():
     return synth.CONFIGS["toy"].replace(n=512, H=4, l_a=32, l_p=16, d_hidden=32)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, layout="block"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = _cfg()
@@ -47,7 +68,7 @@ def _worker(rank, world, port, q):
     ids = [None] * world
     dist.all_gather_object(ids, uid[0])
     w = synth.retain_weights(cfg, 0)
-    mine = hosts_of_rank(cfg.H, world, rank)
+    mine = hosts_of_rank(cfg.H, world, rank, layout)
     hosts = {h: synth.host_qkv(cfg, 0, h) for h in mine}
     # steps 1-2 for owned hosts, written into their own slots of a full-size buffer
     gathered = np.zeros((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d), np.uint16)
@@ -55,11 +76,20 @@ def _worker(rank, world, port, q):
         x = hosts[h]
         s = oracle.retain_score(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
         gathered[h] = oracle.compact(x["k"], x["v"], x["L_A"], oracle.select_all_heads(s, cfg.l_p))
-    # step 3: in-place all-gather of contiguous per-rank slot ranges (apb_exchange_passing layout)
-    flat = torch.from_numpy(gathered.view(np.int32)).reshape(world, -1)  # bf16 pairs as int32 (gloo)
-    parts = [torch.empty_like(flat[0]) for _ in range(world)]
-    dist.all_gather(parts, flat[rank].clone())
-    gathered = torch.stack(parts).numpy().view(np.uint16).reshape(gathered.shape)
+    # step 3: in-place all-gather of contiguous per-rank slot ranges (apb_exchange_passing layout),
+    # or, cyclic, one all-gather per round k of slots [k*N, (k+1)*N) (apb_exchange_passing_cyclic)
+    if layout == "block":
+        flat = torch.from_numpy(gathered.view(np.int32)).reshape(world, -1)  # bf16 pairs as int32 (gloo)
+        parts = [torch.empty_like(flat[0]) for _ in range(world)]
+        dist.all_gather(parts, flat[rank].clone())
+        gathered = torch.stack(parts).numpy().view(np.uint16).reshape(gathered.shape)
+    else:
+        slots = torch.from_numpy(gathered.view(np.int32)).reshape(cfg.H, -1)
+        for k in range(cfg.H // world):
+            parts = [torch.empty_like(slots[0]) for _ in range(world)]
+            dist.all_gather(parts, slots[k * world + rank].clone())
+            slots[k * world: (k + 1) * world] = torch.stack(parts)
+        gathered = slots.numpy().view(np.uint16).reshape(gathered.shape)
     # step 4
     outs = {}
     for h in mine:
@@ -71,13 +101,14 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_layer_matches_single_process():
+@pytest.mark.parametrize("layout", ["block", "cyclic"])
+def test_two_rank_layer_matches_single_process(layout):
     cfg = _cfg()
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, layout)) for r in range(world)]
     for p in procs:
         p.start()
     res = []
