@@ -90,7 +90,7 @@ def main(args=None):
     layers = args.layers or cfg.layers
     base = apb.Dims(n=cfg.n, H=H, host=0, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
                     head_dim=cfg.d, l_q=cfg.l_q)
-    hosts = hosts_of_rank(H, world, rank)
+    hosts = hosts_of_rank(H, world, rank, args.host_layout)
     comm = None
     if world > 1:
         uid = [apb.Comm.unique_id() if rank == 0 else None]
@@ -234,6 +234,8 @@ def main(args=None):
                                        f"n={cfg.n}, H={H} hosts over {world} GPU(s), l_a={cfg.l_a}, "
                                        f"l_p={cfg.l_p}, {layers} layers",
                            "n": cfg.n, "H": H, "layers": layers, "parallelism": f"apb-sp{H}/{world}gpu",
+                           "host_layout": ("all hosts on one GPU" if world == 1 else
+                                           args.host_layout if world < H else "one host per GPU"),
                            "l2": "residual stream 1.3 GB and 14 GB of per-layer weights, far larger than L2"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
