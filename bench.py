@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--hosts", type=int, default=None, help="override H (default: the paper's 8)")
     ap.add_argument("--host-layout", choices=["cyclic", "block"], default="cyclic",
                     help="host ownership when N < H ranks: cyclic r, r+N, ... (work-balanced) or contiguous blocks")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
@@ -376,7 +376,8 @@ def main():
 
 def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank, barrier):
     """Same hot path, inputs streamed from pinned host memory every layer (prefetched on a copy
-    stream one layer ahead) and the last layer's outputs read back to the host."""
+    stream one layer ahead, continuing across steps) and every step's last-layer outputs read back
+    to the host on their own stream."""
     import torch.distributed as dist
     pinned = {}
     for h in hosts:
@@ -386,11 +387,18 @@ def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank,
     h2d_layer = sum(t.numel() * t.element_size() for h in hosts for t in pinned[h])
     d2h = sum(t.numel() * t.element_size() for t in out_host.values())
     copy = torch.cuda.Stream(device=dev)
+    d2h_stream = torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     done = [torch.cuda.Event(), torch.cuda.Event()]
-    for e in done:
+    read = [torch.cuda.Event(), torch.cuda.Event()]
+    for e in done + read:
         e.record(main)
+    # own output buffers per buffer set, so a step's D2H (on its own stream) overlaps the next
+    # step's first layers instead of serialising with them
+    from paper_2502_12085_b200.prefill import HostIO
+    sets = [{h: HostIO(q=x.q, k=x.k, v=x.v, out=torch.empty_like(x.out), lse=x.lse) for h, x in st.items()}
+            for st in sets]
 
     def upload(s):
         copy.wait_event(done[s])
@@ -400,24 +408,32 @@ def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank,
                     dst.copy_(src, non_blocking=True)
         copied[s].record(copy)
 
-    def step():
+    def run(n_steps):
+        # layers of consecutive steps form one stream of uploads: layer l+1's inputs (the next
+        # step's layer 0 after the last layer) are copied while layer l computes
+        total = n_steps * layers
         upload(0)
-        for l in range(layers):
-            s = l % 2
-            if l + 1 < layers:
-                upload((l + 1) % 2)
+        for g in range(total):
+            l, s = g % layers, g % 2
+            if g + 1 < total:
+                upload((g + 1) % 2)
             main.wait_event(copied[s])
+            main.wait_event(read[s])  # set s's outputs of an earlier step are on the host
             pr.layer(sets[s], weights[l], overlap=not args.no_overlap, layer_idx=l)
             done[s].record(main)
-        for h in hosts:
-            out_host[h].copy_(sets[(layers - 1) % 2][h].out, non_blocking=True)
+            if l == layers - 1:  # this step's result back to the host, off the compute stream
+                d2h_stream.wait_event(done[s])
+                with torch.cuda.stream(d2h_stream):
+                    for h in hosts:
+                        out_host[h].copy_(sets[s][h].out, non_blocking=True)
+                read[s].record(d2h_stream)
 
-    step()
+    run(1)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(main)
-    for _ in range(args.e2e_steps):
-        step()
+    run(args.e2e_steps)
+    main.wait_stream(d2h_stream)  # the last step's result is on the host inside the timed region
     ev1.record(main)
     barrier()
     ms = ev0.elapsed_time(ev1)
@@ -427,8 +443,9 @@ def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank,
         ms = t.item()
     return {"value": cfg.n * args.e2e_steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_layer * layers,
             "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-            "how": "pinned host Q/K/V -> H2D every layer on a copy stream (one layer ahead) -> libapb hot path -> "
-                   "D2H of the last layer's attention output, all inside the timed region (per-rank volumes)"}
+            "how": "pinned host Q/K/V -> H2D every layer on a copy stream (one layer ahead, continuing across "
+                   "steps) -> libapb hot path -> D2H of every step's last-layer attention output, all inside the "
+                   "timed region (per-rank volumes)"}
 
 
 if __name__ == "__main__":
