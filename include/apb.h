@@ -257,6 +257,16 @@ apb_status apb_decode_attention_hosts(const apb_decode_dims* dims, int32_t n_hos
                                       apb_stream_t stream);
 apb_status apb_decode_hosts_workspace_size(const apb_decode_dims* dims, int32_t n_hosts, const int64_t* cache_lens,
                                            size_t* bytes);
+/* The whole decode step when ONE rank holds every host (N = 1; dims->host == 0, H <= 16 caches,
+ * host arrays as above): the partial streaming launch of apb_decode_attention_hosts followed by
+ * MergeScore directly over every host's splits — no per-host partials, no Gather (the
+ * log-sum-exp merge is associative, so the grouping does not change the result beyond fp32
+ * summation order).  out bf16 [t_new][n_heads][head_dim]; out_lse fp32 [t_new][n_heads] (natural
+ * log) or NULL.  ws: apb_decode_hosts_workspace_size(dims, H, cache_lens) bytes.               */
+apb_status apb_decode_step_hosts(const apb_decode_dims* dims, const int64_t* cache_lens, const void* const* k_caches,
+                                 const void* const* v_caches, int64_t cache_row_stride, const void* q,
+                                 const void* k_new, const void* v_new, int64_t new_row_stride, void* out,
+                                 float* out_lse, void* ws, size_t ws_bytes, apb_stream_t stream);
 
 /* MergeScore: out[r] = sum_h parts_o[h][r] * exp(parts_lse[h][r] - L[r]),
  * L[r] = log sum_h exp(parts_lse[h][r]).  parts_o fp32 with part stride part_stride_o floats

@@ -29,7 +29,8 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
             "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count",
             "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
-            "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic")
+            "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic",
+            "apb_decode_step_hosts")
 
 
 class ApbError(RuntimeError):
@@ -86,6 +87,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_decode_workspace_size.argtypes = [ddp, ctypes.POINTER(sz)]
     lib.apb_decode_attention_hosts.argtypes = [ddp, i32, vp, vp, vp, i64, vp, vp, vp, i64, vp, i64, i64, vp, sz, vp]
     lib.apb_decode_hosts_workspace_size.argtypes = [ddp, i32, vp, ctypes.POINTER(sz)]
+    lib.apb_decode_step_hosts.argtypes = [ddp, vp, vp, vp, i64, vp, vp, vp, i64, vp, vp, vp, sz, vp]
     lib.apb_merge_partials.argtypes = [i32, i64, i32, vp, i64, vp, i64, vp, vp, vp]
     lib.apb_exchange_partials.argtypes = [vp, i64, vp, vp]
     lib.apb_random_scores.argtypes = [dp, ctypes.c_uint64, i32, vp, vp]
@@ -98,7 +100,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size",
-              "apb_exchange_passing_cyclic"):
+              "apb_exchange_passing_cyclic", "apb_decode_step_hosts"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -393,6 +395,25 @@ def decode_attention_hosts(dims: DecodeDims, q, k_caches: list, v_caches: list, 
                                              _ptr(v_new), ns, parts.data_ptr(), parts.stride(0), lse_offset,
                                              _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                                              _stream(stream)), "apb_decode_attention_hosts")
+
+
+def decode_step_hosts(dims: DecodeDims, q, k_caches: list, v_caches: list, k_new, v_new, out, out_lse=None,
+                      ws=None, stream=None) -> None:
+    """The whole decode step with every host on this rank (dims.host == 0, len(k_caches) == H):
+    one streaming launch + MergeScore straight into bf16 out [t][hq][d] (and lse [t][hq])."""
+    lens = [k.shape[0] for k in k_caches]
+    nz = [k for k in k_caches if k.numel()]
+    cs = _rowstride(nz[0], "k_cache") if nz else 0
+    for t in list(k_caches) + list(v_caches):
+        if t.numel() and _rowstride(t, "cache") != cs:
+            raise ValueError("all caches of one call must share a row stride")
+    ns = _rowstride(k_new, "k_new") if k_new is not None else 0
+    _, lp, kp, vp = _host_arrays(lens, k_caches, v_caches)
+    d = dims.c()
+    _check(load().apb_decode_step_hosts(ctypes.byref(d), lp, kp, vp, cs, q.data_ptr(), _ptr(k_new), _ptr(v_new), ns,
+                                        out.data_ptr(), _ptr(out_lse), _ptr(ws),
+                                        0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+           "apb_decode_step_hosts")
 
 
 def merge_partials(n_parts: int, rows: int, head_dim: int, parts_o, stride_o: int, parts_lse, stride_lse: int,

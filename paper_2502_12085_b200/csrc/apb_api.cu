@@ -623,12 +623,12 @@ extern "C" apb_status apb_decode_hosts_workspace_size(const apb_decode_dims* d, 
   return APB_OK;
 }
 
-extern "C" apb_status apb_decode_attention_hosts(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens,
+static apb_status decode_hosts_impl(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens,
                                                  const void* const* k_caches, const void* const* v_caches,
                                                  int64_t cache_row_stride, const void* q, const void* k_new,
                                                  const void* v_new, int64_t new_row_stride, float* parts,
-                                                 int64_t part_stride, int64_t lse_offset, void* ws, size_t ws_bytes,
-                                                 apb_stream_t stream) {
+                                                 int64_t part_stride, int64_t lse_offset, void* merged_out,
+                                                 float* merged_lse, void* ws, size_t ws_bytes, apb_stream_t stream) {
   apb_status st = check_decode_hosts(d, n, cache_lens);
   if (st) return st;
   const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
@@ -652,9 +652,13 @@ extern "C" apb_status apb_decode_attention_hosts(const apb_decode_dims* d, int32
     if ((st = check_rows(v_new, new_row_stride, (int64_t)hk * D, "v_new"))) return st;
   }
   const int64_t rows = (int64_t)d->t_new * hq;
-  if (!parts || !aligned16(parts)) return fail(APB_ERR_CONTRACT, "parts NULL or misaligned");
-  if (part_stride < rows * D + rows || lse_offset < rows * D || lse_offset + rows > part_stride)
-    return fail(APB_ERR_CONTRACT, "part_stride / lse_offset do not hold O [rows][head_dim] and lse [rows]");
+  if (merged_out) {
+    if (!aligned16(merged_out)) return fail(APB_ERR_CONTRACT, "out misaligned");
+  } else {
+    if (!parts || !aligned16(parts)) return fail(APB_ERR_CONTRACT, "parts NULL or misaligned");
+    if (part_stride < rows * D + rows || lse_offset < rows * D || lse_offset + rows > part_stride)
+      return fail(APB_ERR_CONTRACT, "part_stride / lse_offset do not hold O [rows][head_dim] and lse [rows]");
+  }
   int64_t keys[kDecMaxHosts];
   decode_hosts_keys(d, n, cache_lens, keys);
   const size_t need = decode_hosts_workspace_bytes(n, keys, d->t_new, hq, hk, D);
@@ -674,7 +678,30 @@ extern "C" apb_status apb_decode_attention_hosts(const apb_decode_dims* d, int32
   p.k_new = static_cast<const __nv_bfloat16*>(k_new);
   p.v_new = static_cast<const __nv_bfloat16*>(v_new);
   p.ws_o = static_cast<float*>(ws);
-  return launch_decode_hosts(p, hb, keys, parts, part_stride, lse_offset, reinterpret_cast<cudaStream_t>(stream));
+  return launch_decode_hosts(p, hb, keys, parts, part_stride, lse_offset, merged_out, merged_lse,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_decode_attention_hosts(const apb_decode_dims* d, int32_t n, const int64_t* cache_lens,
+                                                 const void* const* k_caches, const void* const* v_caches,
+                                                 int64_t cache_row_stride, const void* q, const void* k_new,
+                                                 const void* v_new, int64_t new_row_stride, float* parts,
+                                                 int64_t part_stride, int64_t lse_offset, void* ws, size_t ws_bytes,
+                                                 apb_stream_t stream) {
+  return decode_hosts_impl(d, n, cache_lens, k_caches, v_caches, cache_row_stride, q, k_new, v_new, new_row_stride,
+                           parts, part_stride, lse_offset, nullptr, nullptr, ws, ws_bytes, stream);
+}
+
+extern "C" apb_status apb_decode_step_hosts(const apb_decode_dims* d, const int64_t* cache_lens,
+                                            const void* const* k_caches, const void* const* v_caches,
+                                            int64_t cache_row_stride, const void* q, const void* k_new,
+                                            const void* v_new, int64_t new_row_stride, void* out, float* out_lse,
+                                            void* ws, size_t ws_bytes, apb_stream_t stream) {
+  if (d && (d->host != 0 || d->H > kDecMaxHosts))
+    return fail(APB_ERR_CONFIG, "apb_decode_step_hosts needs every host: host == 0 and H <= 16");
+  if (!out) return fail(APB_ERR_CONTRACT, "out is NULL");
+  return decode_hosts_impl(d, d ? d->H : 0, cache_lens, k_caches, v_caches, cache_row_stride, q, k_new, v_new,
+                           new_row_stride, nullptr, 0, 0, out, out_lse, ws, ws_bytes, stream);
 }
 
 extern "C" apb_status apb_merge_partials(int32_t n_parts, int64_t rows, int32_t head_dim, const float* parts_o,

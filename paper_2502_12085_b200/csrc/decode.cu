@@ -503,7 +503,8 @@ apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse,
 }
 
 apb_status launch_decode_hosts(const DecodeParams& p0, DecodeHosts hb, const int64_t* n_keys, float* parts,
-                               int64_t part_stride, int64_t lse_offset, cudaStream_t stream) {
+                               int64_t part_stride, int64_t lse_offset, void* merged_out, float* merged_lse,
+                               cudaStream_t stream) {
   DecodeParams p = p0;
   int cps;
   const int64_t splits = decode_hosts_plan(hb.n, n_keys, p.hk, hb.split_begin, &cps);
@@ -513,6 +514,9 @@ apb_status launch_decode_hosts(const DecodeParams& p0, DecodeHosts hb, const int
   if (splits > 0)
     if (apb_status st = launch_partials(p, hb, splits, cps, stream)) return st;
   if (rows == 0) return APB_OK;
+  if (merged_out)  // every host is here: MergeScore directly over all hosts' splits (log2 lse), bf16 out
+    return launch_merge((int)splits, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, merged_out, true, merged_lse,
+                        stream);
   const dim3 grid((unsigned)rows, (unsigned)hb.n);
   size_t smem = 0;
   for (int i = 0; i < hb.n; ++i) {

@@ -103,9 +103,11 @@ size_t decode_workspace_bytes(int64_t n_keys, int t, int hq, int hk, int D);
 size_t decode_hosts_workspace_bytes(int n, const int64_t* n_keys, int t, int hq, int hk, int D);
 apb_status launch_decode(const DecodeParams& p, float* part_o, float* part_lse, cudaStream_t stream);
 // p: common fields (q, k_new/v_new, strides, scale, ws); n hosts with keys n_keys[i] (cache plus
-// the new tokens for hb.new_host); host i's partial -> parts + i*part_stride (O), + lse_offset (lse)
+// the new tokens for hb.new_host); host i's partial -> parts + i*part_stride (O), + lse_offset (lse);
+// or, with merged_out != NULL (all hosts present), the merged bf16 output and natural lse directly
 apb_status launch_decode_hosts(const DecodeParams& p, DecodeHosts hb, const int64_t* n_keys, float* parts,
-                               int64_t part_stride, int64_t lse_offset, cudaStream_t stream);
+                               int64_t part_stride, int64_t lse_offset, void* merged_out, float* merged_lse,
+                               cudaStream_t stream);
 apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,
                         int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,
                         cudaStream_t stream);

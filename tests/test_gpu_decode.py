@@ -115,9 +115,9 @@ def test_merge_partials_parity():
     assert np.isneginf(ol.cpu().numpy()[7])
 
 
-@pytest.mark.parametrize("batch", [True, False])
+@pytest.mark.parametrize("mode", ["fused", "hosts", "per-host"])
 @pytest.mark.parametrize("name,t", [("toy", 1), ("toy", 3), ("gqa3", 2)])
-def test_decode_step_end_to_end(name, t, batch):
+def test_decode_step_end_to_end(name, t, mode):
     """All hosts on one GPU through DecodeRank: partials -> (in-place) gather -> MergeScore, vs the
     oracle's decode step AND vs exact attention over [B_1 .. B_H | new] (the step is exact)."""
     from paper_2502_12085_b200.decode import DecodeRank
@@ -128,7 +128,8 @@ def test_decode_step_end_to_end(name, t, batch):
     caches = [(x["k"][x["L_A"]:], x["v"][x["L_A"]:]) for x in hosts]  # block KV cache
     q = _bits((t, cfg.hq, cfg.d), rng)
     kn, vn = _bits((t, cfg.hk, cfg.d), rng), _bits((t, cfg.hk, cfg.d), rng)
-    dr = DecodeRank(cfg.H, list(range(cfg.H)), t, cfg.hq, cfg.hk, cfg.d, batch_hosts=batch)
+    dr = DecodeRank(cfg.H, list(range(cfg.H)), t, cfg.hq, cfg.hk, cfg.d, batch_hosts=mode != "per-host",
+                    fuse_merge=mode == "fused")
     out = torch.empty((t, cfg.hq, cfg.d), dtype=torch.bfloat16, device="cuda")
     ol = torch.empty((t, cfg.hq), device="cuda")
     dr.step(dev(q), {h: (dev(kc), dev(vc)) for h, (kc, vc) in enumerate(caches)}, dev(kn), dev(vn), out, ol)
