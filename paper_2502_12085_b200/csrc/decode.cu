@@ -350,7 +350,24 @@ __device__ __forceinline__ void merge_row(int64_t row, int n, const float* __res
   float acc[kPer];
 #pragma unroll
   for (int e = 0; e < kPer; ++e) acc[e] = 0.f;
-  for (int h = warp; h < n; h += kMergeWarps) {
+  int h = warp;
+  // four parts' loads in flight per warp, accumulated in the same (part-ascending) order
+  for (; h + 3 * kMergeWarps < n; h += 4 * kMergeWarps) {
+    float v[4][kPer];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float* src = parts_o + (h + u * kMergeWarps) * stride_o + row * D;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) v[u][e] = __ldg(src + e * 32 + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float w = wsm[h + u * kMergeWarps];
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) acc[e] = fmaf(w, v[u][e], acc[e]);
+    }
+  }
+  for (; h < n; h += kMergeWarps) {
     const float w = wsm[h];
     const float* src = parts_o + h * stride_o + row * D;
 #pragma unroll

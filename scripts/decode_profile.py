@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--hk", type=int, default=None, help="override KV heads")
     ap.add_argument("--lb", type=int, default=None, help="override cache rows per host")
     ap.add_argument("--per-host", action="store_true", help="one apb_decode_attention per host (no batched launch)")
-    ap.add_argument("--fuse", action="store_true", help="apb_decode_step_hosts (MergeScore over all hosts' splits)")
+    ap.add_argument("--no-fuse", action="store_true", help="batched partials + MergeScore (not apb_decode_step_hosts)")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
     over = {k: v for k, v in (("hq", a.hq), ("hk", a.hk)) if v is not None}
@@ -41,7 +41,7 @@ def main():
     kn = torch.randn((a.t, cfg.hk, cfg.d), device=dev).bfloat16()
     vn = torch.randn((a.t, cfg.hk, cfg.d), device=dev).bfloat16()
     dr = DecodeRank(cfg.H, list(range(cfg.H)), a.t, cfg.hq, cfg.hk, cfg.d, batch_hosts=not a.per_host,
-                    fuse_merge=a.fuse)
+                    fuse_merge=not a.no_fuse)
     out = torch.empty((a.t, cfg.hq, cfg.d), dtype=torch.bfloat16, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2: cold caches each iteration
     times = []
@@ -59,8 +59,8 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     gbs = cache_bytes / (ms / 1e3) / 1e9
-    print(json.dumps({"config": a.config, "launch": "per-host" if a.per_host else ("fused step (apb_decode_step_hosts)" if a.fuse
-                                                                    else "batched partials (apb_decode_attention_hosts)"), "hq": cfg.hq, "hk": cfg.hk, "t_new": a.t, "hosts": cfg.H, "cache_rows_per_host": cfg.l_b,
+    print(json.dumps({"config": a.config, "launch": "per-host" if a.per_host else ("batched partials (apb_decode_attention_hosts)" if a.no_fuse
+                                                                    else "fused step (apb_decode_step_hosts)"), "hq": cfg.hq, "hk": cfg.hk, "t_new": a.t, "hosts": cfg.H, "cache_rows_per_host": cfg.l_b,
                       "ms_per_layer_step": round(ms, 4), "cache_bytes": cache_bytes, "achieved_gbs": round(gbs, 1),
                       "hbm_peak_gbs": peaks["hbm_gbs"], "frac": round(gbs / peaks["hbm_gbs"], 3)}))
 
