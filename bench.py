@@ -327,6 +327,8 @@ def main():
     flops_rank = sum(workload.attention_flops(cfg.n, H, h, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q) for h in hosts)
     flops_all = sum(workload.attention_flops(cfg.n, H, h, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q) for h in range(H))
     crit = workload.attention_flops(cfg.n, H, H - 1, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q)
+    executed_rank = sum(workload.attention_executed_flops(cfg.n, H, h, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q)
+                        for h in hosts)
     peaks, peak_src = load_peaks()
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     achieved = flops_rank * layers * args.steps / (attn_ms / 1e3) / 1e12
@@ -340,6 +342,8 @@ def main():
                                                            else "one ordered PHASE_ALL launch per host") + ")",
                 "peak_source": f"bf16_tflops_sustained, {peak_src}",
                 "flops_per_step": flops_rank * layers,
+                "executed_mma_flops_per_step": executed_rank * layers,
+                "tile_efficiency": round(flops_rank / executed_rank, 4),
                 "attn_ms_per_step": round(attn_ms / args.steps, 3)}
 
     # ---- end to end through the public API: pinned host inputs -> H2D every layer -> ... -> D2H

@@ -22,6 +22,21 @@ def attention_flops(n: int, H: int, host: int, l_a: int, l_p: int, hq: int, d: i
     return 4 * d * hq * visible_pairs(host_L_A(host, l_q, l_a), host * lpp, l_b)
 
 
+def attention_executed_flops(n: int, H: int, host: int, l_a: int, l_p: int, hq: int, d: int, l_q: int = 0,
+                             tile: int = 128) -> int:
+    """MMA FLOPs the attention kernel executes: whole tile x tile (query x key) tiles, every tile
+    a row tile reaches (anchor rows: anchor key tiles up to the diagonal; local rows: all anchor
+    tiles, every passing slot's tiles, local tiles up to the diagonal).  useful / executed is the
+    tile efficiency."""
+    l_b = n // H
+    lpp = min(l_p, l_b)
+    L_A = host_L_A(host, l_q, l_a)
+    cdiv = lambda a: (a + tile - 1) // tile  # noqa: E731
+    nA, nB, nP = cdiv(L_A), cdiv(l_b), cdiv(lpp)
+    visits = nA * (nA + 1) // 2 + nB * (nA + host * nP) + nB * (nB + 1) // 2
+    return 4 * d * hq * tile * tile * visits
+
+
 def attention_flops_split(n, H, host, l_a, l_p, hq, d, l_q=0):
     """(LOCAL-phase FLOPs, PASSING-phase FLOPs) of one host's layer."""
     l_b = n // H
