@@ -200,13 +200,22 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+MODEL_SHAPES = {"llama8b-128k": "Llama-3.1-8B", "llama8b-32k": "Llama-3.1-8B", "qwen14b-128k": "Qwen-2.5-14B",
+                "yi34b-200k": "Yi-34B-200K", "llama8b-512k": "Llama-3-8B-1M", "llama8b-1m": "Llama-3-8B-1M"}
+
+
 def workload_config(cfg, H, layers, n_gpus, variant=""):
-    return {"workload": f"{cfg.name}{variant}: APB prefill hot path, Llama-3.1-8B-shaped layer stack "
+    shape = MODEL_SHAPES.get(cfg.name, cfg.name)
+    l_b = cfg.n // H
+    rows = sum(l_b + (0 if h == 0 else cfg.l_q + cfg.l_a) for h in range(H))
+    qkv_gib = rows * (cfg.hq + 2 * cfg.hk) * cfg.d * 2 / 2 ** 30
+    return {"workload": f"{cfg.name}{variant}: APB prefill hot path, {shape}-shaped layer stack "
                         f"(hq={cfg.hq}, hk={cfg.hk}, d={cfg.d}), n={cfg.n}, H={H} hosts over {n_gpus} GPU(s), "
                         f"l_a={cfg.l_a}, l_p={cfg.l_p}, {layers} layers, retaining head d_R={cfg.d_hidden}",
             "n": cfg.n, "H": H, "l_a": cfg.l_a, "l_p": cfg.l_p, "layers": layers, "hq": cfg.hq, "hk": cfg.hk,
             "d": cfg.d, "parallelism": f"apb-sp{H}/{n_gpus}gpu",
-            "l2": "inputs larger than L2: ~2 GiB of Q/K/V per layer at N=1, two alternating layer buffer sets"}
+            "l2": f"inputs larger than L2: {qkv_gib:.1f} GiB of Q/K/V per layer over all hosts (126 MB L2), "
+                  "two alternating layer buffer sets"}
 
 
 # ----------------------------------------------------------------------------- GPU arm
