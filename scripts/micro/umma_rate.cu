@@ -292,6 +292,72 @@ void run(const char* name, int sms) {
   cudaFree(cyc);
 }
 
+// SS MMA with M = 64 (cta_group::1): rate per SM relative to the 8192 FLOP/clk peak
+template <int N>
+__global__ void __launch_bounds__(128, 1) umma_m64_kernel(unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
+  constexpr int kSubA = 64 * 128, kSubB = N * 128;
+  const uint32_t sA = smem_u32(smem), sB = sA + 2 * kSubA, bar = sB + 2 * kSubB;
+  __shared__ uint32_t tmem_slot;
+  for (int i = threadIdx.x; i < (2 * kSubA + 2 * kSubB) / 4; i += 128)
+    reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  constexpr uint32_t idesc = idesc_bf16_f32(64, N, false, false);
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < kIters; ++it) {
+      const uint32_t dcol = (it & 1) * 256;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t off = (k / 4) * kSubA + (k % 4) * 32, offb = (k / 4) * kSubB + (k % 4) * 32;
+        mma_ss(tmem + dcol, sdesc_sw128(sA + off, 16, 1024), sdesc_sw128(sB + offb, 16, 1024), idesc, k > 0);
+      }
+    }
+    mma_commit(bar);
+    mbar_wait(bar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int N>
+void run_m64(const char* name, int sms) {
+  auto kern = umma_m64_kernel<N>;
+  const int smem = 2 * 64 * 128 + 2 * N * 128 + 64 + 1024;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sizeof(unsigned long long) * sms);
+  kern<<<sms, 128, smem>>>(cyc);
+  kern<<<sms, 128, smem>>>(cyc);
+  if (cudaDeviceSynchronize() != cudaSuccess) { printf("%s: error\n", name); return; }
+  unsigned long long h[1024];
+  cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+  double c = 0;
+  for (int i = 0; i < sms; ++i) c += h[i];
+  c /= sms;
+  const double flop = 2.0 * 64 * N * 128 * kIters;
+  printf("%-28s %7.0f FLOP/clk/SM (%.3f of 8192)\n", name, flop / c, flop / c / 8192.0);
+  cudaFree(cyc);
+}
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -314,5 +380,7 @@ int main() {
   run_chain<3>("chain sleep, P halves", sms);
   run_chain<6>("chain + smem writes (max)", sms);
   run_chain<14>("chain + smem writes (paced)", sms);
+  run_m64<128>("cg1 SS M64 N128", sms);
+  run_m64<256>("cg1 SS M64 N256", sms);
   return 0;
 }
