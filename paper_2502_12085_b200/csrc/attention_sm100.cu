@@ -36,8 +36,14 @@ constexpr int BN = 128;
 #ifndef APB_RING
 #define APB_RING 5
 #endif
+#ifdef APB_PSMEM
+// P lives in shared memory (64 KB for the two tiles), which leaves room for 3 K/V tiles at d = 128
+template <int D>
+constexpr int ring_slots() { return D == 128 ? 3 : 6; }
+#else
 template <int D>
 constexpr int ring_slots() { return D == 128 ? APB_RING : 2 * APB_RING; }
+#endif
 constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, {TMA, MMA, 2 idle}
 constexpr int kLoadWarp = 10;  // SMSP 2 (warps 0/4 on SMSP 0 would otherwise share with it)
 constexpr int kMmaWarp = 9;
@@ -100,9 +106,16 @@ struct Layout {
   static constexpr int kRing = ring_slots<D>();
   static constexpr int kQ = 0;
   static constexpr int kR = kQ + 2 * kTile;  // the K/V ring
+#ifdef APB_PSMEM
+  static constexpr int kP = kR + kRing * kTile;    // P_t: [128 rows][128 keys] bf16, two SW128 sub-tiles
+  static constexpr int kBar = kP + 2 * 2 * kSub;
+  // barriers: Qfull, full[kRing], empty[kRing], Sfull[2], Sfree[2], Pfull[2][2 halves], PVdone[2]
+  static constexpr int kNumBars = 1 + 2 * kRing + 10;
+#else
   static constexpr int kBar = kR + kRing * kTile;
   // barriers: Qfull, full[kRing], empty[kRing], Sfull[2], Pfull[2][2 halves], Odone[2]
   static constexpr int kNumBars = 1 + 2 * kRing + 8;
+#endif
   static constexpr int kTmemPtr = kBar + kNumBars * 8;
   static constexpr int kUsed = kTmemPtr + 16;
   // keep one CTA per SM (each CTA allocates all 512 TMEM columns)
@@ -219,6 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bS = [&](int t) { return bar0 + 8u * (1 + 2 * NR + t); };
   auto bP = [&](int t, int half) { return bar0 + 8u * (3 + 2 * NR + 2 * t + half); };
   auto bO = [&](int t) { return bar0 + 8u * (7 + 2 * NR + t); };
+#ifdef APB_PSMEM
+  // bO(t) doubles as PVdone(t) (one commit per PV_t(i)); Sfree(t): the softmax has S_t in registers
+  auto bSf = [&](int t) { return bar0 + 8u * (9 + 2 * NR + t); };
+  auto sP = [&](int t) { return sbase + L::kP + t * 2 * L::kSub; };
+#endif
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtr);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
@@ -236,6 +254,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bP(t, 0), BM);
       mbar_init(bP(t, 1), BM);
       mbar_init(bO(t), 1);
+#ifdef APB_PSMEM
+      mbar_init(bSf(t), BM);
+#endif
     }
     fence_mbar_init();
   }
@@ -281,12 +302,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       }
       __syncwarp();
+#ifdef APB_PSMEM
+      // loads in the MMA warp's consumption order: K(0), then per step i: K(i+1), V(i)
+      for (int n = 0; n < 2 * it.nkv; ++n) {
+        int kv, i;
+        if (n == 0) { kv = 0; i = 0; }
+        else if (n - 1 == 2 * (it.nkv - 1)) { kv = 1; i = it.nkv - 1; }
+        else if (((n - 1) & 1) == 0) { kv = 0; i = (n - 1) / 2 + 1; }
+        else { kv = 1; i = (n - 2) / 2; }
+        const KvTile kt = kv_tile(p, it, i);
+        const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
+        {
+          const int r = n % NR;
+#else
       for (int i = 0; i < it.nkv; ++i) {
         const KvTile kt = kv_tile(p, it, i);
         const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
 #pragma unroll
         for (int kv = 0; kv < 2; ++kv) {
           const int n = 2 * i + kv, r = n % NR;
+#endif
           mbar_wait_sleep(bRe(r), ((n / NR) & 1) ^ 1);
           if (elect_one()) {
             if ((p.dbg_skip & (1 << kv)) && i >= NR) {
@@ -352,6 +387,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool carry = (p.phase == APB_PHASE_PASSING);
       mbar_wait_sleep(bQ, 0);
       tc_fence_after();
+#ifdef APB_PSMEM
+      // S_t(i+1) is issued as soon as the softmax holds S_t(i) in registers (Sfree), so it runs
+      // under softmax_t(i); PV_t(i) (SS: A = P_t from shared memory) when P_t(i) is published.
+      // Ring sequence numbers follow the producer's order K(0), K(1), V(0), K(2), V(1), ...
+      auto nK = [&](int i) { return i == 0 ? 0 : 2 * i - 1; };
+      auto nV = [&](int i) { return i == it.nkv - 1 ? 2 * it.nkv - 1 : 2 * i + 2; };
+      if (it.nkv > 0) {
+        mbar_wait_sleep(bRf(0), 0);
+        tc_fence_after();
+        for (int t = 0; t < it.ntiles; ++t) issue_S(t, 0);
+        commit(bRe(0));
+      }
+      for (int i = 0; i < it.nkv; ++i) {
+        if (i + 1 < it.nkv) {
+          const int n = nK(i + 1);
+          for (int t = 0; t < it.ntiles; ++t) {
+            mbar_wait_sleep(bSf(t), i & 1);
+            if (t == 0) mbar_wait_sleep(bRf(n % NR), (n / NR) & 1);
+            tc_fence_after();
+            issue_S(t, n % NR);
+          }
+          commit(bRe(n % NR));
+        }
+        const int n = nV(i), sv = n % NR;
+        mbar_wait_sleep(bRf(sv), (n / NR) & 1);
+        tc_fence_after();
+        for (int t = 0; t < it.ntiles; ++t) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            mbar_wait_sleep(bP(t, half), i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int k = half * (BN / 32); k < (half + 1) * (BN / 32); ++k)
+                mma_ss(tmem + 256 + t * D, sdesc_sw128(sP(t) + (k / 4) * L::kSub + (k % 4) * 32, 16, 1024),
+                       sdesc_sw128(sR(sv) + k * 2048, L::kSub, 1024), idPV, (carry || i > 0 || k > 0) ? 1u : 0u);
+            }
+            __syncwarp();
+          }
+          commit(bO(t));  // PVdone(t): P_t is free and O_t stable
+        }
+        commit(bRe(sv));
+      }
+      (void)issue_PV;
+#else
       for (int i = 0; i < it.nkv; ++i) {
         trace_i = i;
         const int nK = 2 * i, nV = 2 * i + 1, nK1 = 2 * i + 2;  // ring sequence numbers
@@ -384,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+#endif
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
@@ -451,6 +532,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
         tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
         tmem_wait_ld();
+#ifdef APB_PSMEM
+        tc_fence_before();
+        mbar_arrive(bSf(t));  // S_t(i) is in registers: the MMA warp may compute S_t(i+1) now
+#endif
         float* s = reinterpret_cast<float*>(sr);
         if (tid == 0) TRACE(16 + t * 4, i);
         if (nv < BN) {
@@ -517,6 +602,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool grow = !have_m || (mx > m_run + kRescaleThreshold);
         float alpha = 1.f;
         if (tid == 0) TRACE(17 + t * 4, i);
+#ifdef APB_PSMEM
+        if (i > 0) {  // PV_t(i-1) complete: O_t may be rescaled and P_t overwritten
+          mbar_wait(bO(t), (i - 1) & 1);
+          tc_fence_after();
+        }
+#endif
         if (__any_sync(0xffffffffu, grow)) {
           if (grow) {
             const float m_new = fmaxf(m_run, mx);
@@ -543,16 +634,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
         if (tid == 0) TRACE(18 + t * 4, i);
+#ifdef APB_PSMEM
+        auto store_P = [&](int half) {  // row tid of the SW128 K-major sub-tile `half` of P_t
+          const uint32_t base = sP(t) + half * L::kSub + tid * 128;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + ((q ^ (tid & 7)) << 4)),
+                         "r"(pk[4 * q]), "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3]) : "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+        };
+        store_P(0);
+        tmem_wait_st();  // an O rescale above
+        tc_fence_before();
+        mbar_arrive(bP(t, 0));
+#else
         tmem_st32(tS, pk);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bP(t, 0));
+#endif
         if (tid == 0) TRACE(8 + 2 * t, i);
         exp_half(1, m_use, pk, acc2);
+#ifdef APB_PSMEM
+        store_P(1);
+        tc_fence_before();
+        mbar_arrive(bP(t, 1));
+#else
         tmem_st32(tS + 32, pk);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bP(t, 1));
+#endif
         if (tid == 0) TRACE(9 + 2 * t, i);
         if ((tid & 31) == 0) TRACE(24 + t * 4 + (tid >> 5), i);
 #ifdef APB_PINGPONG
@@ -569,7 +681,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (pingpong && t == 0) named_bar_sync(1, 256);  // consume tile 1's last hand-off
 #endif
       // ============================================================== epilogue
+#ifdef APB_PSMEM
+      mbar_wait(bO(t), (it.nkv - 1) & 1);  // PV_t of the last step
+#else
       mbar_wait(bO(t), 0);
+#endif
       tc_fence_after();
       const float inv_l = 1.f / l_run;
       const bool to_ws = (it.seg == 1) && p.local_to_ws;

@@ -292,6 +292,151 @@ void run(const char* name, int sms) {
   cudaFree(cyc);
 }
 
+// P-in-shared-memory pipeline (candidate attention restructure): per tile t and step i the
+// "softmax" warpgroup waits S_t(i), arrives Sfree_t (the MMA warp may overwrite S_t at once),
+// writes P_t (32 KB bf16, SW128 K-major) into shared memory with st.shared.v4, fences the async
+// proxy and arrives P_t; the MMA warp issues S_t(i+1) on Sfree_t and PV_t(i) (SS: A = P_t from
+// smem) on P_t.  MODE & 4: a concurrent 32 KB-per-round bulk-copy stream (the K/V TMA traffic).
+template <int MODE>
+__global__ void __launch_bounds__(384, 1) pchain_kernel(unsigned long long* cycles, int steps, const uint8_t* src) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
+  constexpr int kSub = 128 * 128;
+  const uint32_t sQ = smem_u32(smem), sK = sQ + 4 * kSub, sV = sK + 2 * kSub, sP = sV + 2 * kSub, sX = sP + 4 * kSub;
+  const uint32_t bar = sX + ((MODE & 4) ? 2 * kSub : 0);
+  auto bS = [&](int t) { return bar + 8 * t; };
+  auto bSf = [&](int t) { return bar + 16 + 8 * t; };
+  auto bP = [&](int t) { return bar + 32 + 8 * t; };
+  auto bPV = [&](int t) { return bar + 48 + 8 * t; };
+  const uint32_t bX = bar + 64;
+  __shared__ uint32_t tmem_slot;
+  __shared__ volatile int done_flag;
+  for (int i = threadIdx.x; i < 12 * kSub / 4; i += 384)
+    reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(bS(t), 1);
+      mbar_init(bSf(t), 128);
+      mbar_init(bP(t), 128);
+      mbar_init(bPV(t), 1);
+    }
+    mbar_init(bX, 1);
+    done_flag = 0;
+    fence_mbar_init();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x / 32 == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
+  const int warp = threadIdx.x / 32;
+  constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false), idPV = idesc_bf16_f32(128, 128, false, true);
+  if (warp == 9) {
+    const unsigned long long t0 = clock64();
+    auto issue_S = [&](int t) {
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t off = (k / 4) * kSub + (k % 4) * 32;
+          mma_ss(tmem + t * 128, sdesc_sw128(sQ + t * 2 * kSub + off, 16, 1024), sdesc_sw128(sK + off, 16, 1024), idS, k > 0);
+        }
+        mma_commit(bS(t));
+      }
+      __syncwarp();
+    };
+    auto issue_PV = [&](int t) {
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t off = (k / 4) * kSub + (k % 4) * 32;
+          mma_ss(tmem + 256 + t * 128, sdesc_sw128(sP + t * 2 * kSub + off, 16, 1024),
+                 sdesc_sw128(sV + k * 2048, kSub, 1024), idPV, 1);
+        }
+        mma_commit(bPV(t));
+      }
+      __syncwarp();
+    };
+    for (int t = 0; t < 2; ++t) issue_S(t);
+    for (int i = 0; i < steps; ++i) {
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(bSf(t), i & 1);
+        tc_fence_after();
+        if (i + 1 < steps) issue_S(t);
+      }
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(bP(t), i & 1);
+        tc_fence_after();
+        issue_PV(t);
+      }
+    }
+    mbar_wait(bPV(1), (steps - 1) & 1);
+    if (elect_one()) cycles[blockIdx.x] = clock64() - t0;
+    done_flag = 1;
+  } else if (warp == 10 && (MODE & 4)) {
+    uint32_t ph = 0;
+    while (!done_flag) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(bX, 2 * kSub);
+        for (int c = 0; c < 2; ++c) bulk_load_g(sX + c * kSub, src + (size_t)(blockIdx.x % 8) * 2 * kSub + c * kSub, kSub, bX);
+      }
+      __syncwarp();
+      mbar_wait(bX, ph);
+      ph ^= 1;
+    }
+  } else if (warp < 8) {
+    const int t = warp / 4, row = threadIdx.x % 128;
+    for (int i = 0; i < steps; ++i) {
+      mbar_wait(bS(t), i & 1);
+      tc_fence_after();
+      tc_fence_before();
+      mbar_arrive(bSf(t));
+      if (i > 0) mbar_wait(bPV(t), (i - 1) & 1);  // P_t(i-1) consumed
+      // write this row's 128 bf16 P values (SW128 K-major: two [128][64] sub-tiles)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int sub = j / 8, chunk = j % 8;
+        const uint32_t a = sP + t * 2 * kSub + sub * kSub + row * 128 + ((chunk ^ (row & 7)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(i + j), "r"(row), "r"(j), "r"(i) : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(bP(t));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int MODE>
+void run_pchain(const char* name, int sms) {
+  auto kern = pchain_kernel<MODE>;
+  const int smem = 12 * 128 * 128 + ((MODE & 4) ? 2 * 128 * 128 : 0) + 128 + 1024;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static uint8_t* src = nullptr;
+  if (!src) { cudaMalloc(&src, 8 * 4 * 128 * 128); cudaMemset(src, 0x3c, 8 * 4 * 128 * 128); }
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sizeof(unsigned long long) * sms);
+  cudaMemset(cyc, 0, sizeof(unsigned long long) * sms);
+  const int steps = 512;
+  kern<<<sms, 384, smem>>>(cyc, steps, src);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
+  unsigned long long h[1024];
+  cudaMemcpy(h, cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+  double csum = 0;
+  for (int i = 0; i < sms; ++i) csum += h[i];
+  const double flop = 2.0 * 2 * 2.0 * 128 * 128 * 128 * steps;
+  printf("%-28s %7.0f FLOP/clk/SM (%.3f of 8192)\n", name, flop / (csum / sms), flop / (csum / sms) / 8192.0);
+  cudaFree(cyc);
+}
+
 // SS MMA with M = 64 (cta_group::1): rate per SM relative to the 8192 FLOP/clk peak
 template <int N>
 __global__ void __launch_bounds__(128, 1) umma_m64_kernel(unsigned long long* cycles) {
@@ -380,6 +525,8 @@ int main() {
   run_chain<3>("chain sleep, P halves", sms);
   run_chain<6>("chain + smem writes (max)", sms);
   run_chain<14>("chain + smem writes (paced)", sms);
+  run_pchain<0>("P-in-smem chain", sms);
+  run_pchain<4>("P-in-smem chain + TMA stream", sms);
   run_m64<128>("cg1 SS M64 N128", sms);
   run_m64<256>("cg1 SS M64 N256", sms);
   return 0;
