@@ -76,11 +76,12 @@ def main():
         import pynvml
         pynvml.nvmlInit()
         hdl = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
-        mhz, stop = [], threading.Event()
+        mhz, watts, stop = [], [], threading.Event()
 
         def sample():
             while not stop.is_set():
                 mhz.append(pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM))
+                watts.append(pynvml.nvmlDeviceGetPowerUsage(hdl) / 1e3)
                 stop.wait(0.005)
         th = threading.Thread(target=sample)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -97,8 +98,12 @@ def main():
         tf = flops / ms / 1e9
         # dense bf16 tcgen05 rate: 8192 FLOP/clk/SM (M=128, N=128, K=16 in 64 cycles) x 148 SMs
         peak = 148 * 8192 * f * 1e6 / 1e12
+        late = mhz[len(mhz) // 2:]  # second half of the run: steady state
+        w_late = sorted(watts[len(watts) // 2:])
         print(f"clock: {ms:.3f} ms/launch  {tf:.1f} TFLOP/s  SM {f} MHz ({len(mhz)} samples)  "
-              f"tensor peak at that clock {peak:.0f} TF/s -> {tf / peak:.3f}")
+              f"tensor peak at that clock {peak:.0f} TF/s -> {tf / peak:.3f}; second half: SM "
+              f"{sorted(late)[len(late) // 2]} MHz, board {w_late[len(w_late) // 2]:.0f} W "
+              f"(max {w_late[-1]:.0f} W)")
     if a.ctatimes:
         import numpy as np
         g_ = cfg.hq // cfg.hk
