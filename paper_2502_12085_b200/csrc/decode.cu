@@ -94,6 +94,10 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
   using L = MmaSmem<D>;
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int NT = D / 64;  // O n-tiles (of 8 columns) per warp: D/8 tiles over 8 warps
+  // programmatic dependent launch: the merge / fold that follows may be scheduled as soon as every
+  // CTA of this grid has started (it waits in griddepcontrol.wait for this grid's completion and
+  // memory flush), so its launch latency and ramp overlap this grid's tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int R = p.t * p.g;
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(smem + kMStages * L::kStage);  // [16 MT][kRow]
   __nv_bfloat16* pss = qs + 16 * MT * L::kRow;                                       // [16 MT][kPRow]
@@ -394,6 +398,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(int n, int64_t 
                                                                  const float* __restrict__ parts_lse, int64_t stride_o,
                                                                  int64_t stride_lse, int lse_in_log2,
                                                                  OutT* __restrict__ out, float* __restrict__ out_lse) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched with PDL
   merge_row<D, OutT>(blockIdx.x, n, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, out, out_lse);
 }
 
@@ -405,6 +410,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fold_hosts_kernel(const Deco
                                                                       const float* __restrict__ ws_lse,
                                                                       float* __restrict__ parts, int64_t part_stride,
                                                                       int64_t lse_offset) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched with PDL
   const int i = blockIdx.y, s0 = hb.split_begin[i];
   float* dst = parts + (int64_t)i * part_stride;
   merge_row<D, float>(blockIdx.x, hb.split_begin[i + 1] - s0, ws_o + (int64_t)s0 * rows * D, ws_lse + (int64_t)s0 * rows,
@@ -412,6 +418,26 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fold_hosts_kernel(const Deco
 }
 
 }  // namespace dec
+
+// Launch configuration for a kernel that follows decode_mma_kernel on the same stream: with `pdl`
+// it is a programmatic dependent launch (scheduled once every streaming CTA has issued
+// griddepcontrol.launch_dependents; the kernel's griddepcontrol.wait then blocks until the
+// streaming grid has completed and its writes are visible).
+static cudaLaunchAttribute pdl_attr() {
+  cudaLaunchAttribute a;
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+  return a;
+}
+static cudaLaunchConfig_t pdl_config(dim3 grid, int threads, size_t smem, cudaStream_t stream, bool pdl) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = grid;
+  c.blockDim = dim3(threads);
+  c.dynamicSmemBytes = smem;
+  c.stream = stream;
+  c.numAttrs = pdl ? 1 : 0;
+  return c;
+}
 
 // Split plan of the streaming kernel: ~kSplitTarget CTAs over (splits x KV heads), whole
 // 64-key chunks per split.  Deterministic in the sizes only (no device query), so the
@@ -510,13 +536,14 @@ apb_status launch_decode(const DecodeParams& p0, float* part_o, float* part_lse,
   char* base = reinterpret_cast<char*>(p.ws_o);
   p.ws_lse = reinterpret_cast<float*>(base + ws_off_lse(splits, rows, p.D));
   if (splits == 0)  // no key at all: the merge of zero parts writes O = 0, lse = -inf
-    return launch_merge(0, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream);
+    return launch_merge(0, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream, false);
   DecodeHosts hb{};
   hb.n = 0;
   hb.new_host = -1;
   if (apb_status st = launch_partials(p, hb, splits, cps, stream)) return st;
   // fold the splits (LSE merge, fixed order): the host's fp32 partial, natural-log lse
-  return launch_merge((int)splits, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream);
+  return launch_merge((int)splits, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, part_o, false, part_lse, stream,
+                      true);
 }
 
 apb_status launch_decode_hosts(const DecodeParams& p0, DecodeHosts hb, const int64_t* n_keys, float* parts,
@@ -533,20 +560,23 @@ apb_status launch_decode_hosts(const DecodeParams& p0, DecodeHosts hb, const int
   if (rows == 0) return APB_OK;
   if (merged_out)  // every host is here: MergeScore directly over all hosts' splits (log2 lse), bf16 out
     return launch_merge((int)splits, rows, p.D, p.ws_o, p.ws_lse, rows * p.D, rows, 1, merged_out, true, merged_lse,
-                        stream);
+                        stream, splits > 0);
   const dim3 grid((unsigned)rows, (unsigned)hb.n);
   size_t smem = 0;
   for (int i = 0; i < hb.n; ++i) {
     const size_t b = (size_t)(hb.split_begin[i + 1] - hb.split_begin[i]) * sizeof(float);
     smem = b > smem ? b : smem;
   }
-  if (p.D == 128)
-    dec::fold_hosts_kernel<128><<<grid, dec::kMergeWarps * 32, smem, stream>>>(hb, rows, p.ws_o, p.ws_lse, parts,
-                                                                                part_stride, lse_offset);
-  else
-    dec::fold_hosts_kernel<64><<<grid, dec::kMergeWarps * 32, smem, stream>>>(hb, rows, p.ws_o, p.ws_lse, parts,
-                                                                               part_stride, lse_offset);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = pdl_config(grid, dec::kMergeWarps * 32, smem, stream, splits > 0);
+  cudaLaunchAttribute attr = pdl_attr();
+  cfg.attrs = &attr;
+  const float* ws_o = p.ws_o;
+  const float* ws_lse = p.ws_lse;
+  cudaError_t e = p.D == 128 ? cudaLaunchKernelEx(&cfg, dec::fold_hosts_kernel<128>, hb, rows, ws_o, ws_lse, parts,
+                                                  part_stride, lse_offset)
+                             : cudaLaunchKernelEx(&cfg, dec::fold_hosts_kernel<64>, hb, rows, ws_o, ws_lse, parts,
+                                                  part_stride, lse_offset);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("fold launch: ") + cudaGetErrorString(e));
   count_launch();
   return APB_OK;
@@ -554,24 +584,25 @@ apb_status launch_decode_hosts(const DecodeParams& p0, DecodeHosts hb, const int
 
 apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,
                         int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, bool pdl) {
   if (rows == 0) return APB_OK;
-  if (D == 128) {
-    if (out_bf16)
-      dec::merge_kernel<128, __nv_bfloat16><<<(unsigned)rows, dec::kMergeWarps * 32, (size_t)n * sizeof(float), stream>>>(
-          n, rows, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, static_cast<__nv_bfloat16*>(out), out_lse);
-    else
-      dec::merge_kernel<128, float><<<(unsigned)rows, dec::kMergeWarps * 32, (size_t)n * sizeof(float), stream>>>(
-          n, rows, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, static_cast<float*>(out), out_lse);
-  } else {
-    if (out_bf16)
-      dec::merge_kernel<64, __nv_bfloat16><<<(unsigned)rows, dec::kMergeWarps * 32, (size_t)n * sizeof(float), stream>>>(
-          n, rows, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, static_cast<__nv_bfloat16*>(out), out_lse);
-    else
-      dec::merge_kernel<64, float><<<(unsigned)rows, dec::kMergeWarps * 32, (size_t)n * sizeof(float), stream>>>(
-          n, rows, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, static_cast<float*>(out), out_lse);
-  }
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = pdl_config(dim3((unsigned)rows), dec::kMergeWarps * 32, (size_t)n * sizeof(float), stream, pdl);
+  cudaLaunchAttribute attr = pdl_attr();
+  cfg.attrs = &attr;
+  __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(out);
+  float* of = static_cast<float*>(out);
+  cudaError_t e;
+  if (D == 128)
+    e = out_bf16 ? cudaLaunchKernelEx(&cfg, dec::merge_kernel<128, __nv_bfloat16>, n, rows, parts_o, parts_lse, stride_o,
+                                      stride_lse, lse_in_log2, ob, out_lse)
+                 : cudaLaunchKernelEx(&cfg, dec::merge_kernel<128, float>, n, rows, parts_o, parts_lse, stride_o,
+                                      stride_lse, lse_in_log2, of, out_lse);
+  else
+    e = out_bf16 ? cudaLaunchKernelEx(&cfg, dec::merge_kernel<64, __nv_bfloat16>, n, rows, parts_o, parts_lse, stride_o,
+                                      stride_lse, lse_in_log2, ob, out_lse)
+                 : cudaLaunchKernelEx(&cfg, dec::merge_kernel<64, float>, n, rows, parts_o, parts_lse, stride_o,
+                                      stride_lse, lse_in_log2, of, out_lse);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
   count_launch();
   return APB_OK;

@@ -110,6 +110,6 @@ apb_status launch_decode_hosts(const DecodeParams& p, DecodeHosts hb, const int6
                                cudaStream_t stream);
 apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const float* parts_lse, int64_t stride_o,
                         int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,
-                        cudaStream_t stream);
+                        cudaStream_t stream, bool pdl = false);  // pdl: follows decode_mma_kernel on `stream`
 
 }  // namespace apb

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--hk", type=int, default=None, help="override KV heads")
     ap.add_argument("--lb", type=int, default=None, help="override cache rows per host")
     ap.add_argument("--per-host", action="store_true", help="one apb_decode_attention per host (no batched launch)")
+    ap.add_argument("--queued", action="store_true",
+                    help="spin the GPU ~1 ms before the start event so the step's launches are queued (device time only)")
     ap.add_argument("--no-fuse", action="store_true", help="batched partials + MergeScore (not apb_decode_step_hosts)")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
@@ -47,6 +49,8 @@ def main():
     times = []
     for i in range(a.iters + 3):
         flush.zero_()
+        if a.queued:
+            torch.cuda._sleep(2_000_000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         dr.step(q, caches, kn, vn, out)
@@ -61,7 +65,7 @@ def main():
     gbs = cache_bytes / (ms / 1e3) / 1e9
     print(json.dumps({"config": a.config, "launch": "per-host" if a.per_host else ("batched partials (apb_decode_attention_hosts)" if a.no_fuse
                                                                     else "fused step (apb_decode_step_hosts)"), "hq": cfg.hq, "hk": cfg.hk, "t_new": a.t, "hosts": cfg.H, "cache_rows_per_host": cfg.l_b,
-                      "ms_per_layer_step": round(ms, 4), "cache_bytes": cache_bytes, "achieved_gbs": round(gbs, 1),
+                      "queued": a.queued, "ms_per_layer_step": round(ms, 4), "cache_bytes": cache_bytes, "achieved_gbs": round(gbs, 1),
                       "hbm_peak_gbs": peaks["hbm_gbs"], "frac": round(gbs / peaks["hbm_gbs"], 3)}))
 
 
