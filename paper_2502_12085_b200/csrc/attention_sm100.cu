@@ -20,6 +20,8 @@
 // in-order tensor pipe never overwrites P_t(j) before it is read.
 // Online softmax in the log2 domain with conditional rescaling: O_t is rescaled only when a
 // row max grows by more than 8 (2^8 headroom in fp32), which after the first few tiles is rare.
+#include <cstdlib>
+
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -213,7 +215,12 @@ __device__ __forceinline__ int visible_cols(const AttnParams& p, const Item& it,
   return ub < 0 ? 0 : (ub > BN ? BN : ub);
 }
 
-template <int D>
+// PAIR (cluster of 2 CTAs, D = 128, g % 4 == 0): the two CTAs of a cluster hold consecutive work
+// items, i.e. the 4 query heads of one row tile of KV head j, and walk the same key tiles.  Each
+// CTA loads one 64-column half of every K/V tile and multicasts it to both, so each tile crosses
+// L2 -> SM once per pair instead of once per CTA.  A ring slot is refilled only after both CTAs'
+// MMAs released it (empty barriers count 2, released by multicast commits).
+template <int D, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     apb_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(bQ, 1);
     for (int r = 0; r < NR; ++r) {
       mbar_init(bRf(r), 1);
-      mbar_init(bRe(r), 1);
+      mbar_init(bRe(r), PAIR ? 2 : 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(bS(t), 1);
@@ -272,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the peer's barriers are initialised before any multicast
   tc_fence_after();
   // TMEM base broadcast from lane 0: provably warp-uniform, so every TMEM address and UMMA
   // operand below lives in uniform registers (no per-instruction waterfall loops).
@@ -288,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d_hint(dst, map, bar, a, b, c, pol_kv)
 #define KV_LOAD4(dst, map, bar, a, b, c, d) tma_load_4d_hint(dst, map, bar, a, b, c, d, pol_kv)
 #else
+      const uint64_t pol_kv = policy_evict_last();  // PAIR's multicast loads keep the hint
 #define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d(dst, map, bar, a, b, c)
 #define KV_LOAD4(dst, map, bar, a, b, c, d) tma_load_4d(dst, map, bar, a, b, c, d)
 #endif
@@ -324,8 +333,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
           mbar_wait_sleep(bRe(r), ((n / NR) & 1) ^ 1);
           if (elect_one()) {
-            if ((p.dbg_skip & (1 << kv)) && i >= NR) {
+            if (!PAIR && (p.dbg_skip & (1 << kv)) && i >= NR) {
               mbar_arrive(bRf(r));
+            } else if constexpr (PAIR) {
+              // this CTA's half of the tile, into the same slot of both CTAs of the pair
+              const int h = static_cast<int>(cluster_ctarank());
+              mbar_arrive_expect_tx(bRf(r), L::kTile);
+              if (kt.kind == 1)
+                tma_load_4d_mc_hint(sR(r) + h * L::kSub, &tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv, 0x3, pol_kv);
+              else
+                tma_load_3d_mc_hint(sR(r) + h * L::kSub, kv ? &tm_v : &tm_k, bRf(r), h * 64, it.j, row0, 0x3, pol_kv);
             } else {
               mbar_arrive_expect_tx(bRf(r), L::kTile);
               for (int h = 0; h < L::kHalves; ++h) {
@@ -337,6 +354,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           __syncwarp();
+        }
+      }
+      if constexpr (PAIR) {
+        // drain: every release of this CTA's slots (by both MMA warps) has landed before exit
+        const int ntot = 2 * it.nkv;
+        for (int r = 0; r < NR && r < ntot; ++r) {
+          const int n_last = r + ((ntot - 1 - r) / NR) * NR;
+          mbar_wait_sleep(bRe(r), (n_last / NR) & 1);
         }
       }
     } else if (warp == kMmaWarp) {
@@ -358,6 +383,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto commit = [&](uint32_t bar) {
         if (elect_one()) mma_commit(bar);
+        __syncwarp();
+      };
+      // release of a ring slot: in PAIR mode on both CTAs' empty barriers
+      auto release = [&](int slot) {
+        if (elect_one()) {
+          if constexpr (PAIR) mma_commit_mc(bRe(slot), 0x3);
+          else mma_commit(bRe(slot));
+        }
         __syncwarp();
       };
       int trace_i = 0;
@@ -397,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(bRf(0), 0);
         tc_fence_after();
         for (int t = 0; t < it.ntiles; ++t) issue_S(t, 0);
-        commit(bRe(0));
+        release(0);
       }
       for (int i = 0; i < it.nkv; ++i) {
         if (i + 1 < it.nkv) {
@@ -408,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             issue_S(t, n % NR);
           }
-          commit(bRe(n % NR));
+          release(n % NR);
         }
         const int n = nV(i), sv = n % NR;
         mbar_wait_sleep(bRf(sv), (n / NR) & 1);
@@ -428,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           commit(bO(t));  // PVdone(t): P_t is free and O_t stable
         }
-        commit(bRe(sv));
+        release(sv);
       }
       (void)issue_PV;
 #else
@@ -442,14 +475,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             TRACE(t, 0);
             issue_S(t, nK % NR);
           }
-          commit(bRe(nK % NR));
+          release(nK % NR);
         }
         mbar_wait_sleep(bRf(nV % NR), (nV / NR) & 1);
         TRACE(12, i);
         tc_fence_after();
         for (int t = 0; t < it.ntiles; ++t) {
           issue_PV(t, nV % NR, carry || i > 0, i & 1);
-          if (t == it.ntiles - 1) commit(bRe(nV % NR));
+          if (t == it.ntiles - 1) release(nV % NR);
           if (i + 1 < it.nkv) {
             if (t == 0) {
               mbar_wait_sleep(bRf(nK1 % NR), (nK1 / NR) & 1);
@@ -458,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             TRACE(t, i + 1);
             issue_S(t, nK1 % NR);
-            if (t == it.ntiles - 1) commit(bRe(nK1 % NR));
+            if (t == it.ntiles - 1) release(nK1 % NR);
           } else {
             commit(bO(t));
           }
@@ -730,6 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // neither CTA exits while the peer may still write to it
   CTA_TIME(1);
   if (warp == kLoadWarp) {
     tc_fence_after();
@@ -737,17 +771,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D>
+// Paired (2-CTA cluster, multicast K/V) launch: on by default where it applies (D = 128, g % 4 == 0);
+// APB_ATTN_PAIR=0 in the environment selects the single-CTA kernel (A/B timing).
+// Read per launch (a getenv per multi-ms launch) so a test can compare both kernels in one process.
+static bool pair_enabled() {
+  const char* e = std::getenv("APB_ATTN_PAIR");
+  return !(e && e[0] == '0');
+}
+
+template <int D, bool PAIR>
 static apb_status launch_impl(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                               const CUtensorMap& tg, cudaStream_t stream) {
   using L = Layout<D>;
   const int grid = p.n_local_items + p.n_anchor_items;
   if (grid == 0) return APB_OK;
   static std::atomic<uint64_t> smem_set{0};
-  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(apb_attention_kernel<D>), L::kAlloc, smem_set))
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(apb_attention_kernel<D, PAIR>), L::kAlloc, smem_set))
     return st;
-  apb_attention_kernel<D><<<grid, kThreads, L::kAlloc, stream>>>(tq, tk, tv, tg, p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = L::kAlloc;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, apb_attention_kernel<D, PAIR>, tq, tk, tv, tg, p);
+  } else {
+    apb_attention_kernel<D, PAIR><<<grid, kThreads, L::kAlloc, stream>>>(tq, tk, tv, tg, p);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   count_launch();
   return APB_OK;
@@ -770,8 +829,13 @@ extern "C" int apb_debug_cta_times(unsigned long long* out, int n_ctas) {
 
 apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream) {
-  if (D == 128) return attn::launch_impl<128>(p, tq, tk, tv, tg, stream);
-  if (D == 64) return attn::launch_impl<64>(p, tq, tk, tv, tg, stream);
+#ifndef APB_PSMEM
+  // pairs of consecutive work items share (KV head, row tile) exactly when g % 4 == 0; both
+  // segments then hold an even number of items (decode_item)
+  if (D == 128 && p.g % 4 == 0 && attn::pair_enabled()) return attn::launch_impl<128, true>(p, tq, tk, tv, tg, stream);
+#endif
+  if (D == 128) return attn::launch_impl<128, false>(p, tq, tk, tv, tg, stream);
+  if (D == 64) return attn::launch_impl<64, false>(p, tq, tk, tv, tg, stream);
   return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
 }
 

@@ -96,6 +96,9 @@ CASES = {
     # MHA (g = 1: one query head per KV head, odd unit count per KV head) and g = 8 (Llama-70B ratio)
     "mha": synth.Config("mha", 16, n=1152, H=3, l_a=70, l_p=40, hq=3, hk=3, d=128, d_hidden=256),
     "gqa8": synth.Config("gqa8", 17, n=768, H=2, l_a=130, l_p=96, hq=16, hk=2, d=64, d_hidden=256),
+    # d = 128 with g % 4 == 0 runs the paired (2-CTA cluster, multicast K/V) kernel; g = 8 pairs
+    # two items of one row tile, ragged anchor / local tails
+    "gqa8-d128": synth.Config("gqa8-d128", 18, n=1656, H=3, l_a=150, l_p=70, hq=16, hk=2, d=128, d_hidden=256),
 }
 
 
@@ -259,6 +262,22 @@ def test_attention_determinism():
     a = run_attention(cfg, 3, hosts[3], ref["gathered"], "split")
     b = run_attention(cfg, 3, hosts[3], ref["gathered"], "split")
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("name", ["d128-ragged", "gqa8-d128"])
+@pytest.mark.parametrize("phase", ["all", "split"])
+def test_attention_paired_matches_single_cta(name, phase, monkeypatch):
+    """The paired kernel (2-CTA cluster, each CTA multicasting half of every K/V tile) feeds the
+    MMAs the same tiles in the same order as the single-CTA kernel: bit-identical O and lse."""
+    cfg = CASES[name]
+    assert cfg.d == 128 and (cfg.hq // cfg.hk) % 4 == 0
+    hosts, ref = oracle_layer(cfg)
+    for h in range(cfg.H):
+        monkeypatch.setenv("APB_ATTN_PAIR", "1")
+        a = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
+        monkeypatch.setenv("APB_ATTN_PAIR", "0")
+        b = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
+        assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True), f"host {h}"
 
 
 # ----------------------------------------------------------------------------- full size
