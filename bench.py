@@ -347,7 +347,11 @@ def main():
         traffic = json.load(open(tpath)).get(args.config, {}).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
-                "kernel": "apb_attention_kernel<128> (" + ("LOCAL + PASSING launches" if pr.split_phases
+                "kernel": "apb_attention_kernel<128" + (", paired: 2-CTA clusters multicasting K/V"
+                                                         if (cfg.hq // cfg.hk) % 4 == 0
+                                                         and os.environ.get("APB_ATTN_PAIR", "1")[:1] != "0"
+                                                         else "") + "> ("
+                + ("LOCAL + PASSING launches" if pr.split_phases
                                                            else "one ordered PHASE_ALL launch per host") + ")",
                 "peak_source": f"bf16_tflops_sustained, {peak_src}",
                 "flops_per_step": flops_rank * layers,

@@ -27,37 +27,48 @@ using namespace apb::sm100;
 constexpr int TM = 128;     // tokens per CTA
 constexpr int TN = 256;     // hidden units per chunk (MMA N)
 constexpr int TK = 64;      // K block (one 128-byte swizzle atom)
-constexpr int STAGES = 3;
 constexpr int kThreads = 320;
 constexpr int kLoadWarp = 8, kMmaWarp = 9;
-constexpr int kMaxOut = 64;
 constexpr int kCluster = 4;
 constexpr int kBSlice = TN / kCluster;  // W1 rows each CTA fetches per k block
-
 constexpr int kABytes = TM * TK * 2;  // 16 KB
 constexpr int kBBytes = TN * TK * 2;  // 32 KB
-constexpr int kOffA = 0;
-constexpr int kOffB = kOffA + STAGES * kABytes;
-constexpr int kOffW2 = kOffB + STAGES * kBBytes;            // fp32 W2 slice of one chunk [kMaxOut][TN]
-constexpr int kOffB1 = kOffW2 + kMaxOut * TN * 4;             // fp32 b1 slice [TN]
-constexpr int kOffBar = kOffB1 + TN * 4;
-constexpr int kNumBars = 2 * STAGES + 4;                      // full/empty per stage, acc full/empty x2
-constexpr int kOffTmem = kOffBar + kNumBars * 8;
-constexpr int kSmem = kOffTmem + 16 + 1024;
 
+// Shared-memory plan for a pipeline depth and a W2-slice capacity (outputs).  n_out <= 32 (every
+// paper config scores per query head at most 32 heads per host) leaves room for a 4th stage:
+// the A rows stream from HBM (re-read once per hidden chunk), so the deeper ring hides more of
+// their latency.
+template <int STAGES_, int MAXOUT_>
+struct Plan {
+  static constexpr int STAGES = STAGES_;
+  static constexpr int kMaxOut = MAXOUT_;
+  static constexpr int kOffA = 0;
+  static constexpr int kOffB = kOffA + STAGES * kABytes;
+  static constexpr int kOffW2 = kOffB + STAGES * kBBytes;     // fp32 W2 slice of one chunk [kMaxOut][TN]
+  static constexpr int kOffB1 = kOffW2 + kMaxOut * TN * 4;      // fp32 b1 slice [TN]
+  static constexpr int kOffBar = kOffB1 + TN * 4;
+  static constexpr int kNumBars = 2 * STAGES + 4;               // full/empty per stage, acc full/empty x2
+  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
+  static constexpr int kSmem = kOffTmem + 16 + 1024;
+  static_assert(kSmem <= 232448, "shared memory");
+};
+
+template <class PL>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     retain_score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_w1,
                         const ScoreParams p) {
+  constexpr int STAGES = PL::STAGES, kMaxOut = PL::kMaxOut;
+  constexpr int kOffA = PL::kOffA, kOffB = PL::kOffB, kOffW2 = PL::kOffW2, kOffB1 = PL::kOffB1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar0 = sbase + kOffBar;
+  const uint32_t bar0 = sbase + PL::kOffBar;
   auto bFull = [&](int s) { return bar0 + 8u * s; };
   auto bEmpty = [&](int s) { return bar0 + 8u * (STAGES + s); };
   auto bAccFull = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
   auto bAccEmpty = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + PL::kOffTmem);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   const int m0 = blockIdx.x * TM;
@@ -231,18 +242,30 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
 
 }  // namespace score
 
-apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                               const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream) {
+namespace score {
+template <class PL>
+static apb_status launch(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                         const CUtensorMap& tw1, cudaStream_t stream) {
   static std::atomic<uint64_t> smem_set{0};
-  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(score::retain_score_kernel), score::kSmem, smem_set))
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(retain_score_kernel<PL>), PL::kSmem, smem_set))
     return st;
-  int grid = (p.l_b + score::TM - 1) / score::TM;
-  grid = (grid + score::kCluster - 1) / score::kCluster * score::kCluster;  // whole clusters
-  score::retain_score_kernel<<<grid, score::kThreads, score::kSmem, stream>>>(tq, tk, tv, tw1, p);
+  int grid = (p.l_b + TM - 1) / TM;
+  grid = (grid + kCluster - 1) / kCluster * kCluster;  // whole clusters
+  retain_score_kernel<PL><<<grid, kThreads, PL::kSmem, stream>>>(tq, tk, tv, tw1, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("retain_score launch: ") + cudaGetErrorString(e));
   count_launch();
   return APB_OK;
+}
+}  // namespace score
+
+apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                               const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream) {
+#ifndef APB_SCORE_STAGES4
+#define APB_SCORE_STAGES4 1
+#endif
+  if (APB_SCORE_STAGES4 && p.n_out <= 32) return score::launch<score::Plan<4, 32>>(p, tq, tk, tv, tw1, stream);
+  return score::launch<score::Plan<3, 64>>(p, tq, tk, tv, tw1, stream);
 }
 
 }  // namespace apb
