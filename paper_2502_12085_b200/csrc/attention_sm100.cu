@@ -215,11 +215,14 @@ __device__ __forceinline__ int visible_cols(const AttnParams& p, const Item& it,
   return ub < 0 ? 0 : (ub > BN ? BN : ub);
 }
 
-// PAIR (cluster of 2 CTAs, D = 128, g % 4 == 0): the two CTAs of a cluster hold consecutive work
-// items, i.e. the 4 query heads of one row tile of KV head j, and walk the same key tiles.  Each
-// CTA loads one 64-column half of every K/V tile and multicasts it to both, so each tile crosses
-// L2 -> SM once per pair instead of once per CTA.  A ring slot is refilled only after both CTAs'
-// MMAs released it (empty barriers count 2, released by multicast commits).
+// PAIR (cluster of 2 CTAs, D = 128): the two CTAs of a cluster hold consecutive work items of the
+// same KV head j and segment.  The key-tile walk depends only on (segment, phase, tile index), so
+// the lighter item's walk is a prefix of the heavier one's (equal when g % 4 == 0; one diagonal
+// tile shorter for odd g).  Over the shared prefix each CTA loads one 64-column half of every K/V
+// tile and multicasts it to both, so the tile crosses L2 -> SM once per pair; a ring slot is
+// refilled only after both CTAs' MMAs released it (empty barriers count 2, released by multicast
+// commits).  Tiles past the prefix are loaded whole by the CTA that needs them and released by two
+// local commits.
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     apb_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -248,6 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   const Item it = decode_item(p, blockIdx.x);
+  // K/V tiles shared with the partner CTA (PAIR): the common prefix of the two walks
+  const int n_shared = PAIR ? min(it.nkv, decode_item(p, blockIdx.x ^ 1).nkv) : 0;
   CTA_TIME(0);
 
   if (threadIdx.x == 0) {
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (elect_one()) {
             if (!PAIR && (p.dbg_skip & (1 << kv)) && i >= NR) {
               mbar_arrive(bRf(r));
-            } else if constexpr (PAIR) {
+            } else if (PAIR && i < n_shared) {
               // this CTA's half of the tile, into the same slot of both CTAs of the pair
               const int h = static_cast<int>(cluster_ctarank());
               mbar_arrive_expect_tx(bRf(r), L::kTile);
@@ -386,10 +391,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       };
       // release of a ring slot: in PAIR mode on both CTAs' empty barriers
-      auto release = [&](int slot) {
+      // (tile i of the walk; past the shared prefix both arrivals are local)
+      auto release = [&](int slot, int i) {
         if (elect_one()) {
-          if constexpr (PAIR) mma_commit_mc(bRe(slot), 0x3);
-          else mma_commit(bRe(slot));
+          if (PAIR && i < n_shared) {
+            mma_commit_mc(bRe(slot), 0x3);
+          } else {
+            mma_commit(bRe(slot));
+            if (PAIR) mma_commit(bRe(slot));
+          }
         }
         __syncwarp();
       };
@@ -430,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(bRf(0), 0);
         tc_fence_after();
         for (int t = 0; t < it.ntiles; ++t) issue_S(t, 0);
-        release(0);
+        release(0, 0);
       }
       for (int i = 0; i < it.nkv; ++i) {
         if (i + 1 < it.nkv) {
@@ -441,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             issue_S(t, n % NR);
           }
-          release(n % NR);
+          release(n % NR, i + 1);
         }
         const int n = nV(i), sv = n % NR;
         mbar_wait_sleep(bRf(sv), (n / NR) & 1);
@@ -461,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           commit(bO(t));  // PVdone(t): P_t is free and O_t stable
         }
-        release(sv);
+        release(sv, i);
       }
       (void)issue_PV;
 #else
@@ -475,14 +485,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             TRACE(t, 0);
             issue_S(t, nK % NR);
           }
-          release(nK % NR);
+          release(nK % NR, 0);
         }
         mbar_wait_sleep(bRf(nV % NR), (nV / NR) & 1);
         TRACE(12, i);
         tc_fence_after();
         for (int t = 0; t < it.ntiles; ++t) {
           issue_PV(t, nV % NR, carry || i > 0, i & 1);
-          if (t == it.ntiles - 1) release(nV % NR);
+          if (t == it.ntiles - 1) release(nV % NR, i);
           if (i + 1 < it.nkv) {
             if (t == 0) {
               mbar_wait_sleep(bRf(nK1 % NR), (nK1 / NR) & 1);
@@ -491,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             TRACE(t, i + 1);
             issue_S(t, nK1 % NR);
-            if (t == it.ntiles - 1) release(nK1 % NR);
+            if (t == it.ntiles - 1) release(nK1 % NR, i + 1);
           } else {
             commit(bO(t));
           }
@@ -830,9 +840,10 @@ extern "C" int apb_debug_cta_times(unsigned long long* out, int n_ctas) {
 apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream) {
 #ifndef APB_PSMEM
-  // pairs of consecutive work items share (KV head, row tile) exactly when g % 4 == 0; both
-  // segments then hold an even number of items (decode_item)
-  if (D == 128 && p.g % 4 == 0 && attn::pair_enabled()) return attn::launch_impl<128, true>(p, tq, tk, tv, tg, stream);
+  // clusters pair items 2c and 2c+1: both must belong to the same (segment, KV head), i.e. every
+  // segment holds an even number of items per KV head (decode_item: per_head = ceil(units / 2))
+  const bool even_heads = (p.n_local_items / p.hk) % 2 == 0 && (p.n_anchor_items / p.hk) % 2 == 0;
+  if (D == 128 && even_heads && attn::pair_enabled()) return attn::launch_impl<128, true>(p, tq, tk, tv, tg, stream);
 #endif
   if (D == 128) return attn::launch_impl<128, false>(p, tq, tk, tv, tg, stream);
   if (D == 64) return attn::launch_impl<64, false>(p, tq, tk, tv, tg, stream);
