@@ -348,7 +348,7 @@ def main():
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
                 "kernel": "apb_attention_kernel<128" + (", paired: 2-CTA clusters multicasting K/V"
-                                                         if (cfg.hq // cfg.hk) % 4 == 0
+                                                         if cfg.d == 128
                                                          and os.environ.get("APB_ATTN_PAIR", "1")[:1] != "0"
                                                          else "") + "> ("
                 + ("LOCAL + PASSING launches" if pr.split_phases

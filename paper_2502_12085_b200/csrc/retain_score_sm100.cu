@@ -16,6 +16,8 @@
 // Clusters of kCluster CTAs (consecutive token tiles) share every W1 tile: each CTA fetches a
 // 1/kCluster slice and multicasts it to the whole cluster, so W1 crosses L2 once per cluster
 // instead of once per CTA (the kernel is otherwise bound by streaming W1 through L2).
+#include <cstdlib>
+
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -38,13 +40,17 @@ constexpr int kBBytes = TN * TK * 2;  // 32 KB
 // paper config scores per query head at most 32 heads per host) leaves room for a 4th stage:
 // the A rows stream from HBM (re-read once per hidden chunk), so the deeper ring hides more of
 // their latency.
-template <int STAGES_, int MAXOUT_>
+// PASS = 2 hidden chunks per pass over the A rows: every A tile feeds both TMEM accumulators, so
+// the A rows are read d_R / 512 instead of d_R / 256 times, at the cost of the MMA/epilogue
+// overlap across the pass boundary.
+template <int STAGES_, int MAXOUT_, int PASS_ = 1>
 struct Plan {
   static constexpr int STAGES = STAGES_;
   static constexpr int kMaxOut = MAXOUT_;
+  static constexpr int PASS = PASS_;
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + STAGES * kABytes;
-  static constexpr int kOffW2 = kOffB + STAGES * kBBytes;     // fp32 W2 slice of one chunk [kMaxOut][TN]
+  static constexpr int kOffW2 = kOffB + STAGES * PASS * kBBytes;  // fp32 W2 slice of one chunk [kMaxOut][TN]
   static constexpr int kOffB1 = kOffW2 + kMaxOut * TN * 4;      // fp32 b1 slice [TN]
   static constexpr int kOffBar = kOffB1 + TN * 4;
   static constexpr int kNumBars = 2 * STAGES + 4;               // full/empty per stage, acc full/empty x2
@@ -58,7 +64,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     retain_score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_w1,
                         const ScoreParams p) {
-  constexpr int STAGES = PL::STAGES, kMaxOut = PL::kMaxOut;
+  constexpr int STAGES = PL::STAGES, kMaxOut = PL::kMaxOut, PASS = PL::PASS;
+  constexpr int kStageB = PASS * kBBytes;
   constexpr int kOffA = PL::kOffA, kOffB = PL::kOffB, kOffW2 = PL::kOffW2, kOffB1 = PL::kOffB1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
@@ -97,12 +104,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == kLoadWarp) {
     // warp-converged producer; one elected lane issues the TMA copies
     const int row = p.L_A + m0;
-    for (int c = 0; c < nchunks; ++c) {
+    for (int pc = 0; pc < nchunks / PASS; ++pc) {
       for (int kb = 0; kb < nkb; ++kb) {
-        const int it = c * nkb + kb, s = it % STAGES;
+        const int it = pc * nkb + kb, s = it % STAGES;
         mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(bFull(s), kABytes + kBBytes);
+          mbar_arrive_expect_tx(bFull(s), kABytes + kStageB);
           const uint32_t dA = sbase + kOffA + s * kABytes;
           if (kb < p.kq)
             tma_load_2d(dA, &tm_q, bFull(s), kb * TK, row);
@@ -110,8 +117,10 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d(dA, &tm_k, bFull(s), (kb - p.kq) * TK, row);
           else
             tma_load_2d(dA, &tm_v, bFull(s), (kb - p.kq - p.kk) * TK, row);
-          tma_load_2d_mc(sbase + kOffB + s * kBBytes + crank * (kBSlice * 128), &tm_w1, bFull(s), kb * TK,
-                         c * TN + crank * kBSlice, kMask);
+#pragma unroll
+          for (int q = 0; q < PASS; ++q)
+            tma_load_2d_mc(sbase + kOffB + s * kStageB + q * kBBytes + crank * (kBSlice * 128), &tm_w1, bFull(s),
+                           kb * TK, (pc * PASS + q) * TN + crank * kBSlice, kMask);
         }
         __syncwarp();
       }
@@ -119,22 +128,30 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     // warp-converged MMA issuer; one elected lane issues tcgen05.mma / commit
     constexpr uint32_t idesc = idesc_bf16_f32(TM, TN, false, false);
-    for (int c = 0; c < nchunks; ++c) {
-      const int b = c & 1;
-      mbar_wait(bAccEmpty(b), ((c >> 1) & 1) ^ 1);
+    for (int pc = 0; pc < nchunks / PASS; ++pc) {
+      for (int q = 0; q < PASS; ++q) {
+        const int c = pc * PASS + q;
+        mbar_wait(bAccEmpty(c & 1), ((c >> 1) & 1) ^ 1);
+      }
       tc_fence_after();
       for (int kb = 0; kb < nkb; ++kb) {
-        const int it = c * nkb + kb, s = it % STAGES;
+        const int it = pc * nkb + kb, s = it % STAGES;
         mbar_wait(bFull(s), (it / STAGES) & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t aA = sbase + kOffA + s * kABytes, aB = sbase + kOffB + s * kBBytes;
+          const uint32_t aA = sbase + kOffA + s * kABytes;
 #pragma unroll
-          for (int k = 0; k < TK / 16; ++k)
-            mma_ss(tmem + b * TN, sdesc_sw128(aA + k * 32, 16, 1024), sdesc_sw128(aB + k * 32, 16, 1024), idesc,
-                   (kb > 0 || k > 0) ? 1u : 0u);
+          for (int q = 0; q < PASS; ++q) {
+            const int b = (pc * PASS + q) & 1;
+            const uint32_t aB = sbase + kOffB + s * kStageB + q * kBBytes;
+#pragma unroll
+            for (int k = 0; k < TK / 16; ++k)
+              mma_ss(tmem + b * TN, sdesc_sw128(aA + k * 32, 16, 1024), sdesc_sw128(aB + k * 32, 16, 1024), idesc,
+                     (kb > 0 || k > 0) ? 1u : 0u);
+          }
           mma_commit_mc(bEmpty(s), kMask);  // frees the stage in every CTA (their loads multicast here)
-          if (kb == nkb - 1) mma_commit(bAccFull(b));
+          if (kb == nkb - 1)
+            for (int q = 0; q < PASS; ++q) mma_commit(bAccFull((pc * PASS + q) & 1));
         }
         __syncwarp();
       }
@@ -261,10 +278,13 @@ static apb_status launch(const ScoreParams& p, const CUtensorMap& tq, const CUte
 
 apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream) {
-#ifndef APB_SCORE_STAGES4
-#define APB_SCORE_STAGES4 1
-#endif
-  if (APB_SCORE_STAGES4 && p.n_out <= 32) return score::launch<score::Plan<4, 32>>(p, tq, tk, tv, tw1, stream);
+  // APB_SCORE_PLAN (timing experiments): "s3" forces the 3-stage plan, "p2" two chunks per pass
+  const char* plan = std::getenv("APB_SCORE_PLAN");
+  const bool force3 = plan && plan[0] == 's' && plan[1] == '3';
+  const bool pass2 = plan && plan[0] == 'p' && plan[1] == '2';
+  if (pass2 && p.n_out <= 32 && (p.d_hidden / score::TN) % 2 == 0)
+    return score::launch<score::Plan<2, 32, 2>>(p, tq, tk, tv, tw1, stream);
+  if (!force3 && p.n_out <= 32) return score::launch<score::Plan<4, 32>>(p, tq, tk, tv, tw1, stream);
   return score::launch<score::Plan<3, 64>>(p, tq, tk, tv, tw1, stream);
 }
 

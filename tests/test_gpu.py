@@ -168,6 +168,24 @@ def test_retain_score_parity(name, n_out):
         assert np.array_equal(s2.cpu().double().numpy(), s)
 
 
+@pytest.mark.parametrize("plan", ["s3", "p2"])
+def test_retain_score_plans_bit_identical(plan, monkeypatch):
+    """The scoring kernel's pipeline plans (3- or 4-stage ring, one or two hidden chunks per pass
+    over the A rows) run the same MMAs in the same K order and the same epilogue: bit-identical."""
+    from paper_2502_12085_b200 import apb
+    cfg = CASES["d128-ragged"].replace(d_hidden=1024)
+    w = synth.retain_weights(cfg, 0, n_out=cfg.hq)
+    x = synth.host_qkv(cfg, 0, 1)
+    out = []
+    for env in ("", plan):
+        monkeypatch.setenv("APB_SCORE_PLAN", env)
+        s = torch.empty((cfg.hk, cfg.l_b), dtype=torch.float32, device="cuda")
+        apb.retain_score(dims_of(cfg, 1), weights_dev(w), dev(x["q"]), dev(x["k"]), dev(x["v"]), s)
+        torch.cuda.synchronize()
+        out.append(s.cpu().numpy())
+    assert np.array_equal(out[0], out[1])
+
+
 def _select_gpu(cfg, h, x, scores_np):
     from paper_2502_12085_b200 import apb
     s = torch.from_numpy(np.ascontiguousarray(scores_np, dtype=np.float32)).cuda()
