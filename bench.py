@@ -182,11 +182,14 @@ def run_reference(args, rank):
     cfg = synth.CONFIGS[args.config]
     H = args.hosts or cfg.H
     layers = args.layers or cfg.layers
+    # Same bounded sample as the GPU arm's cpu_baseline leg (64 rows/host, 16 tokens: ~4 s per step
+    # on 16 cores), so both report one oracle throughput; a smaller sample is dominated by the
+    # oracle's fixed per-call cost and extrapolates to a ~4x lower number.
     for _ in range(args.warmup):
-        oracle_sample(cfg, H, layers, rows_per_host=8, tokens=4)
+        oracle_sample(cfg, H, layers)
     vals, secs = [], []
     for _ in range(args.steps):
-        v, s, sample = oracle_sample(cfg, H, layers, rows_per_host=8, tokens=4)
+        v, s, sample = oracle_sample(cfg, H, layers)
         vals.append(v)
         secs.append(s)
     value = statistics.median(vals)
