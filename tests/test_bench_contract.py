@@ -22,3 +22,5 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+    # the reference arm times the same bounded oracle sample as the GPU arm's cpu_baseline leg
+    assert "64 sampled query rows" in d["cpu_baseline"]["sample"] and "16 tokens" in d["cpu_baseline"]["sample"]
