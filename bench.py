@@ -64,6 +64,10 @@ def parse():
                     help="auto: LOCAL/PASSING split around the exchange only when N > 1")
     ap.add_argument("--same-device", action="store_true",
                     help="debug: every rank uses cuda:0 (multi-rank logic on a single GPU)")
+    ap.add_argument("--dist", choices=["D1", "D2"], default="D1",
+                    help="Q/K/V distribution: D1 N(0,1) (the paper's synthetic timing input) or D2 'peaky' "
+                         "(Q, K ~ N(0, 2^2): logit std 4, more online-softmax rescales)")
+    ap.add_argument("--no-breakdown", action="store_true", help="skip the per-op breakdown pass")
     return ap.parse_args()
 
 
@@ -174,6 +178,56 @@ def oracle_sample(cfg, H, layers, rows_per_host=64, tokens=16, hosts_sample=None
     return cfg.n / step_s, measured, sample
 
 
+def host_cores():
+    """(physical cores, cores this process may run on) of the host."""
+    phys = None
+    try:
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        phys = len({ln for ln in out.splitlines() if ln and not ln.startswith("#")})
+    except Exception:
+        pass
+    return phys, len(os.sched_getaffinity(0))
+
+
+def oracle_toy_full():
+    """The toy config (BASELINE configs[0]) through the whole oracle layer (Alg. apb_prefill,
+    every host, every row: no sampling), with all threads and with one: (tokens/s, s) each."""
+    import oracle
+    cfg = synth.CONFIGS["toy"]
+    hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    w = synth.retain_weights(cfg, 0)
+    res = {}
+    threads = oracle.num_threads()
+    for label, nt in (("all_threads", threads), ("single_thread", 1)):
+        oracle.set_num_threads(nt)
+        t0 = time.perf_counter()
+        oracle.prefill_layer(hosts, w, cfg.l_p)
+        dt = time.perf_counter() - t0
+        res[label] = {"tokens_per_s": round(cfg.n / dt, 1), "seconds": round(dt, 3), "threads": nt}
+    oracle.set_num_threads(threads)
+    return res
+
+
+def cpu_baseline_line(cfg, H, layers, value=None, sample=None):
+    """The cpu_baseline object: the oracle's extrapolated tokens/s on this workload, plus the
+    toy full run, the single-thread rate and the host's core counts."""
+    import oracle
+    if value is None:
+        value, _, sample = oracle_sample(cfg, H, layers)
+    phys, avail = host_cores()
+    toy = oracle_toy_full()
+    return {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "sample": sample,
+            "physical_cores": phys, "affinity_cores": avail,
+            "toy_full_oracle": dict(toy, config="toy: n=2048, H=4, l_a=128, l_p=64, hq=4, hk=2, d=64, 1 layer, "
+                                                "every row of every host (no extrapolation)"),
+            "single_thread_extrapolated": round(value * toy["single_thread"]["seconds"]
+                                                / toy["all_threads"]["seconds"], 4)}
+
+
+def host_layout_desc(world, H, layout):
+    return "all hosts on one GPU" if world == 1 else layout if world < H else "one host per GPU"
+
+
 def run_reference(args, rank):
     """--impl reference: the oracle (as it stands) on the host cores, bounded sample per step."""
     if rank != 0:
@@ -193,12 +247,13 @@ def run_reference(args, rank):
         vals.append(v)
         secs.append(s)
     value = statistics.median(vals)
-    cores = oracle.num_threads()
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus or 1,
+    world = args.gpus or 1
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg.n / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(cfg, H, layers, args.gpus or 1),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "config": dict(workload_config(cfg, H, layers, world),
+                           host_layout=host_layout_desc(world, H, args.host_layout)),
+            "cpu_baseline": cpu_baseline_line(cfg, H, layers, value, sample),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -248,6 +303,9 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL init logging (ranks, channels, NVLS) so the N-rank run is visible in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if args.same_device:  # NCCL refuses two ranks on one GPU: plumbing-only test mode
             dist.init_process_group("gloo")
         else:
@@ -267,7 +325,8 @@ def main():
     if args.same_device and world > 1 and split is None:
         split = True  # the multi-rank schedule (the exchange itself is skipped in this mode)
     pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True, split_phases=split,
-                     compressor=args.compressor, shared_set=args.shared_set, seed=2502)
+                     compressor=args.compressor, shared_set=args.shared_set, seed=2502,
+                     same_device=args.same_device)
 
     # ---- synthetic inputs: D1 N(0,1) Q/K/V (the paper's timing input is synthetic random
     # input), two alternating layer buffer sets, random-init retaining heads.
@@ -288,8 +347,9 @@ def main():
             if outs[h] is None:
                 outs[h] = (torch.empty((rows, cfg.hq, cfg.d), dtype=torch.bfloat16, device=dev),
                            torch.empty((cfg.hq, rows), dtype=torch.float32, device=dev))
-            io[h] = HostIO(q=rnd(rows, cfg.hq, cfg.d), k=rnd(rows, cfg.hk, cfg.d), v=rnd(rows, cfg.hk, cfg.d),
-                           out=outs[h][0], lse=outs[h][1])
+            qk_scale = 2.0 if args.dist == "D2" else 1.0
+            io[h] = HostIO(q=rnd(rows, cfg.hq, cfg.d, scale=qk_scale), k=rnd(rows, cfg.hk, cfg.d, scale=qk_scale),
+                           v=rnd(rows, cfg.hk, cfg.d), out=outs[h][0], lse=outs[h][1])
         sets.append(io)
     weights = [apb.RetainWeights(w1=rnd(cfg.d_hidden, cfg.d_in, scale=cfg.d_in ** -0.5),
                                  w2=rnd(cfg.hq, cfg.d_hidden, dtype=torch.float32, scale=cfg.d_hidden ** -0.5),
@@ -362,36 +422,97 @@ def main():
                 "tile_efficiency": round(flops_rank / executed_rank, 4),
                 "attn_ms_per_step": round(attn_ms / args.steps, 3)}
 
+    # ---- per-op breakdown (one extra, untimed step with events around every libapb call)
+    breakdown = None
+    if not args.no_breakdown:
+        breakdown = op_breakdown(pr, step, cfg, H, hosts, layers, world, peaks, barrier)
+
     # ---- end to end through the public API: pinned host inputs -> H2D every layer -> ... -> D2H
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank, barrier)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle
-        v, secs, sample = oracle_sample(cfg, H, layers)
-        cpu = {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "sample": sample}
+    if rank == 0 and not args.no_cpu_baseline:  # rank 0 only, at any N (the others wait below)
+        cpu = cpu_baseline_line(cfg, H, layers)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) Q/K/V, random-init retaining heads)",
                 "config": dict(workload_config(cfg, H, layers, world,
-                                          ("" if args.compressor == "retain" else " [compressor Rd.]")
-                                          + (" [shared index set]" if args.shared_set else "")),
-                               host_layout=("all hosts on one GPU" if world == 1 else
-                                            args.host_layout if world < H else "one host per GPU")),
+                                               ("" if args.compressor == "retain" else " [compressor Rd.]")
+                                               + (" [shared index set]" if args.shared_set else "")
+                                               + (" [D2 peaky Q/K]" if args.dist == "D2" else "")),
+                               host_layout=host_layout_desc(world, H, args.host_layout),
+                               **({"same_device": True} if args.same_device else {})),
                 "attn_peak_frac": {"critical_host": round(crit * layers / (ms_per_step / 1e3) / 1e12 / peak_tf, 4)
                                    if world == H else None,
                                    "aggregate": round(flops_all * layers / (ms_per_step / 1e3) / 1e12 / (peak_tf * world), 4)},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "breakdown": breakdown, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
+    if world > 1:
+        barrier()  # ranks > 0 wait here while rank 0 times the CPU oracle
     if comm is not None:
+        comm.check()
         comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (hardware fact; no measured figure on this pool)
+
+
+def op_breakdown(pr, step, cfg, H, hosts, layers, world, peaks, barrier):
+    """Per-step device time of every libapb op of this rank (CUDA events around each call on the
+    stream it runs on; one extra untimed step), beside its roofline lower bound.  Side-stream
+    ops (score, select_compact, exchange) overlap the attention: these are op times, not a
+    partition of ms_per_step."""
+    pr.trace = []
+    barrier()
+    step()
+    barrier()
+    tr, pr.trace = pr.trace, None
+    lpp = min(cfg.l_p, cfg.n // H)
+    l_b = cfg.n // H
+    hbm = peaks["hbm_gbs"] * 1e9
+    tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * 1e12
+    slot = 2 * cfg.hk * lpp * cfg.d * 2
+    score_flops = l_b * (2 * cfg.d_in * cfg.d_hidden + 2 * cfg.d_hidden * cfg.hq)
+    sel_bytes = 4 * cfg.hk * l_b + 4 * cfg.hk * lpp + 2 * slot
+    recv = (H - len(hosts)) * slot if world > 1 else 0
+    out = {}
+    for name, h, a, b in tr:
+        e = out.setdefault(name, {"ms_per_step": 0.0, "launches": 0, "lower_bound_ms": 0.0})
+        e["ms_per_step"] += a.elapsed_time(b)
+        e["launches"] += 1
+        if name == "score":
+            e["lower_bound_ms"] += score_flops / tf * 1e3
+        elif name == "select_compact":
+            e["lower_bound_ms"] += sel_bytes / hbm * 1e3
+        elif name == "exchange":
+            e["lower_bound_ms"] += recv / (NVLINK_GBS * 1e9) * 1e3
+        else:
+            L_A = 0 if h == 0 else cfg.l_q + cfg.l_a
+            f_all = workload.attention_flops(cfg.n, H, h, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q)
+            f_pass = 4 * cfg.d * cfg.hq * l_b * h * lpp
+            f = {"attn_all": f_all, "attn_local": f_all - f_pass, "attn_passing": f_pass}[name]
+            e["lower_bound_ms"] += f / tf * 1e3
+    for name, e in out.items():
+        e["us_per_launch"] = round(1e3 * e["ms_per_step"] / max(e["launches"], 1), 2)
+        e["frac_of_bound"] = round(e["lower_bound_ms"] / e["ms_per_step"], 4) if e["ms_per_step"] > 0 else None
+        e["ms_per_step"] = round(e["ms_per_step"], 3)
+        e["lower_bound_ms"] = round(e["lower_bound_ms"], 4)
+    out["bounds"] = {"score": "tensor (sustained bf16)", "select_compact": "HBM (scores + indices + 2x payload)",
+                     "exchange": f"NVLink {NVLINK_GBS:.0f} GB/s per direction, received bytes"
+                                 + ("" if world > 1 else " (N = 1: no exchange, the slots are written in place)"),
+                     "attn_*": "tensor (sustained bf16), useful mask-counted FLOPs"}
+    if world > 1 and "exchange" in out and out["exchange"]["ms_per_step"] > 0:
+        out["exchange"]["nvlink_frac"] = round(recv * layers / (out["exchange"]["ms_per_step"] / 1e3)
+                                               / (NVLINK_GBS * 1e9), 4)
+    return out
 
 
 def run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank, barrier):

@@ -189,6 +189,32 @@ apb_status apb_exchange_passing(apb_comm* comm, const apb_dims* dims, void* gath
 apb_status apb_exchange_passing_cyclic(apb_comm* comm, const apb_dims* dims, void* gathered,
                                        apb_stream_t stream);
 
+/* Host ownership of a multi-rank run: BLOCK = rank r owns hosts
+ * [r*H/N, (r+1)*H/N); CYCLIC = rank r owns hosts r, r+N, r+2N, ...                        */
+typedef enum { APB_LAYOUT_BLOCK = 0, APB_LAYOUT_CYCLIC = 1 } apb_host_layout;
+
+/* The exchange plan (host-only, no GPU needed): the in-place AllGather rounds that
+ * apb_exchange_passing (BLOCK) / apb_exchange_passing_cyclic (CYCLIC) enqueue for rank `rank`
+ * of `nranks`.  Round i gathers count[i] bf16 ELEMENTS per rank: this rank's payload is
+ * gathered[send_offset[i] .. + count[i]) and the round fills gathered[recv_offset[i] ..
+ * + nranks*count[i]) with rank r's payload at recv_offset[i] + r*count[i].  The arrays are
+ * caller-owned with max_rounds entries (H/nranks always suffices); *n_rounds gets the number of
+ * rounds (0 when nranks == 1 or l_p' == 0: nothing to exchange).  Errors: APB_ERR_CONFIG for
+ * bad dims / nranks not dividing H / unknown layout; APB_ERR_CONTRACT for NULL arrays or
+ * max_rounds too small.  P:194-197.                                            */
+apb_status apb_exchange_plan(const apb_dims* dims, int32_t nranks, int32_t rank, apb_host_layout layout,
+                             int32_t max_rounds, int64_t* send_offset, int64_t* recv_offset, int64_t* count,
+                             int32_t* n_rounds);
+
+/* Polls the communicator for an asynchronous NCCL error (ncclCommGetAsyncError): a failure of
+ * an already-enqueued collective (peer lost, network error) surfaces here as APB_ERR_NCCL with
+ * the NCCL message in apb_last_error().  apb_exchange_passing{,_cyclic} poll before and after
+ * they enqueue.  APB_OK for a NULL or 1-rank comm.                                          */
+apb_status apb_comm_check(apb_comm* comm);
+/* Aborts (ncclCommAbort: does not wait for pending collectives) and frees the comm — the
+ * recovery path after apb_comm_check reported an error.                                   */
+apb_status apb_comm_abort(apb_comm* comm);
+
 /* ---------------------------------------------------------------- step 4: masked attention
  * eq:apb: for query head qh and query row r in [0, L_A + l_b), with the key
  * sequence [anchor rows of k | passing P_h | block rows of k] (passing = slots 0..host-1 of
@@ -279,6 +305,13 @@ apb_status apb_merge_partials(int32_t n_parts, int64_t rows, int32_t head_dim, c
 /* Gather of the partials: in-place AllGather of fp32 buffer [nranks][count_per_rank]
  * (rank r owns block r).  No-op for comm == NULL or a 1-rank comm.                             */
 apb_status apb_exchange_partials(apb_comm* comm, int64_t count_per_rank, float* buf, apb_stream_t stream);
+
+/* The same Gather for CYCLIC host ownership (rank r owns hosts r, r+N, ...): buf is fp32
+ * [H][slot_count], host h's partial in slot h; H/N in-place AllGather rounds, round k gathering
+ * slots [k*N, (k+1)*N) (one per rank), so every slot ends in host order on every rank.  No-op
+ * for comm == NULL or a 1-rank comm; APB_ERR_CONFIG unless nranks divides H.                */
+apb_status apb_exchange_partials_cyclic(apb_comm* comm, int32_t H, int64_t slot_count, float* buf,
+                                        apb_stream_t stream);
 
 /* ---------------------------------------------------------------- plumbing */
 apb_status apb_workspace_size(const apb_dims* dims, apb_ws_kind which, size_t* bytes);

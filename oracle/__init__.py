@@ -70,6 +70,8 @@ def _load():
                       lib.oracle_decode_partial, lib.oracle_merge_score, lib.oracle_random_scores):
                 f.restype = ctypes.c_int
             lib.oracle_num_threads.restype = ctypes.c_int
+            lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+            lib.oracle_set_num_threads.restype = None
             _lib = lib
     return _lib
 
@@ -80,6 +82,11 @@ def _p(a, t=ctypes.c_double):
 
 def num_threads() -> int:
     return int(_load().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the C oracle (timing legs only; results do not depend on it)."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def _as_f64(x):

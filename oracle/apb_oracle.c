@@ -195,6 +195,17 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count for the timing legs (bench.py cpu_baseline reports a single-thread rate too);
+ * the arithmetic does not depend on it (each output is computed by one thread, fixed order). */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+
 /* ------------------------------------------------------------------ decode (NEXT #1) */
 /* Alg. apb_decode: the t new tokens' queries attend on host h to its block KV cache
  * (P:745-746); the last host also attends to the new tokens' own keys, causally among

@@ -22,6 +22,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libapb.so")
 
 OK, ERR_CONFIG, ERR_CONTRACT, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL = range(6)
+LAYOUT_BLOCK, LAYOUT_CYCLIC = 0, 1
 PHASE_ALL, PHASE_LOCAL, PHASE_PASSING = 0, 1, 2
 WS_RETAIN, WS_SELECT, WS_ATTENTION = 0, 1, 2
 
@@ -30,7 +31,8 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_check_dims", "apb_status_string", "apb_last_error", "apb_version", "apb_launch_count",
             "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
             "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic",
-            "apb_decode_step_hosts")
+            "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check", "apb_comm_abort",
+            "apb_exchange_partials_cyclic")
 
 
 class ApbError(RuntimeError):
@@ -96,11 +98,17 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_swiglu.argtypes = [i64, i32, vp, i64, vp, i64, vp]
     lib.apb_gemm_bf16.argtypes = [i64, i32, i32, vp, i64, vp, i64, vp, i64, ctypes.c_float, vp, sz, vp]
     lib.apb_share_scores.argtypes = [dp, vp, vp]
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    lib.apb_exchange_plan.argtypes = [dp, i32, i32, ctypes.c_int, i32, i64p, i64p, i64p, ctypes.POINTER(i32)]
+    lib.apb_comm_check.argtypes = [vp]
+    lib.apb_comm_abort.argtypes = [vp]
+    lib.apb_exchange_partials_cyclic.argtypes = [vp, i32, i64, vp, vp]
     for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size",
-              "apb_exchange_passing_cyclic", "apb_decode_step_hosts"):
+              "apb_exchange_passing_cyclic", "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check",
+              "apb_comm_abort", "apb_exchange_partials_cyclic"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -194,6 +202,45 @@ def _rowstride(t: torch.Tensor, name: str) -> int:
     return t.stride(0)
 
 
+def _need(t, name: str, dtype, min_rows: int | None = None, width: int | None = None, dense: bool = False):
+    """Validate what the C ABI cannot see from a pointer: device, dtype, and that the tensor
+    covers the rows / row width (elements) the call will read or write from `dims`."""
+    if t is None:
+        raise ApbError(ERR_CONTRACT, name, "is None")
+    if not t.is_cuda:
+        raise ApbError(ERR_CONTRACT, name, "must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ApbError(ERR_CONTRACT, name, f"dtype must be {dtype}, got {t.dtype}")
+    if dense and not t.is_contiguous():
+        raise ApbError(ERR_CONTRACT, name, "must be contiguous")
+    if min_rows is not None and (t.dim() == 0 or t.shape[0] < min_rows):
+        raise ApbError(ERR_CONTRACT, name, f"needs >= {min_rows} rows, has {tuple(t.shape)}")
+    if width is not None:
+        w = t[0].numel() if t.dim() >= 2 else t.numel()
+        if w < width:
+            raise ApbError(ERR_CONTRACT, name, f"rows must hold >= {width} elements, have {w}")
+
+
+def _need_numel(t, name: str, dtype, numel: int):
+    _need(t, name, dtype, dense=True)
+    if t.numel() < numel:
+        raise ApbError(ERR_CONTRACT, name, f"needs >= {numel} elements, has {t.numel()}")
+
+
+def _check_qkv(dims: "Dims", q, k, v) -> int:
+    """q [rows][hq][d], k/v [rows][hk][d] bf16 with one shared K/V row stride (the ABI takes
+    one kv_row_stride for both).  Returns that stride."""
+    rows = dims.rows
+    _need(q, "q", torch.bfloat16, rows, dims.n_heads * dims.head_dim)
+    _need(k, "k", torch.bfloat16, rows, dims.n_kv_heads * dims.head_dim)
+    _need(v, "v", torch.bfloat16, rows, dims.n_kv_heads * dims.head_dim)
+    ks, vs = _rowstride(k, "k"), _rowstride(v, "v")
+    if ks != vs:
+        raise ApbError(ERR_CONTRACT, "k/v", f"K and V must share one row stride ({ks} != {vs})")
+    _rowstride(q, "q")
+    return ks
+
+
 def _stream(stream) -> int | None:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -219,6 +266,15 @@ def check_dims(dims: Dims) -> None:
 
 
 def retain_score(dims: Dims, w: RetainWeights, q, k, v, scores, stream=None) -> None:
+    _check_qkv(dims, q, k, v)
+    _need_numel(scores, "scores", torch.float32, dims.n_kv_heads * dims.l_b)
+    _need(w.w1, "w1", torch.bfloat16, dense=True)
+    _need(w.w2, "w2", torch.float32, dense=True)
+    for b, nm in ((w.b1, "b1"), (w.b2, "b2")):
+        if b is not None:
+            _need(b, nm, torch.float32, dense=True)
+    if w.w2.dim() != 2 or w.w2.shape[1] != w.w1.shape[0]:
+        raise ApbError(ERR_CONTRACT, "w2", "must be [n_out][d_hidden]")
     d, wc = dims.c(), w.c()
     _check(load().apb_retain_score(ctypes.byref(d), ctypes.byref(wc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                    _rowstride(q, "q"), _rowstride(k, "k"), scores.data_ptr(), None, 0,
@@ -226,6 +282,14 @@ def retain_score(dims: Dims, w: RetainWeights, q, k, v, scores, stream=None) -> 
 
 
 def select_topk(dims: Dims, scores, k, v, indices, send, stream=None) -> None:
+    _need_numel(scores, "scores", torch.float32, dims.n_kv_heads * dims.l_b)
+    if dims.l_pp > 0:
+        _need(k, "k", torch.bfloat16, dims.rows, dims.n_kv_heads * dims.head_dim)
+        _need(v, "v", torch.bfloat16, dims.rows, dims.n_kv_heads * dims.head_dim)
+        if _rowstride(k, "k") != _rowstride(v, "v"):
+            raise ApbError(ERR_CONTRACT, "k/v", "K and V must share one row stride")
+        _need_numel(indices, "indices", torch.int32, dims.n_kv_heads * dims.l_pp)
+        _need_numel(send, "send", torch.bfloat16, 2 * dims.n_kv_heads * dims.l_pp * dims.head_dim)
     d = dims.c()
     _check(load().apb_select_topk(ctypes.byref(d), scores.data_ptr(), k.data_ptr(), v.data_ptr(),
                                   _rowstride(k, "k"), indices.data_ptr(), send.data_ptr(), None, 0,
@@ -234,6 +298,7 @@ def select_topk(dims: Dims, scores, k, v, indices, send, stream=None) -> None:
 
 def random_scores(dims: Dims, seed: int, layer: int, scores, stream=None) -> None:
     """The "Rd." compressor (Table 4): scores [n_kv_heads][l_b] fp32 <- seeded uniform [0,1)."""
+    _need_numel(scores, "scores", torch.float32, dims.n_kv_heads * dims.l_b)
     d = dims.c()
     _check(load().apb_random_scores(ctypes.byref(d), seed % (1 << 64), layer, scores.data_ptr(), _stream(stream)),
            "apb_random_scores")
@@ -241,12 +306,23 @@ def random_scores(dims: Dims, seed: int, layer: int, scores, stream=None) -> Non
 
 def share_scores(dims: Dims, scores, stream=None) -> None:
     """Shared index set: scores rows <- max over KV heads, in place."""
+    _need_numel(scores, "scores", torch.float32, dims.n_kv_heads * dims.l_b)
     d = dims.c()
     _check(load().apb_share_scores(ctypes.byref(d), scores.data_ptr(), _stream(stream)), "apb_share_scores")
 
 
 def attention_fwd(dims: Dims, q, k, v, gathered, out, lse=None, phase: int = PHASE_ALL, ws=None,
                   stream=None) -> None:
+    _check_qkv(dims, q, k, v)
+    _need(out, "out", torch.bfloat16, dims.rows, dims.n_heads * dims.head_dim)
+    if lse is not None:
+        _need(lse, "lse", torch.float32, dims.n_heads, dims.rows, dense=True)
+        if lse.dim() != 2 or lse.shape[1] != dims.rows:
+            raise ApbError(ERR_CONTRACT, "lse", f"must be [n_heads][{dims.rows}]")
+    if gathered is not None and dims.P > 0 and phase != PHASE_LOCAL:
+        _need_numel(gathered, "gathered", torch.bfloat16, dims.H * 2 * dims.n_kv_heads * dims.l_pp * dims.head_dim)
+    if ws is not None:
+        _need(ws, "ws", ws.dtype, dense=True)
     d = dims.c()
     _check(load().apb_attention_fwd(ctypes.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), _rowstride(q, "q"),
                                     _rowstride(k, "k"), _ptr(gathered), out.data_ptr(), _rowstride(out, "out"),
@@ -301,6 +377,16 @@ class Comm:
     def handle(self):
         return self._h
 
+    def check(self) -> None:
+        """Raise ApbError(ERR_NCCL) if an enqueued collective failed asynchronously."""
+        _check(load().apb_comm_check(self._h), "apb_comm_check")
+
+    def abort(self) -> None:
+        """ncclCommAbort + free (recovery after an asynchronous error)."""
+        if self._h:
+            h, self._h = self._h, ctypes.c_void_p()
+            _check(load().apb_comm_abort(h), "apb_comm_abort")
+
     def close(self) -> None:
         if self._h:
             _check(load().apb_comm_destroy(self._h), "apb_comm_destroy")
@@ -309,10 +395,24 @@ class Comm:
 
 def exchange_passing(comm: Comm | None, dims: Dims, gathered, stream=None, cyclic: bool = False) -> None:
     """cyclic: rank r owns hosts r, r+N, ... (apb_exchange_passing_cyclic), else contiguous blocks."""
+    if comm is not None and comm.nranks > 1 and dims.l_pp > 0:
+        _need_numel(gathered, "gathered", torch.bfloat16, dims.H * 2 * dims.n_kv_heads * dims.l_pp * dims.head_dim)
     d = dims.c()
     fn = "apb_exchange_passing_cyclic" if cyclic else "apb_exchange_passing"
     _check(getattr(load(), fn)(comm.handle if comm is not None else None, ctypes.byref(d),
                                gathered.data_ptr(), _stream(stream)), fn)
+
+
+def exchange_plan(dims: Dims, nranks: int, rank: int, layout: int = LAYOUT_BLOCK) -> list[tuple[int, int, int]]:
+    """apb_exchange_plan: the in-place AllGather rounds of apb_exchange_passing{,_cyclic} for
+    `rank` of `nranks`, as (send_offset, recv_offset, count) in bf16 elements of gathered."""
+    n = max(dims.H, 1)
+    so, ro, ct = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+    rounds = ctypes.c_int32(0)
+    d = dims.c()
+    _check(load().apb_exchange_plan(ctypes.byref(d), nranks, rank, layout, n, so, ro, ct, ctypes.byref(rounds)),
+           "apb_exchange_plan")
+    return [(so[i], ro[i], ct[i]) for i in range(rounds.value)]
 
 
 def launch_count() -> int:
@@ -428,3 +528,9 @@ def exchange_partials(comm: "Comm | None", count_per_rank: int, buf, stream=None
     """Gather: in-place AllGather of fp32 [nranks][count_per_rank]."""
     _check(load().apb_exchange_partials(comm.handle if comm is not None else None, count_per_rank,
                                         buf.data_ptr(), _stream(stream)), "apb_exchange_partials")
+
+
+def exchange_partials_cyclic(comm: "Comm | None", H: int, slot_count: int, buf, stream=None) -> None:
+    """Gather for cyclic ownership: buf fp32 [H][slot_count], host h in slot h."""
+    _check(load().apb_exchange_partials_cyclic(comm.handle if comm is not None else None, H, slot_count,
+                                               buf.data_ptr(), _stream(stream)), "apb_exchange_partials_cyclic")

@@ -1,8 +1,10 @@
 """Build libapb.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with the repo)."""
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
+import shutil
 import subprocess
 import sys
 
@@ -11,7 +13,8 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libapb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default", "-shared"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default"]
+LIBS = ["-ldl", "-lcublasLt"]
 
 
 def sources() -> list[str]:
@@ -33,14 +36,24 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     if not force and not trace and not _stale():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-ldl", "-lcublasLt"]
-    if trace:
-        cmd.insert(1, "-DAPB_TRACE")
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = os.path.join(ROOT, "build", ("trace" if trace else "release") + f".{os.getpid()}")
+    os.makedirs(objdir, exist_ok=True)
+    extra = (["-DAPB_TRACE"] if trace else []) + (["-Xptxas=-v"] if verbose else [])
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        return obj
+
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, *LIBS])
     os.replace(tmp, lib)
+    shutil.rmtree(objdir, ignore_errors=True)
     return lib
 
 

@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -418,6 +419,8 @@ struct NcclApi {
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
 };
 NcclApi* nccl() {
   static NcclApi api;
@@ -432,6 +435,8 @@ NcclApi* nccl() {
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
     api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.commGetAsyncError = reinterpret_cast<decltype(api.commGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+    api.commAbort = reinterpret_cast<decltype(api.commAbort)>(dlsym(h, "ncclCommAbort"));
     if (api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather) api.h = h;
   });
   return api.h ? &api : nullptr;
@@ -490,45 +495,110 @@ extern "C" apb_status apb_comm_destroy(apb_comm* c) {
   return st;
 }
 
-extern "C" apb_status apb_exchange_passing(apb_comm* c, const apb_dims* d, void* gathered, apb_stream_t stream) {
+// The exchange plan: the in-place AllGather rounds for rank `rank` of `nranks` (element offsets
+// into gathered [H][2][hk][l_p'][d]).  BLOCK ownership is one round over contiguous per-rank slot
+// ranges; CYCLIC ownership is H/N rounds, round k gathering slots [k*N, (k+1)*N) one per rank.
+// apb_exchange_passing{,_cyclic} enqueue exactly these rounds (the CPU multi-rank tests drive
+// their gloo all-gathers from the same function).
+static apb_status exchange_plan(const apb_dims* d, int32_t nranks, int32_t rank, int32_t layout, int32_t max_rounds,
+                                int64_t* send_off, int64_t* recv_off, int64_t* count, int32_t* n_rounds) {
+  apb_status st = check_dims(d);
+  if (st) return st;
+  if (!n_rounds) return fail(APB_ERR_CONTRACT, "n_rounds is NULL");
+  *n_rounds = 0;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(APB_ERR_CONFIG, "bad nranks/rank");
+  if (d->H % nranks) return fail(APB_ERR_CONFIG, "comm nranks must divide H");
+  if (layout != APB_LAYOUT_BLOCK && layout != APB_LAYOUT_CYCLIC) return fail(APB_ERR_CONFIG, "unknown host layout");
+  const int64_t lpp = lpp_of(d);
+  if (nranks == 1 || lpp == 0) return APB_OK;  // nothing to exchange
+  const int64_t slot = (int64_t)2 * d->n_kv_heads * lpp * d->head_dim;  // bf16 elements per host slot
+  const int32_t rounds = layout == APB_LAYOUT_BLOCK ? 1 : d->H / nranks;
+  if (max_rounds < rounds) return fail(APB_ERR_CONTRACT, "plan arrays hold fewer than H/nranks rounds");
+  if (!send_off || !recv_off || !count) return fail(APB_ERR_CONTRACT, "plan arrays are NULL");
+  if (layout == APB_LAYOUT_BLOCK) {
+    count[0] = slot * (d->H / nranks);
+    recv_off[0] = 0;
+    send_off[0] = (int64_t)rank * count[0];
+  } else {
+    for (int32_t k = 0; k < rounds; ++k) {
+      count[k] = slot;
+      recv_off[k] = (int64_t)k * nranks * slot;
+      send_off[k] = recv_off[k] + (int64_t)rank * slot;
+    }
+  }
+  *n_rounds = rounds;
+  return APB_OK;
+}
+
+extern "C" apb_status apb_exchange_plan(const apb_dims* d, int32_t nranks, int32_t rank, apb_host_layout layout,
+                                        int32_t max_rounds, int64_t* send_offset, int64_t* recv_offset,
+                                        int64_t* count, int32_t* n_rounds) {
+  return exchange_plan(d, nranks, rank, layout, max_rounds, send_offset, recv_offset, count, n_rounds);
+}
+
+// Poll the communicator for an asynchronous NCCL failure (a peer died, a network error): such
+// errors surface only here, never as a return code of the enqueueing call.
+static apb_status comm_async_check(NcclApi* api, apb_comm* c) {
+  if (!c || !c->comm || !api->commGetAsyncError) return APB_OK;
+  ncclResult_t async = ncclSuccess;
+  ncclResult_t r = api->commGetAsyncError(c->comm, &async);
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclCommGetAsyncError");
+  if (async != ncclSuccess && async != ncclInProgress) return nccl_fail(api, async, "NCCL asynchronous error");
+  return APB_OK;
+}
+
+extern "C" apb_status apb_comm_check(apb_comm* c) {
+  if (!c || !c->comm) return APB_OK;
+  NcclApi* api = nccl();
+  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+  return comm_async_check(api, c);
+}
+
+extern "C" apb_status apb_comm_abort(apb_comm* c) {
+  if (!c) return APB_OK;
+  apb_status st = APB_OK;
+  if (c->comm) {
+    NcclApi* api = nccl();
+    if (api && api->commAbort) {
+      ncclResult_t r = api->commAbort(c->comm);
+      if (r != ncclSuccess) st = nccl_fail(api, r, "ncclCommAbort");
+    }
+  }
+  delete c;
+  return st;
+}
+
+static apb_status exchange_impl(apb_comm* c, const apb_dims* d, int32_t layout, void* gathered, apb_stream_t stream) {
   apb_status st = check_dims(d);
   if (st) return st;
   if (!c || c->nranks == 1) return APB_OK;
-  const int64_t lpp = lpp_of(d);
-  if (lpp == 0) return APB_OK;
+  const int32_t max_rounds = d->H;
+  std::vector<int64_t> send_off(max_rounds), recv_off(max_rounds), count(max_rounds);
+  int32_t rounds = 0;
+  if ((st = exchange_plan(d, c->nranks, c->rank, layout, max_rounds, send_off.data(), recv_off.data(), count.data(),
+                          &rounds)))
+    return st;
+  if (rounds == 0) return APB_OK;
   if (!gathered || !aligned16(gathered)) return fail(APB_ERR_CONTRACT, "gathered NULL or misaligned");
-  if (d->H % c->nranks) return fail(APB_ERR_CONFIG, "comm nranks must divide H");
   NcclApi* api = nccl();
   if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
-  const size_t slot = (size_t)2 * d->n_kv_heads * lpp * d->head_dim;  // bf16 elements per host slot
-  const size_t count = slot * (d->H / c->nranks);                         // elements per rank
+  if ((st = comm_async_check(api, c))) return st;
   char* base = static_cast<char*>(gathered);
-  ncclResult_t r = api->allGather(base + (size_t)c->rank * count * 2, base, count, ncclBfloat16, c->comm,
-                                  reinterpret_cast<cudaStream_t>(stream));
-  if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather");
-  return APB_OK;
+  for (int32_t k = 0; k < rounds; ++k) {
+    ncclResult_t r = api->allGather(base + send_off[k] * 2, base + recv_off[k] * 2, (size_t)count[k], ncclBfloat16,
+                                    c->comm, reinterpret_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return nccl_fail(api, r, layout == APB_LAYOUT_BLOCK ? "ncclAllGather" : "ncclAllGather (cyclic round)");
+  }
+  return comm_async_check(api, c);
+}
+
+extern "C" apb_status apb_exchange_passing(apb_comm* c, const apb_dims* d, void* gathered, apb_stream_t stream) {
+  return exchange_impl(c, d, APB_LAYOUT_BLOCK, gathered, stream);
 }
 
 extern "C" apb_status apb_exchange_passing_cyclic(apb_comm* c, const apb_dims* d, void* gathered,
                                                   apb_stream_t stream) {
-  apb_status st = check_dims(d);
-  if (st) return st;
-  if (!c || c->nranks == 1) return APB_OK;
-  const int64_t lpp = lpp_of(d);
-  if (lpp == 0) return APB_OK;
-  if (!gathered || !aligned16(gathered)) return fail(APB_ERR_CONTRACT, "gathered NULL or misaligned");
-  if (d->H % c->nranks) return fail(APB_ERR_CONFIG, "comm nranks must divide H");
-  NcclApi* api = nccl();
-  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
-  const size_t slot = (size_t)2 * d->n_kv_heads * lpp * d->head_dim;  // bf16 elements per host slot
-  char* base = static_cast<char*>(gathered);
-  for (int k = 0; k < d->H / c->nranks; ++k) {  // round k: hosts k*N .. k*N+N-1, one per rank
-    char* round = base + (size_t)k * c->nranks * slot * 2;
-    ncclResult_t r = api->allGather(round + (size_t)c->rank * slot * 2, round, slot, ncclBfloat16, c->comm,
-                                    reinterpret_cast<cudaStream_t>(stream));
-    if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather (cyclic round)");
-  }
-  return APB_OK;
+  return exchange_impl(c, d, APB_LAYOUT_CYCLIC, gathered, stream);
 }
 
 // ---------------------------------------------------------------- decode step (NEXT #1)
@@ -727,4 +797,22 @@ extern "C" apb_status apb_exchange_partials(apb_comm* c, int64_t count_per_rank,
                                   c->comm, reinterpret_cast<cudaStream_t>(stream));
   if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather (partials)");
   return APB_OK;
+}
+
+extern "C" apb_status apb_exchange_partials_cyclic(apb_comm* c, int32_t H, int64_t slot_count, float* buf,
+                                                   apb_stream_t stream) {
+  if (!c || c->nranks == 1 || slot_count == 0) return APB_OK;
+  if (slot_count < 0 || H < 1 || H % c->nranks) return fail(APB_ERR_CONFIG, "slot_count >= 0 and nranks | H required");
+  if (!buf || !aligned16(buf)) return fail(APB_ERR_CONTRACT, "buf NULL or misaligned");
+  NcclApi* api = nccl();
+  if (!api) return fail(APB_ERR_NCCL, "libnccl.so.2 not found");
+  apb_status st = comm_async_check(api, c);
+  if (st) return st;
+  for (int32_t k = 0; k < H / c->nranks; ++k) {  // round k: slots k*N .. k*N+N-1, one per rank
+    float* round = buf + (size_t)k * c->nranks * slot_count;
+    ncclResult_t r = api->allGather(round + (size_t)c->rank * slot_count, round, (size_t)slot_count, ncclFloat32,
+                                    c->comm, reinterpret_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather (partials, cyclic round)");
+  }
+  return comm_async_check(api, c);
 }

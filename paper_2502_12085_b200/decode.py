@@ -25,6 +25,13 @@ class DecodeRank:
         self.H, self.hosts, self.t = H, list(hosts), t_new
         self.hq, self.hk, self.d = n_heads, n_kv_heads, head_dim
         self.comm, self.scale, self.batch_hosts, self.fuse_merge = comm, softmax_scale, batch_hosts, fuse_merge
+        nr = comm.nranks if comm is not None else 1
+        self.contiguous = self.hosts == list(range(self.hosts[0], self.hosts[0] + len(self.hosts)))
+        self.cyclic = nr > 1 and not self.contiguous
+        if self.cyclic and self.hosts != list(range(self.hosts[0], H, nr)):
+            raise ValueError("owned hosts must be a contiguous block or the cyclic set r, r+N, ...")
+        if nr == 1 and sorted(self.hosts) != list(range(H)):
+            raise ValueError("a single rank must own every host")
         self.device = torch.device(device)
         self.rows = t_new * n_heads
         # floats per host: O [rows][d] then lse [rows], padded to 16 B so every slot stays aligned
@@ -49,7 +56,7 @@ class DecodeRank:
                 self.ws["batch"] = torch.zeros(max(n, 16), dtype=torch.uint8, device=self.device)
             apb.decode_step_hosts(d, q, kcs, vcs, k_new, v_new, out, out_lse, self.ws["batch"], stream=stream)
             return
-        if len(self.hosts) > 1 and self.batch_hosts:
+        if len(self.hosts) > 1 and self.batch_hosts and self.contiguous:
             # every owned host's partial in one streaming launch + one fold (same partials up to
             # the split plan's fp32 summation order)
             h0 = self.hosts[0]
@@ -73,7 +80,10 @@ class DecodeRank:
                 apb.decode_attention(d, q, kc, vc, k_new if h == self.H - 1 else None,
                                      v_new if h == self.H - 1 else None, slot[: self.rows * self.d],
                                      slot[self.rows * self.d:], self.ws[h], stream=stream)
-        per_rank = self.slot * (self.H // (self.comm.nranks if self.comm else 1))
-        apb.exchange_partials(self.comm, per_rank, self.parts, stream=stream)
+        if self.cyclic:  # host h's partial sits in slot h; H/N rounds of one slot per rank
+            apb.exchange_partials_cyclic(self.comm, self.H, self.slot, self.parts, stream=stream)
+        else:
+            per_rank = self.slot * (self.H // (self.comm.nranks if self.comm else 1))
+            apb.exchange_partials(self.comm, per_rank, self.parts, stream=stream)
         apb.merge_partials(self.H, self.rows, self.d, self.parts, self.slot, self.parts[:, self.rows * self.d:],
                            self.slot, out, out_lse, stream=stream)

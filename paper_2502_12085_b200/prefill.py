@@ -41,7 +41,7 @@ class PrefillRank:
     def __init__(self, base: apb.Dims, hosts: list[int], comm: apb.Comm | None = None,
                  device: torch.device | str = "cuda", skip_unused_last: bool = False,
                  split_phases: bool | None = None, compressor: str = "retain", shared_set: bool = False,
-                 seed: int = 0):
+                 seed: int = 0, same_device: bool = False):
         """base: problem dims (its `host` field is ignored); hosts: host indices this rank owns
         (contiguous, in order).  skip_unused_last: do not score/select host H-1 — its
         compressed block is ignored by every host, so outputs are unchanged.
@@ -49,7 +49,10 @@ class PrefillRank:
         communicator is given; a single rank uses one ordered APB_PHASE_ALL launch per host).
         compressor: "retain" (retaining heads R) or "random" (the "Rd." selector of
         Table 4, seeded by `seed` and the layer index); shared_set: one index set per host, the
-        max over KV heads instead of per-KV-head sets (reading G3)."""
+        max over KV heads instead of per-KV-head sets (reading G3).
+        same_device: debug only — allow owning a strict subset of the hosts WITHOUT a multi-rank
+        communicator (the passing slots of hosts owned elsewhere are then never filled, so the
+        outputs are not APB's; used to exercise the N > 1 schedule on one GPU)."""
         if compressor not in ("retain", "random"):
             raise ValueError(f"compressor must be 'retain' or 'random', not {compressor!r}")
         self.compressor, self.shared_set, self.seed = compressor, shared_set, seed
@@ -58,6 +61,15 @@ class PrefillRank:
         self.skip_unused_last = skip_unused_last
         self.split_phases = (comm is not None and comm.nranks > 1) if split_phases is None else split_phases
         nr = comm.nranks if comm is not None else 1
+        if nr > 1 and not self.split_phases:
+            # the ordered one-pass schedule waits only on this rank's own slot events, never on
+            # the AllGather that fills the other ranks' slots: it is a single-rank schedule
+            raise ValueError("split_phases=False (the ordered schedule) needs a single rank; "
+                             "a multi-rank communicator requires the LOCAL/PASSING split")
+        if nr == 1 and sorted(self.hosts) != list(range(base.H)) and not same_device:
+            raise ValueError(f"hosts {self.hosts} are a strict subset of range(H={base.H}) but there is no "
+                             "multi-rank communicator to fill the other hosts' passing slots")
+        self.same_device = same_device
         self.cyclic = nr > 1 and nr < base.H and self.hosts == list(range(self.hosts[0], base.H, nr))
         if nr > 1 and not self.cyclic and self.hosts != list(range(self.hosts[0], self.hosts[0] + len(self.hosts))):
             raise ValueError("owned hosts must be a contiguous block or the cyclic set r, r+N, ...")
@@ -73,22 +85,38 @@ class PrefillRank:
         # high priority: the side stream's scoring / selection / NCCL CTAs are scheduled ahead of
         # the main stream's queued attention CTAs, so the exchange completes while LOCAL runs
         self.side = torch.cuda.Stream(device=self.device, priority=-1)
+        # per-op timing (bench breakdown): a list receives (op, host, start, end) CUDA-event
+        # tuples recorded on the stream each op is launched on; None = no events
+        self.trace: list | None = None
         self.ev_exchanged = torch.cuda.Event()
         self.ev_slot = {h: torch.cuda.Event() for h in hosts}
 
     def dims(self, h: int) -> apb.Dims:
         return self.base.with_host(h)
 
+    def _op(self, name: str, h: int, stream, fn) -> None:
+        if self.trace is None:
+            return fn()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        self.trace.append((name, h, a, b))
+
     def _compress_host(self, h: int, io: dict[int, HostIO], weights, layer_idx: int, stream) -> None:
         """Steps 1-2 for host h: scores (compressor) -> top-l_p indices -> gathered[h] (in place)."""
         d, x = self.dims(h), io[h]
         if self.compressor == "random":
-            apb.random_scores(d, self.seed, layer_idx, self.scores[h], stream=stream)
+            self._op("score", h, stream, lambda: apb.random_scores(d, self.seed, layer_idx, self.scores[h],
+                                                                   stream=stream))
         else:
-            apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h], stream=stream)
+            self._op("score", h, stream, lambda: apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h],
+                                                                  stream=stream))
         if self.shared_set:
             apb.share_scores(d, self.scores[h], stream=stream)
-        apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h], self.gathered[h], stream=stream)
+        self._op("select_compact", h, stream, lambda: apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h],
+                                                                      self.gathered[h], stream=stream))
 
     def _compresses(self, h: int) -> bool:
         return self.base.l_pp > 0 and not (self.skip_unused_last and h == self.base.H - 1)
@@ -102,13 +130,15 @@ class PrefillRank:
 
     def exchange(self, stream=None) -> None:
         """Step 3: in-place AllGather(s) of the packed [2][hk][l_p'][d] slots."""
-        apb.exchange_passing(self.comm, self.base, self.gathered, stream=stream, cyclic=self.cyclic)
+        self._op("exchange", -1, stream, lambda: apb.exchange_passing(self.comm, self.base, self.gathered,
+                                                                      stream=stream, cyclic=self.cyclic))
 
     def attention(self, io: dict[int, HostIO], phase: int, stream=None) -> None:
+        name = {apb.PHASE_ALL: "attn_all", apb.PHASE_LOCAL: "attn_local", apb.PHASE_PASSING: "attn_passing"}[phase]
         for h in self.hosts:
             x = io[h]
-            apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse, phase=phase,
-                              ws=self.ws[h], stream=stream)
+            self._op(name, h, stream, lambda: apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out,
+                                                                x.lse, phase=phase, ws=self.ws[h], stream=stream))
 
     def layer(self, io: dict[int, HostIO], weights: apb.RetainWeights | None, overlap: bool = True,
               events: list | None = None, layer_idx: int = 0) -> None:
@@ -145,8 +175,9 @@ class PrefillRank:
                 if h > self.hosts[0]:
                     main.wait_event(self.ev_slot[h - 1])
                 x = io[h]
-                timed(lambda: apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse,
-                                                phase=apb.PHASE_ALL, ws=self.ws[h], stream=main))
+                timed(lambda: self._op("attn_all", h, main, lambda: apb.attention_fwd(
+                    self.dims(h), x.q, x.k, x.v, self.gathered, x.out, x.lse, phase=apb.PHASE_ALL, ws=self.ws[h],
+                    stream=main)))
             main.wait_stream(self.side)  # the last host's compression still reads io[h].k/v
             return
         self.side.wait_stream(main)  # this layer's inputs are produced on the main stream

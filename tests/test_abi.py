@@ -100,14 +100,23 @@ def test_workspace_sizes(lib):
 class _FakeT:
     """Stands in for a device tensor: only data_ptr / stride / shape are read by the binding."""
 
-    def __init__(self, ptr, shape, elem=2):
+    is_cuda = True
+
+    def __init__(self, ptr, shape, elem=2, dtype=None, strides=None):
         self._p, self.shape = ptr, shape
         st, s = [], 1
         for x in reversed(shape):
             st.append(s)
             s *= x
-        self._st = tuple(reversed(st))
+        self._st = tuple(strides) if strides is not None else tuple(reversed(st))
         self._e = elem
+        self.dtype = dtype or {2: torch.bfloat16, 4: torch.float32}[elem]
+
+    def is_contiguous(self):
+        return True
+
+    def __getitem__(self, i):
+        return _FakeT(self._p, self.shape[1:], self._e, self.dtype, self._st[1:])
 
     def data_ptr(self):
         return self._p
@@ -146,6 +155,57 @@ def test_contract_errors_before_any_gpu_work(lib):
     with pytest.raises(apb.ApbError) as e:
         apb.retain_score(d, w, q, k, v, _FakeT(0x70000, (2, 512), 4), stream=0)
     assert e.value.status == apb.ERR_CONFIG
+
+
+def test_binding_validates_tensors_before_the_abi(lib):
+    """apb.py checks what a raw pointer cannot carry: one shared K/V row stride,
+    dtypes, and that every tensor covers the rows / widths `dims` implies."""
+    d = _dims(host=0)
+    rows = d.rows
+    q = _FakeT(0x10000, (rows, 4, 64)); k = _FakeT(0x20000, (rows, 2, 64)); v = _FakeT(0x30000, (rows, 2, 64))
+    out = _FakeT(0x40000, (rows, 4, 64))
+    v_wide = _FakeT(0x30000, (rows, 2, 64), strides=(256, 64, 1))
+    bad = [
+        (q, k, v_wide, out, None),                                          # K/V row strides differ
+        (_FakeT(0x10000, (rows, 4, 64), dtype=torch.float16), k, v, out, None),  # not bf16
+        (_FakeT(0x10000, (rows - 1, 4, 64)), k, v, out, None),               # too few rows
+        (q, _FakeT(0x20000, (rows, 1, 64)), v, out, None),                  # too few KV heads
+        (q, k, v, _FakeT(0x40000, (rows, 2, 64)), None),                    # out too narrow
+        (q, k, v, out, _FakeT(0x50000, (4, rows - 8), 4)),                  # lse too short
+    ]
+    for args in bad:
+        with pytest.raises(apb.ApbError) as e:
+            apb.attention_fwd(d, *args[:3], None, args[3], lse=args[4], stream=0)
+        assert e.value.status == apb.ERR_CONTRACT
+    with pytest.raises(apb.ApbError) as e:  # scores too small
+        apb.select_topk(_dims(host=1), _FakeT(0x70000, (2, 100), 4), k, v, _FakeT(0x80000, (2, 64), 4, torch.int32),
+                        _FakeT(0x90000, (2, 2, 64, 64)), stream=0)
+    assert e.value.status == apb.ERR_CONTRACT
+
+
+def test_exchange_plan(lib):
+    """apb_exchange_plan: block = one round over contiguous per-rank slot ranges; cyclic = H/N
+    rounds of one slot per rank; nothing to do for one rank or l_p = 0."""
+    d = apb.Dims(n=131072, H=8, host=0, l_a=4096, l_p=2048, n_heads=32, n_kv_heads=8, head_dim=128)
+    slot = 2 * 8 * 2048 * 128
+    assert apb.exchange_plan(d, 1, 0) == []
+    assert apb.exchange_plan(d.__class__(**{**d.__dict__, "l_p": 0}), 4, 1) == []
+    assert apb.exchange_plan(d, 8, 3) == [(3 * slot, 0, slot)]
+    assert apb.exchange_plan(d, 2, 1) == [(4 * slot, 0, 4 * slot)]
+    assert apb.exchange_plan(d, 2, 1, apb.LAYOUT_CYCLIC) == [(k * 2 * slot + slot, k * 2 * slot, slot) for k in range(4)]
+    assert apb.exchange_plan(d, 8, 5, apb.LAYOUT_CYCLIC) == [(5 * slot, 0, slot)]
+    for bad, st in (((3, 0), apb.ERR_CONFIG), ((2, 2), apb.ERR_CONFIG), ((0, 0), apb.ERR_CONFIG)):
+        with pytest.raises(apb.ApbError) as e:
+            apb.exchange_plan(d, *bad)
+        assert e.value.status == st
+    with pytest.raises(apb.ApbError) as e:
+        apb.exchange_plan(d, 2, 0, 7)
+    assert e.value.status == apb.ERR_CONFIG
+
+
+def test_comm_check_null_is_ok(lib):
+    assert lib.apb_comm_check(None) == 0
+    assert lib.apb_comm_abort(None) == 0
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")

@@ -1,8 +1,8 @@
 """N > 1 host logic on CPU (gloo, world size 2): host ownership, the in-place slot layout the
 exchange uses (rank r owns slots [r*H/N, (r+1)*H/N) of gathered [H][2][hk][l_p'][d]), the
 128-byte communicator-id broadcast, and that a 2-rank run reproduces the single-process APB
-layer.  The arithmetic here is the oracle's (CPU); the GPU exchange itself (NCCL) is covered
-by the GPU tests / bench."""
+layer.  The arithmetic here is the oracle's (CPU); the exchange rounds are libapb's own
+(apb_exchange_plan, the plan apb_exchange_passing{,_cyclic} hand to NCCL) run over gloo."""
 import os
 import socket
 
@@ -14,6 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
+from paper_2502_12085_b200 import apb
 from paper_2502_12085_b200.prefill import hosts_of_rank
 
 
@@ -76,20 +77,19 @@ def _worker(rank, world, port, q, layout="block"):
         x = hosts[h]
         s = oracle.retain_score(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
         gathered[h] = oracle.compact(x["k"], x["v"], x["L_A"], oracle.select_all_heads(s, cfg.l_p))
-    # step 3: in-place all-gather of contiguous per-rank slot ranges (apb_exchange_passing layout),
-    # or, cyclic, one all-gather per round k of slots [k*N, (k+1)*N) (apb_exchange_passing_cyclic)
-    if layout == "block":
-        flat = torch.from_numpy(gathered.view(np.int32)).reshape(world, -1)  # bf16 pairs as int32 (gloo)
-        parts = [torch.empty_like(flat[0]) for _ in range(world)]
-        dist.all_gather(parts, flat[rank].clone())
-        gathered = torch.stack(parts).numpy().view(np.uint16).reshape(gathered.shape)
-    else:
-        slots = torch.from_numpy(gathered.view(np.int32)).reshape(cfg.H, -1)
-        for k in range(cfg.H // world):
-            parts = [torch.empty_like(slots[0]) for _ in range(world)]
-            dist.all_gather(parts, slots[k * world + rank].clone())
-            slots[k * world: (k + 1) * world] = torch.stack(parts)
-        gathered = slots.numpy().view(np.uint16).reshape(gathered.shape)
+    # step 3: the in-place all-gather rounds libapb's apb_exchange_passing{,_cyclic} enqueue, as
+    # apb_exchange_plan states them (send / recv offsets and counts in bf16 elements), run on gloo
+    dims = apb.Dims(n=cfg.n, H=cfg.H, host=0, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
+                    head_dim=cfg.d)
+    plan = apb.exchange_plan(dims, world, rank, apb.LAYOUT_CYCLIC if layout == "cyclic" else apb.LAYOUT_BLOCK)
+    assert len(plan) == (1 if layout == "block" else cfg.H // world)
+    flat = torch.from_numpy(gathered.reshape(-1).view(np.int32))  # bf16 pairs as int32 (gloo)
+    for send, recv, count in plan:
+        assert send % 2 == 0 and recv % 2 == 0 and count % 2 == 0
+        parts = [torch.empty(count // 2, dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(parts, flat[send // 2: (send + count) // 2].clone())
+        flat[recv // 2: (recv + world * count) // 2] = torch.cat(parts)
+    gathered = flat.numpy().view(np.uint16).reshape(gathered.shape)
     # step 4
     outs = {}
     for h in mine:
