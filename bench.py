@@ -220,8 +220,8 @@ def cpu_baseline_line(cfg, H, layers, value=None, sample=None):
             "physical_cores": phys, "affinity_cores": avail,
             "toy_full_oracle": dict(toy, config="toy: n=2048, H=4, l_a=128, l_p=64, hq=4, hk=2, d=64, 1 layer, "
                                                 "every row of every host (no extrapolation)"),
-            "single_thread_extrapolated": round(value * toy["single_thread"]["seconds"]
-                                                / toy["all_threads"]["seconds"], 4)}
+            "single_thread_extrapolated": round(value * toy["all_threads"]["seconds"]
+                                                / toy["single_thread"]["seconds"], 4)}
 
 
 def host_layout_desc(world, H, layout):

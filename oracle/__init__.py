@@ -22,6 +22,7 @@ example, the hand-evaluated scorer value tanh(1/2)).  No function is "parity unp
 """
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes
 import os
 import subprocess
@@ -226,6 +227,89 @@ def attention(q, k, v, L_A: int, pk, pv, scale: float | None = None, rows=None, 
                                      _p(O), _p(lse), int(q_subset))
     if rc:
         raise ValueError(f"oracle_attention rc={rc}")
+    return O, lse
+
+
+# ----------------------------------------------------------------------------- full-size forms
+# The same two definitions with fp64 LIBRARY matmuls (numpy / OpenBLAS) as steps, for checks at
+# the bench's full sizes (a retaining head is ~207 GFLOP per L8 host, ~100x the C loops' speed
+# is needed to check every token).  No blocking beyond row chunks, no reordering of the math:
+# each output is the plain definition.  Pinned like the C forms (tests/test_oracle.py,
+# *_blas pins): hand value, SiLU closed form, torch fp64 Linear, torch fp64 SDPA, closed-form
+# lse counts, rows sum to one, one-hot probes.
+
+def retain_score_blas(q, k, v, L_A: int, w1, b1, w2, b2, hk: int, chunk: int = 2048) -> np.ndarray:
+    """s[j][t] (readings G2/G4): z = W1 x_t + b1, a = SiLU(z) = z / (1 + e^-z),
+    o = W2 a + b2, s[j] = max over KV head j's r = n_out/hk outputs.  x_t = [Q_t | K_t | V_t].
+    Arguments as retain_score; returns fp64 [hk][l_b]."""
+    q, k, v = np.asarray(q), np.asarray(k), np.asarray(v)
+    l_b = q.shape[0] - L_A
+    w1 = _as_f64(w1)
+    w2 = _as_f64(w2)
+    b1 = np.zeros(w1.shape[0]) if b1 is None else _as_f64(b1)
+    b2 = np.zeros(w2.shape[0]) if b2 is None else _as_f64(b2)
+    n_out = w2.shape[0]
+    r = n_out // hk
+    s = np.empty((hk, l_b), np.float64)
+    for t0 in range(0, l_b, chunk):
+        t1 = min(l_b, t0 + chunk)
+        x = np.concatenate([_as_f64(a[L_A + t0:L_A + t1]).reshape(t1 - t0, -1) for a in (q, k, v)], axis=1)
+        z = x @ w1.T + b1
+        with np.errstate(over="ignore"):
+            a_ = z / (1.0 + np.exp(-z))
+        o = a_ @ w2.T + b2
+        s[:, t0:t1] = o.reshape(t1 - t0, hk, r).max(axis=2).T
+    return s
+
+
+def attention_blas(q, k, v, L_A: int, pk, pv, rows, scale: float | None = None, q_subset: bool = False,
+                   chunk: int = 256):
+    """eq:apb for the query rows `rows`, with fp64 matmuls for q.k and p.v.
+    Key sequence [K_a ; K_p ; K_h].  vis(r) (reading G1): anchor row r < L_A sees
+    keys 0..r; local row r = L_A + i sees all L_A anchor keys, all P passing keys and local keys
+    0..i — in both cases the first lim(r) keys of the sequence, lim = r+1 (anchor) or
+    L_A + P + i + 1 (local).  Two-pass softmax: m = max, w = e^(l - m), Z = sum w,
+    O = sum w v / Z, lse = m + ln Z.  Arguments as attention(); returns (O [rows][hq][d], lse [rows][hq])."""
+    q, k, v = np.asarray(q), np.asarray(k), np.asarray(v)
+    pk, pv = np.asarray(pk), np.asarray(pv)
+    hq, d = q.shape[1], q.shape[2]
+    hk = k.shape[1]
+    g = hq // hk
+    L_A = int(L_A)
+    P = pk.shape[0]
+    rows = np.asarray(rows, np.int64)
+    if q_subset and len(rows) != q.shape[0]:
+        raise ValueError("q_subset needs rows with one entry per q row")
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)  # 1/sqrt(d_m) (P:112-115)
+    lim = np.where(rows < L_A, rows + 1, P + rows + 1)
+    order = np.argsort(lim, kind="stable")
+    O = np.empty((len(rows), hq, d), np.float64)
+    lse = np.empty((len(rows), hq), np.float64)
+    def head(j):  # KV head j and its g query heads (independent of every other head)
+        kseq = np.concatenate([_as_f64(k[:L_A, j]), _as_f64(pk[:, j]).reshape(P, d), _as_f64(k[L_A:, j])], 0)
+        vseq = np.concatenate([_as_f64(v[:L_A, j]), _as_f64(pv[:, j]).reshape(P, d), _as_f64(v[L_A:, j])], 0)
+        for c0 in range(0, len(rows), chunk):
+            sel = order[c0:c0 + chunk]
+            src = sel if q_subset else rows[sel]
+            Qc = _as_f64(q[src, j * g:(j + 1) * g]).reshape(len(sel) * g, d)
+            lim_c = np.repeat(lim[sel], g)
+            kmax = int(lim_c.max())
+            logits = Qc @ kseq[:kmax].T
+            logits *= scale
+            for i in np.nonzero(lim_c < kmax)[0]:  # keys past lim(r) are not visible
+                logits[i, lim_c[i]:] = -np.inf
+            m = logits.max(axis=1, keepdims=True)
+            logits -= m
+            w = np.exp(logits, out=logits)
+            Z = w.sum(axis=1, keepdims=True)
+            Oc = (w @ vseq[:kmax]) / Z
+            O[sel, j * g:(j + 1) * g] = Oc.reshape(len(sel), g, d)
+            lse[sel, j * g:(j + 1) * g] = (m + np.log(Z)).reshape(len(sel), g)
+
+    # heads in parallel threads (numpy's elementwise passes are single-threaded and release the GIL)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(hk, os.cpu_count() or 1)) as ex:
+        list(ex.map(head, range(hk)))
     return O, lse
 
 

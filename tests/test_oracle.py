@@ -21,19 +21,32 @@ def _rand(shape, seed, scale=1.0):
     return np.random.default_rng(seed).standard_normal(shape) * scale
 
 
+def _attn_blas_all(q, k, v, L_A, pk, pv, scale=None):
+    return oracle.attention_blas(q, k, v, L_A, pk, pv, np.arange(q.shape[0]), scale)
+
+
+# every pin of the two oracle forms: the plain C loops and the full-size (fp64 library matmul) form
+SCORERS = {"c": oracle.retain_score, "blas": oracle.retain_score_blas}
+ATTNS = {"c": oracle.attention, "blas": _attn_blas_all}
+scorer_forms = pytest.mark.parametrize("form", list(SCORERS))
+attn_forms = pytest.mark.parametrize("form", list(ATTNS))
+
+
 # ----------------------------------------------------------------------------- scorer
 
-def test_scorer_hand_value():
+@scorer_forms
+def test_scorer_hand_value(form):
     """P18: worked value tanh(1/2) for a 1-token, hidden-2 retaining head (tests/golden/scorer_hand.json)."""
     g = json.load(open(os.path.join(GOLD, "scorer_hand.json")))
     x = np.array(g["x"], np.float64)
     q, k, v = x[0].reshape(1, 1, 1), x[1].reshape(1, 1, 1), x[2].reshape(1, 1, 1)
-    s = oracle.retain_score(q, k, v, 0, np.array(g["w1"]), np.array(g["b1"]), np.array(g["w2"]),
+    s = SCORERS[form](q, k, v, 0, np.array(g["w1"]), np.array(g["b1"]), np.array(g["w2"]),
                             np.array(g["b2"]), hk=1)
     assert abs(s[0, 0] - g["expected"]) < 1e-15
 
 
-def test_scorer_silu_closed_form():
+@scorer_forms
+def test_scorer_silu_closed_form(form):
     """SiLU(z) = z/2 (1 + tanh(z/2)) — selecting single hidden units with W1/W2 one-hots."""
     hq, hk, d = 2, 1, 2
     d_in = (hq + 2 * hk) * d
@@ -46,29 +59,31 @@ def test_scorer_silu_closed_form():
         w1 = np.zeros((4, d_in)); w1[1, u] = 1.0
         b1 = np.array([0.0, 0.25, 0.0, 0.0])
         w2 = np.zeros((1, 4)); w2[0, 1] = 1.0
-        s = oracle.retain_score(q, k, v, 0, w1, b1, w2, None, hk=1)
+        s = SCORERS[form](q, k, v, 0, w1, b1, w2, None, hk=1)
         z = x[:, u] + 0.25
         assert np.allclose(s[0], z / 2 * (1 + np.tanh(z / 2)), rtol=0, atol=1e-13)
 
 
-def test_scorer_group_max_and_bias():
+@scorer_forms
+def test_scorer_group_max_and_bias(form):
     """W2 = 0 => o = b2, s[j] = max of head j's group (reading G4, n_out = hq)."""
     hq, hk, d = 4, 2, 2
     rng = np.random.default_rng(4)
     q = rng.standard_normal((3, hq, d)); k = rng.standard_normal((3, hk, d)); v = rng.standard_normal((3, hk, d))
     w1 = rng.standard_normal((8, (hq + 2 * hk) * d))
     b2 = np.array([0.5, -1.0, 2.0, 3.0])
-    s = oracle.retain_score(q, k, v, 0, w1, None, np.zeros((4, 8)), b2, hk=hk)
+    s = SCORERS[form](q, k, v, 0, w1, None, np.zeros((4, 8)), b2, hk=hk)
     assert np.all(s[0] == 0.5) and np.all(s[1] == 3.0)
 
 
-def test_scorer_matches_torch_fp64():
+@scorer_forms
+def test_scorer_matches_torch_fp64(form):
     """P10: torch fp64 Linear -> SiLU -> Linear -> group max on the same weights."""
     hq, hk, d, L_A, l_b, dh = 4, 2, 8, 3, 17, 32
     q = _rand((L_A + l_b, hq, d), 1); k = _rand((L_A + l_b, hk, d), 2); v = _rand((L_A + l_b, hk, d), 3)
     d_in = (hq + 2 * hk) * d
     w1 = _rand((dh, d_in), 4, 0.2); b1 = _rand(dh, 5, 0.1); w2 = _rand((hq, dh), 6, 0.3); b2 = _rand(hq, 7)
-    s = oracle.retain_score(q, k, v, L_A, w1, b1, w2, b2, hk)
+    s = SCORERS[form](q, k, v, L_A, w1, b1, w2, b2, hk)
     x = torch.cat([torch.from_numpy(a[L_A:]).reshape(l_b, -1) for a in (q, k, v)], 1)
     h = torch.nn.functional.silu(torch.nn.functional.linear(x, torch.from_numpy(w1), torch.from_numpy(b1)))
     o = torch.nn.functional.linear(h, torch.from_numpy(w2), torch.from_numpy(b2))
@@ -76,11 +91,12 @@ def test_scorer_matches_torch_fp64():
     assert np.allclose(s, ref, rtol=0, atol=1e-12)
 
 
-def test_scorer_zero_weights_select_prefix():
+@scorer_forms
+def test_scorer_zero_weights_select_prefix(form):
     """P10: zero W1/W2 => constant scores => ties => indices 0..l_p'-1 (tie rule G5)."""
     hq, hk, d = 2, 1, 4
     q = _rand((10, hq, d), 1); k = _rand((10, hk, d), 2); v = _rand((10, hk, d), 3)
-    s = oracle.retain_score(q, k, v, 2, np.zeros((4, 16)), None, np.zeros((2, 4)), None, hk)
+    s = SCORERS[form](q, k, v, 2, np.zeros((4, 16)), None, np.zeros((2, 4)), None, hk)
     assert np.all(s == 0.0)
     assert oracle.select_topk(s[0], 3).tolist() == [0, 1, 2]
 
@@ -116,7 +132,7 @@ def test_select_fuzz_vs_sort():
 
 # ----------------------------------------------------------------------------- attention
 
-def _onehot_probe(L_A, P, l_b):
+def _onehot_probe(L_A, P, l_b, attn=oracle.attention):
     """Q = 0 => all visible logits 0 => O[r] = mean of visible V rows.  With V_k = e_k
     (one-hot over keys), O[r][k] = 1/|vis(r)| if k visible else 0 — the mask itself."""
     nk = L_A + P + l_b
@@ -126,32 +142,35 @@ def _onehot_probe(L_A, P, l_b):
     eye = np.eye(nk)
     v = np.concatenate([eye[:L_A], eye[L_A + P:]], 0)[:, None, :]
     pv = eye[L_A:L_A + P][:, None, :]
-    O, lse = oracle.attention(q, k, v, L_A, np.zeros((P, 1, d)), pv)
+    O, lse = attn(q, k, v, L_A, np.zeros((P, 1, d)), pv)
     return (O[:, 0, :nk] > 0).astype(int), O, lse
 
 
-def test_mask_spec_worked_examples():
+@attn_forms
+def test_mask_spec_worked_examples(form):
     """P7: SPEC.md:214-215 printed masks (tests/golden/mask_examples.json)."""
     g = json.load(open(os.path.join(GOLD, "mask_examples.json")))
     for c in g["cases"]:
-        vis, _, _ = _onehot_probe(c["L_A"], c["P"], c["l_b"])
+        vis, _, _ = _onehot_probe(c["L_A"], c["P"], c["l_b"], ATTNS[form])
         assert vis.tolist() == c["rows"], c["cite"]
 
 
-def test_mask_closed_form_lse_counts():
+@attn_forms
+def test_mask_closed_form_lse_counts(form):
     """P16: Q = 0 => lse[r] = ln|vis(r)| exactly; counts for (3,4,5) from the golden file."""
     g = json.load(open(os.path.join(GOLD, "mask_examples.json")))
     for c in g["visible_counts"]:
-        vis, O, lse = _onehot_probe(c["L_A"], c["P"], c["l_b"])
+        vis, O, lse = _onehot_probe(c["L_A"], c["P"], c["l_b"], ATTNS[form])
         assert vis.sum(1).tolist() == c["counts"]
         assert np.allclose(lse[:, 0], np.log(c["counts"]), rtol=0, atol=1e-14)
 
 
-def test_mask_equals_restricted_causal_brute_force():
+@attn_forms
+def test_mask_equals_restricted_causal_brute_force(form):
     """P7 / G1: for every (L_A, P, l_b) <= 5 the mask equals rows [0,L_A) u [L_A+P, end) of a
     plain lower-triangular causal mask over the concatenated sequence [A|P|B]."""
     for L_A, P, l_b in itertools.product(range(5), range(5), range(1, 5)):
-        vis, _, _ = _onehot_probe(L_A, P, l_b)
+        vis, _, _ = _onehot_probe(L_A, P, l_b, ATTNS[form])
         nk = L_A + P + l_b
         causal = np.tril(np.ones((nk, nk), int))
         rows = list(range(L_A)) + list(range(L_A + P, nk))
@@ -184,14 +203,15 @@ def _sdpa_reference(q, k, v, L_A, pk, pv, scale):
     return O, lse
 
 
+@attn_forms
 @pytest.mark.parametrize("L_A,P,l_b", [(0, 0, 9), (5, 0, 7), (0, 6, 5), (7, 9, 3), (16, 24, 33), (3, 4, 5)])
-def test_attention_matches_torch_sdpa(L_A, P, l_b):
+def test_attention_matches_torch_sdpa(L_A, P, l_b, form):
     """P1: oracle == torch fp64 SDPA (library special case) on random inputs, GQA g=2."""
     hq, hk, d = 4, 2, 16
     q = _rand((L_A + l_b, hq, d), 1, 2.0); k = _rand((L_A + l_b, hk, d), 2, 2.0); v = _rand((L_A + l_b, hk, d), 3)
     pk = _rand((P, hk, d), 4, 2.0); pv = _rand((P, hk, d), 5)
     scale = 1 / math.sqrt(d)
-    O, lse = oracle.attention(q, k, v, L_A, pk, pv, scale)
+    O, lse = ATTNS[form](q, k, v, L_A, pk, pv, scale)
     Or, lr = _sdpa_reference(q, k, v, L_A, pk, pv, scale)
     assert np.allclose(O, Or, rtol=0, atol=1e-12)
     assert np.allclose(lse, lr, rtol=0, atol=1e-12)
@@ -207,16 +227,18 @@ def test_attention_row_subset_matches_full():
     assert np.array_equal(O2, O[rows]) and np.array_equal(lse2, lse[rows])
 
 
-def test_attention_rows_sum_to_one():
+@attn_forms
+def test_attention_rows_sum_to_one(form):
     """P5: V = 1 => O = 1 (softmax rows sum to 1)."""
     hq, hk, d, L_A, P, l_b = 4, 2, 8, 6, 5, 11
     q = _rand((L_A + l_b, hq, d), 1, 3.0); k = _rand((L_A + l_b, hk, d), 2, 3.0)
     v = np.ones((L_A + l_b, hk, d)); pv = np.ones((P, hk, d))
-    O, _ = oracle.attention(q, k, v, L_A, _rand((P, hk, d), 4, 3.0), pv)
+    O, _ = ATTNS[form](q, k, v, L_A, _rand((P, hk, d), 4, 3.0), pv)
     assert np.allclose(O, 1.0, rtol=0, atol=1e-14)
 
 
-def test_attention_one_hot_probe():
+@attn_forms
+def test_attention_one_hot_probe(form):
     """P17: q_r = c k* (c large) => O[r] = V[k*] iff k* is visible to r; passing keys are
     visible to local rows only; local key i+1 is invisible to local row i."""
     hk, hq, d, L_A, P, l_b = 1, 1, 16, 4, 3, 6
@@ -233,20 +255,21 @@ def test_attention_one_hot_probe():
     q[L_A + 2, 0] = keys[L_A + 1] * 50
     q[3, 0] = keys[L_A + 1] * 50
     q[L_A + 1, 0] = keys[L_A + P + 2] * 50  # local row 1 targets local key 2 (future) -> invisible
-    O, _ = oracle.attention(q, k, v, L_A, pk, pv)
+    O, _ = ATTNS[form](q, k, v, L_A, pk, pv)
     assert np.allclose(O[L_A + 2, 0], vals[L_A + 1], atol=1e-9)
     assert not np.allclose(O[3, 0], vals[L_A + 1], atol=1e-3)
     assert not np.allclose(O[L_A + 1, 0], vals[L_A + P + 2], atol=1e-3)
 
 
-def test_attention_passing_permutation_invariance():
+@attn_forms
+def test_attention_passing_permutation_invariance(form):
     """P9: permuting passing keys together with their values leaves O unchanged."""
     hq, hk, d, L_A, P, l_b = 2, 1, 8, 3, 7, 5
     q = _rand((L_A + l_b, hq, d), 1); k = _rand((L_A + l_b, hk, d), 2); v = _rand((L_A + l_b, hk, d), 3)
     pk = _rand((P, hk, d), 4); pv = _rand((P, hk, d), 5)
     perm = np.random.default_rng(0).permutation(P)
-    O1, l1 = oracle.attention(q, k, v, L_A, pk, pv)
-    O2, l2 = oracle.attention(q, k, v, L_A, pk[perm], pv[perm])
+    O1, l1 = ATTNS[form](q, k, v, L_A, pk, pv)
+    O2, l2 = ATTNS[form](q, k, v, L_A, pk[perm], pv[perm])
     assert np.allclose(O1, O2, atol=1e-13) and np.allclose(l1, l2, atol=1e-13)
 
 
@@ -536,3 +559,23 @@ def test_attention_q_subset_equals_full_rows():
     O2, lse2 = oracle.attention(q[rows], k, v, L_A, pk, pv, rows=rows, q_subset=True)
     np.testing.assert_array_equal(O, O2)
     np.testing.assert_array_equal(lse, lse2)
+
+
+def test_blas_forms_sampled_rows_and_bf16_inputs():
+    """The full-size forms take bf16 bit patterns, sampled (unsorted, repeated-limit) rows and
+    q_subset exactly as the C forms do (same outputs to rounding)."""
+    cfg = synth.CONFIGS["toy"].replace(n=1024, l_a=96, l_p=40, d_hidden=64)
+    x = synth.host_qkv(cfg, 0, 2)
+    w = synth.retain_weights(cfg, 0)
+    s_c = oracle.retain_score(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk)
+    s_b = oracle.retain_score_blas(x["q"], x["k"], x["v"], x["L_A"], w["w1"], w["b1"], w["w2"], w["b2"], cfg.hk,
+                                   chunk=100)
+    assert np.allclose(s_c, s_b, rtol=0, atol=1e-12)
+    g = synth.f32_to_bf16_bits(_rand((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d), 3).astype(np.float32))
+    pk, pv = oracle.passing(g, 2)
+    rows = [300, 0, 95, 96, 97, 351, 5, 200]
+    O_c, l_c = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv, rows=rows)
+    O_b, l_b = oracle.attention_blas(x["q"], x["k"], x["v"], x["L_A"], pk, pv, rows, chunk=3)
+    assert np.allclose(O_c, O_b, rtol=0, atol=1e-12) and np.allclose(l_c, l_b, rtol=0, atol=1e-12)
+    O_s, l_s = oracle.attention_blas(x["q"][rows], x["k"], x["v"], x["L_A"], pk, pv, rows, q_subset=True)
+    assert np.allclose(O_s, O_b, rtol=0, atol=1e-13) and np.allclose(l_s, l_b, rtol=0, atol=1e-13)
