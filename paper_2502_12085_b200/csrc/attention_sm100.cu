@@ -612,8 +612,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
               p2 = f2_pack(p0, p1);
             }
-            acc2[c & 3] = fadd2(acc2[c & 3], p2);
             pk[c] = pack_bf16x2(p0, p1);
+#ifdef APB_ROWSUM_FP32
+            acc2[c & 3] = fadd2(acc2[c & 3], p2);
+#else
+            // the row sum adds the bf16 weights the PV MMA actually uses, so the normalisation
+            // matches them (with the lazy rescale the row max's weight is 2^delta, not 1, and
+            // bf16-rounding it alone would bias O by up to 2^-9 relative)
+            (void)p2;
+            acc2[c & 3] = f2_add_bf16x2(acc2[c & 3], pk[c]);
+#endif
           }
         };
         // Speculation: the running max m_run only moves when a row max grows by more than the

@@ -8,7 +8,10 @@
 // reading G5).  Output indices are ascending by construction.  Bit-exact, no floating point.
 // Kernel 2: gather of the selected K and V rows (256 B each at d=128) into the packed send
 // slot [2][hk][l_p'][d] — vectorised 16-byte copies spread over many CTAs (HBM-bound).
+#include <cstdlib>
+
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace apb {
 namespace sel {
@@ -119,9 +122,393 @@ __global__ void __launch_bounds__(256) compact_kernel(const int32_t* __restrict_
 
 }  // namespace sel
 
+// ---------------------------------------------------------------- fast select + PDL gather
+// select_fast_kernel: one 1024-thread CTA per KV head.  The l_b order-preserving keys are staged
+// in shared memory once (else re-read from L2 when they do not fit), then 4 radix passes of 8-bit
+// digits run on the CTA's histogram: warp-aggregated (match.any: the first digit holds the sign +
+// exponent, so most keys share a handful of bins and plain shared atomics would serialise on
+// them), and the 256-bin suffix scan is parallel (8 warps of shuffles), not one thread's loop.
+// The ordered compaction is warp-local: warp w owns a contiguous index range, counts its
+// (> T, == T) keys, one block scan of the 32 warp counts gives every warp its output offset and
+// tie rank, and each warp writes its ascending indices with ballots — one block barrier instead of
+// two block scans per 1024 elements.  It then triggers the dependent launch.
+// gather_kernel (programmatic dependent launch, many CTAs): copies the selected K/V rows into the
+// send slot, 8 x 16-byte loads in flight per thread.  Both are bit-exact integer logic.
+namespace sel {
+constexpr int kFT = 1024;                 // threads of the select CTA
+constexpr int kMaxSmemKeys = 40 * 1024;   // 160 KB of staged keys; beyond that keys come from L2
+constexpr int kCand = 8192;               // candidate keys kept after the first digit (32 KB)
+
+// Suffix search over `nb` histogram bins (nb = 1024 or 2048; thread t holds bins [t*bpt, t*bpt+bpt)):
+// the bin b with above(b) < kk <= above(b) + hist[b], above(b) = count in bins > b.
+__device__ __forceinline__ void find_bin(const uint32_t* hist, int nb, uint32_t kk, uint32_t* wtot,
+                                         uint32_t* sh_bin, uint32_t* sh_k) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bpt = nb / kFT;  // 1 or 2
+  uint32_t c[2] = {hist[tid * bpt], bpt > 1 ? hist[tid * bpt + 1] : 0u};
+  const uint32_t mine = c[0] + c[1];
+  uint32_t incl = mine;  // suffix within the warp (lanes >= lane)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
+    if (lane + o < 32) incl += y;
+  }
+  if (lane == 0) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {  // suffix over the 32 warp totals, exclusive
+    const uint32_t wt = wtot[lane];
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, wi, o);
+      if (lane + o < 32) wi += y;
+    }
+    wtot[32 + lane] = wi - wt;
+  }
+  __syncthreads();
+  uint32_t above = incl - mine + wtot[32 + warp];  // keys in bins above this thread's bins
+  for (int q = bpt - 1; q >= 0; --q) {
+    if (above < kk && above + c[q] >= kk) {
+      *sh_bin = (uint32_t)(tid * bpt + q);
+      *sh_k = kk - above;
+    }
+    above += c[q];
+  }
+  __syncthreads();
+}
+
+template <bool kSmemKeys>
+__global__ void __launch_bounds__(kFT) select_fast_kernel(const float* __restrict__ scores, int l_b, int lp,
+                                                          int32_t* __restrict__ indices) {
+  extern __shared__ uint32_t dyn[];
+  uint32_t* skeys = dyn;                      // [l_b] (kSmemKeys)
+  uint32_t* cand = dyn + (kSmemKeys ? l_b : 0);  // [kCand]
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t wtot[64];
+  __shared__ uint32_t sh_bin, sh_k, n_cand;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j = blockIdx.x;
+  const float* s = scores + (int64_t)j * l_b;
+  auto key_at = [&](int i) -> uint32_t {
+    if constexpr (kSmemKeys) return skeys[i];
+    else return order_key(__ldg(s + i));
+  };
+  for (int b = tid; b < 2048; b += kFT) hist[b] = 0;
+  if (tid == 0) n_cand = 0;
+  __syncthreads();
+  // ---- stage the keys: loads only, so the compiler keeps many in flight (one HBM latency, not
+  // one per iteration as when each load is followed by a shared atomic)
+  if constexpr (kSmemKeys) {
+#pragma unroll 8
+    for (int i = tid; i < l_b; i += kFT) skeys[i] = order_key(__ldg(s + i));
+    __syncthreads();
+  }
+  // ---- digit 1 (key bits 31..21, 2048 bins)
+  for (int i = tid; i < l_b; i += kFT) atomicAdd(&hist[key_at(i) >> 21], 1u);
+  __syncthreads();
+  find_bin(hist, 2048, (uint32_t)lp, wtot, &sh_bin, &sh_k);
+  uint32_t prefix = sh_bin << 21, kk = sh_k;
+  // ---- candidates: the keys in that bin (unordered; selection only needs their values)
+  for (int b = tid; b < 2048; b += kFT) hist[b] = 0;
+  for (int base = 0; base < l_b; base += kFT) {
+    const int i = base + tid;
+    const bool m = i < l_b && (key_at(i) >> 21) == (prefix >> 21);
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+    uint32_t off = 0;
+    if (lane == 0 && bal) off = atomicAdd(&n_cand, (uint32_t)__popc(bal));
+    off = __shfl_sync(0xFFFFFFFFu, off, 0);
+    const uint32_t slot = off + __popc(bal & ((1u << lane) - 1u));
+    if (m && slot < (uint32_t)kCand) cand[slot] = key_at(i);
+  }
+  __syncthreads();
+  const uint32_t nc = n_cand;
+  const bool use_cand = nc <= (uint32_t)kCand;
+  const int n2 = use_cand ? (int)nc : l_b;
+  // ---- digit 2 (bits 20..10, 2048 bins) and digit 3 (bits 9..0, 1024 bins) over the candidates
+  for (int pass = 0; pass < 2; ++pass) {
+    const int shift = pass == 0 ? 10 : 0;
+    const uint32_t pmask = pass == 0 ? 0xFFE00000u : 0xFFFFFC00u;
+    const uint32_t dmask = pass == 0 ? 0x7FFu : 0x3FFu;
+    if (pass == 1) {
+      for (int b = tid; b < 2048; b += kFT) hist[b] = 0;
+      __syncthreads();
+    }
+    for (int i = tid; i < n2; i += kFT) {
+      const uint32_t key = use_cand ? cand[i] : key_at(i);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    find_bin(hist, pass == 0 ? 2048 : 1024, kk, wtot, &sh_bin, &sh_k);
+    prefix |= sh_bin << shift;
+    kk = sh_k;
+  }
+  const uint32_t T = prefix, need_eq = kk;  // key of the l_p'-th largest score; ties taken
+
+  // ---- warp-local ordered compaction: warp w owns [w*per, (w+1)*per), per a multiple of 32
+  __shared__ uint32_t wg[32], we[32];
+  const int per = ((l_b + 31) / 32 + 31) / 32 * 32;
+  const int w0 = min(l_b, warp * per), w1 = min(l_b, w0 + per);
+  uint32_t gt = 0, eq = 0;
+  for (int b = w0; b < w1; b += 32) {
+    const int i = b + lane;
+    const uint32_t key = i < w1 ? key_at(i) : 0u;
+    gt += __popc(__ballot_sync(0xFFFFFFFFu, i < w1 && key > T));
+    eq += __popc(__ballot_sync(0xFFFFFFFFu, i < w1 && key == T));
+  }
+  if (lane == 0) {
+    wg[warp] = gt;
+    we[warp] = eq;
+  }
+  __syncthreads();
+  uint32_t g_before = 0, e_before = 0;
+  for (int w = 0; w < warp; ++w) {
+    g_before += wg[w];
+    e_before += we[w];
+  }
+  // selected before this warp: its > T keys plus the ties of lower warps that are taken
+  uint32_t pos = g_before + min(need_eq, e_before);
+  uint32_t erank = e_before;
+  int32_t* out = indices + (int64_t)j * lp;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int b = w0; b < w1; b += 32) {
+    const int i = b + lane;
+    const uint32_t key = i < w1 ? key_at(i) : 0u;
+    const bool is_eq = i < w1 && key == T;
+    const uint32_t eqb = __ballot_sync(0xFFFFFFFFu, is_eq);
+    const bool sel = (i < w1 && key > T) || (is_eq && erank + __popc(eqb & lt) < need_eq);
+    const uint32_t selb = __ballot_sync(0xFFFFFFFFu, sel);
+    if (sel) out[pos + __popc(selb & lt)] = i;
+    pos += __popc(selb);
+    erank += __popc(eqb);
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Block exclusive scan of one 32-bit value per thread (1024 threads); returns the prefix.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wt = wtot[lane];
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wtot[32 + lane] = wi - wt;
+  }
+  __syncthreads();
+  return incl - v + wtot[32 + warp];
+}
+
+// Register variant (l_b <= 1024 * KPT, every paper config): thread t holds the keys of indices
+// [t*KPT, (t+1)*KPT) in registers.  Digit 1 (bits 31..21) histograms every key; the keys in the
+// chosen bin are then compacted into a shared candidate list (one block scan, no contended
+// counter), and digits 2 and 3 (11 + 10 bits) histogram only those.  The ordered compaction is one
+// block scan of the per-thread (> T, == T) counts; each thread writes its ascending indices to a
+// shared staging buffer, copied out coalesced.
+constexpr int kCandReg = 4096;  // candidate list capacity (else digits 2-3 scan the registers)
+constexpr int kOutStage = 4096; // staged output indices (else written straight to global)
+
+template <int KPT>
+__global__ void __launch_bounds__(kFT) select_reg_kernel(const float* __restrict__ scores, int l_b, int lp,
+                                                         int32_t* __restrict__ indices) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t wtot[64];
+  __shared__ uint32_t cand[kCandReg];  // candidate keys; reused as the staged output indices
+  __shared__ uint32_t sh_bin, sh_k, sh_nc;
+  const int tid = threadIdx.x;
+  const int j = blockIdx.x;
+  const float* s = scores + (int64_t)j * l_b;
+  const int e0 = tid * KPT;
+  uint32_t key[KPT];
+  if (e0 + KPT <= l_b && (l_b & 3) == 0) {
+#pragma unroll
+    for (int e = 0; e < KPT; e += 4) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(s + e0 + e));
+      key[e] = order_key(f.x);
+      key[e + 1] = order_key(f.y);
+      key[e + 2] = order_key(f.z);
+      key[e + 3] = order_key(f.w);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) key[e] = e0 + e < l_b ? order_key(__ldg(s + e0 + e)) : 0u;
+  }
+  const int nmine = max(0, min(KPT, l_b - e0));
+  for (int b = tid; b < 2048; b += kFT) hist[b] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < KPT; ++e)
+    if (e < nmine) atomicAdd(&hist[key[e] >> 21], 1u);
+  __syncthreads();
+  find_bin(hist, 2048, (uint32_t)lp, wtot, &sh_bin, &sh_k);
+  uint32_t prefix = sh_bin << 21, kk = sh_k;
+  // ---- candidate list: the keys of the chosen digit-1 bin
+  uint32_t nm = 0;
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) nm += (e < nmine && (key[e] >> 21) == sh_bin);
+  uint32_t cpos = block_excl_scan(nm, wtot);
+  if (tid == kFT - 1) sh_nc = cpos + nm;
+  for (int b = tid; b < 2048; b += kFT) hist[b] = 0;
+  __syncthreads();
+  const uint32_t nc = sh_nc;
+  const bool use_cand = nc <= (uint32_t)kCandReg;
+  if (use_cand) {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e)
+      if (e < nmine && (key[e] >> 21) == (prefix >> 21)) cand[cpos++] = key[e];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int shift = pass == 0 ? 10 : 0;
+    const uint32_t pmask = pass == 0 ? 0xFFE00000u : 0xFFFFFC00u;
+    const uint32_t dmask = pass == 0 ? 0x7FFu : 0x3FFu;
+    if (pass == 1) {
+      for (int b = tid; b < 1024; b += kFT) hist[b] = 0;
+      __syncthreads();
+    }
+    if (use_cand) {
+      for (int i = tid; i < (int)nc; i += kFT) {
+        const uint32_t c = cand[i];
+        if ((c & pmask) == prefix) atomicAdd(&hist[(c >> shift) & dmask], 1u);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < KPT; ++e)
+        if (e < nmine && (key[e] & pmask) == prefix) atomicAdd(&hist[(key[e] >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    find_bin(hist, pass == 0 ? 2048 : 1024, kk, wtot, &sh_bin, &sh_k);
+    prefix |= sh_bin << shift;
+    kk = sh_k;
+  }
+  const uint32_t T = prefix, need_eq = kk;  // key of the l_p'-th largest score; ties taken
+  // ---- ordered compaction: block exclusive scan of (gt << 16 | eq) (both <= 1024 * KPT < 2^16)
+  uint32_t gt = 0, eq = 0;
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    gt += (e < nmine && key[e] > T);
+    eq += (e < nmine && key[e] == T);
+  }
+  const uint32_t before = block_excl_scan((gt << 16) | eq, wtot);
+  const uint32_t g_before = before >> 16, e_before = before & 0xFFFFu;
+  uint32_t pos = g_before + min(need_eq, e_before);
+  uint32_t erank = e_before;
+  int32_t* out = indices + (int64_t)j * lp;
+  const bool stage = lp <= kOutStage;
+  int32_t* dst = stage ? reinterpret_cast<int32_t*>(cand) : out;  // the candidates are no longer read
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    if (e < nmine) {
+      bool sel = key[e] > T;
+      if (key[e] == T) sel = erank++ < need_eq;
+      if (sel) dst[pos++] = e0 + e;
+    }
+  }
+  if (stage) {
+    __syncthreads();
+    for (int i = tid; i < lp; i += kFT) out[i] = dst[i];
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// send[kv][j][m][:] = (kv ? V : K)[L_A + idx[j][m]][j][:]; grid (ceil(lp / rows_per_cta), hk, 2)
+template <int D>
+__global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ k,
+                                                     const uint16_t* __restrict__ v, int64_t kv_row_stride, int L_A,
+                                                     int lp, int hk, uint16_t* __restrict__ send) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the select grid's indices are visible
+  constexpr int kVec = D / 8;                         // 16-byte vectors per row
+  constexpr int kBatch = 8;
+  constexpr int kRows = 256 * kBatch / kVec;          // rows per CTA
+  const int j = blockIdx.y, kv = blockIdx.z;
+  const int r0 = blockIdx.x * kRows;
+  const uint16_t* src = (kv ? v : k) + (int64_t)j * D;
+  uint4* dst = reinterpret_cast<uint4*>(send + (((int64_t)kv * hk + j) * lp) * D);
+  uint4 buf[kBatch];
+  int rr[kBatch];
+#pragma unroll
+  for (int q = 0; q < kBatch; ++q) {
+    const int u = q * 256 + threadIdx.x;
+    const int r = r0 + u / kVec, c = u % kVec;
+    rr[q] = r < lp ? r : -1;
+    if (r < lp)
+      buf[q] = __ldg(reinterpret_cast<const uint4*>(src + (L_A + (int64_t)__ldg(idx + (int64_t)j * lp + r)) * kv_row_stride) + c);
+  }
+#pragma unroll
+  for (int q = 0; q < kBatch; ++q)
+    if (rr[q] >= 0) dst[(int64_t)rr[q] * kVec + (q * 256 + threadIdx.x) % kVec] = buf[q];
+}
+
+template <bool kSmem>
+static apb_status launch_fast(const float* scores, int l_b, int lp, int hk, int32_t* indices, cudaStream_t stream) {
+  static std::atomic<uint64_t> smem_set{0};
+  const int smem = ((kSmem ? l_b : 0) + kCand) * 4;
+  apb_status st = set_max_smem_once(reinterpret_cast<const void*>(select_fast_kernel<kSmem>),
+                                    (kMaxSmemKeys + kCand) * 4, smem_set);
+  if (st) return st;
+  select_fast_kernel<kSmem><<<hk, kFT, smem, stream>>>(scores, l_b, lp, indices);
+  return APB_OK;
+}
+
+template <int D>
+static cudaError_t launch_gather(const int32_t* idx, const void* k, const void* v, int64_t kv_row_stride, int L_A,
+                                 int lp, int hk, void* send, cudaStream_t stream) {
+  constexpr int kRows = 256 * 8 / (D / 8);
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3((lp + kRows - 1) / kRows, hk, 2);
+  c.blockDim = dim3(256);
+  c.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = &attr;
+  c.numAttrs = 1;
+  return cudaLaunchKernelEx(&c, gather_kernel<D>, idx, static_cast<const uint16_t*>(k),
+                            static_cast<const uint16_t*>(v), kv_row_stride, L_A, lp, hk, static_cast<uint16_t*>(send));
+}
+
+}  // namespace sel
+
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores, const void* k,
                                  const void* v, int64_t kv_row_stride, int32_t* indices, void* send,
                                  cudaStream_t stream) {
+  const char* env = std::getenv("APB_SELECT");
+  if (!(env && env[0] == 'l')) {
+    apb_status st = APB_OK;
+    if (l_b <= 16 * sel::kFT)
+      sel::select_reg_kernel<16><<<hk, sel::kFT, 0, stream>>>(scores, l_b, lp, indices);
+    else if (l_b <= 32 * sel::kFT)
+      sel::select_reg_kernel<32><<<hk, sel::kFT, 0, stream>>>(scores, l_b, lp, indices);
+    else
+      st = l_b <= sel::kMaxSmemKeys ? sel::launch_fast<true>(scores, l_b, lp, hk, indices, stream)
+                                    : sel::launch_fast<false>(scores, l_b, lp, hk, indices, stream);
+    if (st) return st;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("select launch: ") + cudaGetErrorString(e));
+    const char* dbg = std::getenv("APB_SELECT_DBG");  // timing experiments only: 1 = no gather
+    if (dbg && dbg[0] == '1') {
+      count_launch(1);
+      return APB_OK;
+    }
+    e = D == 128 ? sel::launch_gather<128>(indices, k, v, kv_row_stride, L_A, lp, hk, send, stream)
+                 : sel::launch_gather<64>(indices, k, v, kv_row_stride, L_A, lp, hk, send, stream);
+    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gather launch: ") + cudaGetErrorString(e));
+    count_launch(2);
+    return APB_OK;
+  }
+  // APB_SELECT=legacy: the round-1 two-kernel path (serial bin scan, one block scan per
+  // 1024 elements, one 16-byte copy per thread), kept for A/B timing; both are bit-exact
   sel::select_kernel<<<hk, sel::kThreads, 0, stream>>>(scores, l_b, lp, indices);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("select launch: ") + cudaGetErrorString(e));

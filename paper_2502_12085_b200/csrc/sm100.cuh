@@ -259,6 +259,17 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// acc (fp32 pair) += the two bf16 halves of pk, exactly as rounded (sm_100 mixed-precision
+// add.rn.f32.bf16: one FHADD.BF16 per element, the high half via an operand selector)
+__device__ __forceinline__ uint64_t f2_add_bf16x2(uint64_t acc, uint32_t pk) {
+  float lo, hi;
+  f2_unpack(acc, lo, hi);
+  unsigned short l16, h16;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(l16), "=h"(h16) : "r"(pk));
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(lo) : "h"(l16));
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(hi) : "h"(h16));
+  return f2_pack(lo, hi);
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

@@ -24,6 +24,10 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--config", default="llama8b-128k")
     ap.add_argument("--score", action="store_true", help="profile apb_retain_score instead")
+    ap.add_argument("--select", action="store_true", help="profile apb_select_topk (select + compaction) instead")
+    ap.add_argument("--queued", type=int, default=0,
+                    help="N launches queued behind a ~1 ms GPU spin between the events (device time per launch, "
+                         "no host launch overhead)")
     ap.add_argument("--trace", type=int, default=None, help="CTA index to trace (uses libapb_trace.so)")
     ap.add_argument("--ctatimes", action="store_true", help="per-CTA timeline of the last launch (libapb_trace.so): "
                     "SM utilisation, tail, gaps between CTAs on one SM")
@@ -51,7 +55,13 @@ def main():
     gathered = torch.randn((cfg.H, 2, cfg.hk, d.l_pp, cfg.d), generator=g, device=dev).bfloat16()
     ws = torch.empty(max(apb.workspace_size(d, apb.WS_ATTENTION), 16), dtype=torch.uint8, device=dev)
     loc, pas = workload.attention_flops_split(cfg.n, cfg.H, a.host, cfg.l_a, cfg.l_p, cfg.hq, cfg.d)
-    if a.score:
+    if a.select:
+        s = torch.randn((cfg.hk, d.l_b), generator=g, device=dev)
+        idx = torch.empty((cfg.hk, d.l_pp), dtype=torch.int32, device=dev)
+        send = torch.empty((2, cfg.hk, d.l_pp, cfg.d), dtype=torch.bfloat16, device=dev)
+        fn = lambda: apb.select_topk(d, s, k, v, idx, send)  # noqa: E731
+        flops = 1e6  # report ms; "TFLOP/s" column is meaningless here
+    elif a.score:
         w = apb.RetainWeights(w1=(torch.randn((cfg.d_hidden, cfg.d_in), generator=g, device=dev) * cfg.d_in ** -0.5).bfloat16(),
                               w2=torch.randn((cfg.hq, cfg.d_hidden), generator=g, device=dev) * cfg.d_hidden ** -0.5)
         s = torch.empty((cfg.hk, d.l_b), device=dev)
@@ -65,12 +75,16 @@ def main():
         fn = lambda: apb.attention_fwd(d, q, k, v, gathered, out, lse, phase, ws)  # noqa: E731
     for i in range(a.iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nq = max(a.queued, 1)
+        if a.queued:
+            torch.cuda._sleep(2_000_000)
         e0.record()
-        fn()
+        for _ in range(nq):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        print(f"iter {i}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
+        ms = e0.elapsed_time(e1) / nq
+        print(f"iter {i}: {ms:.4f} ms  {flops / ms / 1e9:.1f} TFLOP/s" + (f" ({nq} queued launches)" if a.queued else ""))
     if a.clock:
         import threading
         import pynvml
