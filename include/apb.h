@@ -143,7 +143,7 @@ apb_status apb_share_scores(const apb_dims* dims, float* scores, apb_stream_t st
  * are caller-owned bf16 device rows (16-byte aligned, row strides in ELEMENTS, multiples of
  * 8); element math is fp32 and each output is rounded once to bf16 (reading G9).  rows == 0
  * is a no-op.  Errors: APB_ERR_CONFIG for bad sizes, APB_ERR_CONTRACT for bad pointers or
- * strides (both before any launch), APB_ERR_CUDA for launch / cuBLASLt failures.
+ * strides (both before any launch), APB_ERR_CUDA for launch failures.
  *
  * apb_rmsnorm — out[r] = x[r] / sqrt(mean(x[r]^2) + eps) * w   (w: bf16 [dim]; dim % 8 == 0).
  *   x and out may alias (same rows, same stride).
@@ -155,9 +155,25 @@ apb_status apb_share_scores(const apb_dims* dims, float* scores, apb_stream_t st
  *   reduced in fp64.  head_dim even and <= 256.
  * apb_swiglu — out[r][c] = SiLU(gu[r][c]) * gu[r][inter + c]   (inter % 8 == 0).
  * apb_gemm_bf16 — C[M][N] = A[M][K] W[N][K]^T + beta * C (fp32 accumulate; beta = 1 adds the
- *   residual in place).  A plain library GEMM (cuBLASLt); ws: optional caller workspace.
+ *   residual in place): apb_gemm with the STORE (beta == 0) or RESIDUAL epilogue.  ws and
+ *   ws_bytes are ignored (kept for ABI compatibility).
  *   With beta != 0 the result is bf16(beta * C + bf16(A W^T)) — the product is rounded before
- *   the add, exactly as a bf16 PyTorch residual add (reading G20).                        */
+ *   the add, exactly as a bf16 PyTorch residual add (reading G20).
+ * apb_gemm — the same product on libapb's tcgen05 GEMM (CTA pairs, 256 x 256 tiles, TMA,
+ *   TMEM double buffering) with an elementwise step fused into its epilogue (P:708 qkv_proj +
+ *   RoPE, P:730 FFN):
+ *     STORE     C = bf16(A W^T)
+ *     RESIDUAL  C = bf16(beta * C + bf16(A W^T))                              (in place, G20)
+ *     SWIGLU    W's rows are [gate; up] interleaved in 128-row blocks (rows 256b..256b+127 =
+ *               gate rows 128b.., rows 256b+128.. = up rows 128b..); C is the activation
+ *               [M][N/2]: C[r][128b+i] = bf16(SiLU(g) * u), g, u the bf16-rounded products.
+ *               N % 256 == 0.
+ *     ROPE      C = bf16(A W^T), then the columns [0, rope_cols) (whole heads of head_dim 64 or
+ *               128, e.g. the Q and K heads of a qkv row) are rotated exactly as apb_rope does
+ *               with pos(r) = positions[r] or pos_offset + r.
+ *   M >= 0; N, K multiples of 8; A, W, C 16-byte aligned with row strides (elements) multiples
+ *   of 8.  C must not alias A or W.  Errors as above, plus APB_ERR_UNSUPPORTED for a ROPE
+ *   head_dim outside {64, 128}.                                                           */
 apb_status apb_rmsnorm(int64_t rows, int32_t dim, const void* x, int64_t x_stride, const void* w, float eps,
                        void* out, int64_t out_stride, apb_stream_t stream);
 apb_status apb_rope(int64_t rows, int32_t n_heads, int32_t head_dim, void* x, int64_t row_stride,
@@ -167,6 +183,18 @@ apb_status apb_swiglu(int64_t rows, int32_t inter, const void* gu, int64_t gu_st
 apb_status apb_gemm_bf16(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w,
                          int64_t ldw, void* c, int64_t ldc, float beta, void* ws, size_t ws_bytes,
                          apb_stream_t stream);
+typedef enum { APB_EPI_STORE = 0, APB_EPI_RESIDUAL = 1, APB_EPI_SWIGLU = 2, APB_EPI_ROPE = 3 } apb_gemm_epilogue;
+typedef struct {
+    int32_t epilogue;          /* apb_gemm_epilogue                                        */
+    float beta;                /* RESIDUAL                                                 */
+    int32_t rope_cols;         /* ROPE: rotated columns [0, rope_cols)                     */
+    int32_t head_dim;          /* ROPE: 64 or 128                                          */
+    float theta;               /* ROPE: base                                               */
+    const int32_t* positions;  /* ROPE: int32 [M] device array, or NULL                    */
+    int64_t pos_offset;        /* ROPE: pos(r) = pos_offset + r when positions == NULL     */
+} apb_gemm_epi;
+apb_status apb_gemm(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w, int64_t ldw,
+                    void* c, int64_t ldc, const apb_gemm_epi* epi, apb_stream_t stream);
 
 /* ---------------------------------------------------------------- step 3: exchange
  * One in-place AllGather of the packed compressed blocks over NCCL (the

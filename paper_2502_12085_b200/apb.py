@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_PKG, "libapb.so")
 
 OK, ERR_CONFIG, ERR_CONTRACT, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL = range(6)
 LAYOUT_BLOCK, LAYOUT_CYCLIC = 0, 1
+EPI_STORE, EPI_RESIDUAL, EPI_SWIGLU, EPI_ROPE = range(4)
 PHASE_ALL, PHASE_LOCAL, PHASE_PASSING = 0, 1, 2
 WS_RETAIN, WS_SELECT, WS_ATTENTION = 0, 1, 2
 
@@ -32,7 +33,7 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
             "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic",
             "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check", "apb_comm_abort",
-            "apb_exchange_partials_cyclic")
+            "apb_exchange_partials_cyclic", "apb_gemm")
 
 
 class ApbError(RuntimeError):
@@ -52,6 +53,12 @@ class _DecodeDims(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int32), ("host", ctypes.c_int32), ("t_new", ctypes.c_int32),
                 ("cache_len", ctypes.c_int64), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
+
+
+class _GemmEpi(ctypes.Structure):
+    _fields_ = [("epilogue", ctypes.c_int32), ("beta", ctypes.c_float), ("rope_cols", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("theta", ctypes.c_float), ("positions", ctypes.c_void_p),
+                ("pos_offset", ctypes.c_int64)]
 
 
 class _Weights(ctypes.Structure):
@@ -103,12 +110,13 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_comm_check.argtypes = [vp]
     lib.apb_comm_abort.argtypes = [vp]
     lib.apb_exchange_partials_cyclic.argtypes = [vp, i32, i64, vp, vp]
+    lib.apb_gemm.argtypes = [i64, i32, i32, vp, i64, vp, i64, vp, i64, ctypes.POINTER(_GemmEpi), vp]
     for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size",
               "apb_exchange_passing_cyclic", "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check",
-              "apb_comm_abort", "apb_exchange_partials_cyclic"):
+              "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -356,6 +364,37 @@ def gemm_bf16(a, w, c, beta: float = 0.0, ws=None, stream=None) -> None:
                                 _rowstride(w, "w"), c.data_ptr(), _rowstride(c, "c"), beta, _ptr(ws),
                                 0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
            "apb_gemm_bf16")
+
+
+def gemm(a, w, c, epilogue: int = EPI_STORE, beta: float = 1.0, rope_cols: int = 0, head_dim: int = 128,
+         theta: float = 0.0, positions=None, pos_offset: int = 0, stream=None) -> None:
+    """apb_gemm: C = A W^T on libapb's tcgen05 GEMM with a fused epilogue (EPI_STORE, EPI_RESIDUAL
+    (C = bf16(beta C + bf16(A W^T))), EPI_SWIGLU (W rows [gate; up] interleaved in 128-row blocks,
+    C = act [M][N/2]), EPI_ROPE (rotate the heads in columns [0, rope_cols))).  a bf16 [M][K],
+    w bf16 [N][K], c bf16 row-strided views."""
+    M, N, K = a.shape[0], w.shape[0], w.shape[1]
+    _need(a, "a", torch.bfloat16, M, K)
+    _need(w, "w", torch.bfloat16, N, K)
+    _need(c, "c", torch.bfloat16, M, N // 2 if epilogue == EPI_SWIGLU else N)
+    if positions is not None:
+        _need_numel(positions, "positions", torch.int32, M)
+    e = _GemmEpi(epilogue, beta if epilogue == EPI_RESIDUAL else 0.0, rope_cols, head_dim, theta, _ptr(positions),
+                 pos_offset)
+    _check(load().apb_gemm(M, N, K, a.data_ptr(), _rowstride(a, "a"), w.data_ptr(), _rowstride(w, "w"),
+                           c.data_ptr(), _rowstride(c, "c"), ctypes.byref(e), _stream(stream)), "apb_gemm")
+
+
+def interleave_gate_up(w_gu: torch.Tensor, block: int = 128) -> torch.Tensor:
+    """[W_gate; W_up] ([2I][hidden]) -> rows interleaved in `block`-row blocks, the weight layout
+    apb_gemm's SWIGLU epilogue reads (one 256-wide tile = the gate and up rows of the same 128
+    intermediate units).  A one-time weight-layout step (row permutation), not a compute step."""
+    two_i, hidden = w_gu.shape
+    inter = two_i // 2
+    if inter % block:
+        raise ApbError(ERR_CONFIG, "interleave_gate_up", f"intermediate size {inter} not a multiple of {block}")
+    g = w_gu[:inter].reshape(inter // block, block, hidden)
+    u = w_gu[inter:].reshape(inter // block, block, hidden)
+    return torch.stack([g, u], dim=1).reshape(two_i, hidden).contiguous()
 
 
 class Comm:

@@ -14,7 +14,7 @@ LIB = os.path.join(PKG, "libapb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default"]
-LIBS = ["-ldl", "-lcublasLt"]
+LIBS = ["-ldl"]
 
 
 def sources() -> list[str]:

@@ -390,19 +390,41 @@ extern "C" apb_status apb_swiglu(int64_t rows, int32_t inter, const void* gu, in
   return launch_swiglu(rows, inter, gu, gu_stride, out, out_stride, reinterpret_cast<cudaStream_t>(stream));
 }
 
-extern "C" apb_status apb_gemm_bf16(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w,
-                                    int64_t ldw, void* c, int64_t ldc, float beta, void* ws, size_t ws_bytes,
-                                    apb_stream_t stream) {
+extern "C" apb_status apb_gemm(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w,
+                               int64_t ldw, void* c, int64_t ldc, const apb_gemm_epi* epi, apb_stream_t stream) {
+  if (!epi) return fail(APB_ERR_CONTRACT, "gemm: epi is NULL");
   if (M < 0 || N <= 0 || K <= 0 || N % 8 != 0 || K % 8 != 0)
     return fail(APB_ERR_CONFIG, "gemm: M >= 0, N and K positive multiples of 8");
+  const int e = epi->epilogue;
+  if (e < APB_EPI_STORE || e > APB_EPI_ROPE) return fail(APB_ERR_CONFIG, "gemm: unknown epilogue");
+  if (e == APB_EPI_SWIGLU && N % 256 != 0)
+    return fail(APB_ERR_CONFIG, "gemm: SWIGLU needs N % 256 == 0 (gate/up rows interleaved in 128-row blocks)");
+  if (e == APB_EPI_ROPE) {
+    if (epi->head_dim != 64 && epi->head_dim != 128) return fail(APB_ERR_UNSUPPORTED, "gemm: ROPE head_dim must be 64 or 128");
+    if (epi->rope_cols < 0 || epi->rope_cols > N || epi->rope_cols % epi->head_dim || N % epi->head_dim)
+      return fail(APB_ERR_CONFIG, "gemm: ROPE needs rope_cols <= N, both multiples of head_dim");
+    if (!(epi->theta > 0.f)) return fail(APB_ERR_CONFIG, "gemm: ROPE theta must be > 0");
+  }
   apb_status st;
   if ((st = check_bf16_rows(a, M, lda, K, "a"))) return st;
   if ((st = check_bf16_rows(w, N, ldw, K, "w"))) return st;
-  if ((st = check_bf16_rows(c, M, ldc, N, "c"))) return st;
-  if (ws_bytes && !ws) return fail(APB_ERR_CONTRACT, "ws NULL with ws_bytes > 0");
+  if ((st = check_bf16_rows(c, M, ldc, e == APB_EPI_SWIGLU ? N / 2 : N, "c"))) return st;
   if (M == 0) return APB_OK;
   if ((st = check_device())) return st;
-  return launch_gemm_bf16(M, N, K, a, lda, w, ldw, c, ldc, beta, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  GemmArgs g{M, N, K, a, lda, w, ldw, c, ldc, e, epi->beta, epi->rope_cols, epi->head_dim, epi->theta,
+             epi->positions, epi->pos_offset};
+  return launch_gemm(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_gemm_bf16(int64_t M, int32_t N, int32_t K, const void* a, int64_t lda, const void* w,
+                                    int64_t ldw, void* c, int64_t ldc, float beta, void* ws, size_t ws_bytes,
+                                    apb_stream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
+  apb_gemm_epi epi{};
+  epi.epilogue = beta != 0.f ? APB_EPI_RESIDUAL : APB_EPI_STORE;
+  epi.beta = beta;
+  return apb_gemm(M, N, K, a, lda, w, ldw, c, ldc, &epi, stream);
 }
 
 // ---------------------------------------------------------------- step 3: exchange (NCCL)

@@ -1,0 +1,336 @@
+// gemm_sm100.cu — the projection GEMMs of the APB prefill layer (qkv_proj
+// P:708, O projection and FFN P:730) with their elementwise steps fused into the epilogue:
+//
+//   C[M][N] = A[M][K] W[N][K]^T          (bf16 in, fp32 accumulate in TMEM)
+//   epilogue STORE     C = bf16(acc)
+//            RESIDUAL  C = bf16(beta * C + bf16(acc))        (O / down projection + residual, G20)
+//            SWIGLU    act[r][i] = bf16(SiLU(g) * u), g = bf16(acc[gate col]), u = bf16(acc[up col])
+//                      (gate/up rows of W interleaved in 128-row blocks, so one 256-wide tile holds
+//                      the gate and up columns of the same 128 intermediate units)
+//            ROPE      C = bf16(acc), then rotate-half RoPE on the columns [0, rope_cols) (the Q and
+//                      K heads of a qkv row) with the row's position — the same arithmetic as
+//                      rope_kernel (fp64 angle reduction to [-pi, pi], then __sincosf), so the
+//                      fused and the separate paths produce the same bits
+//
+// Persistent, warp-specialised, CTA pairs (cta_group::2): a pair owns a 256 x 256 output tile
+// (each CTA 128 rows), each CTA loads its 128 rows of A and its half (128 rows) of the W tile per
+// 64-wide K block through TMA into a 6-stage ring, and the leader CTA's single MMA thread issues
+// M = 256, N = 256 tcgen05 MMAs that read both CTAs' shared memory — per SM, half of the W tile
+// is loaded, which keeps the L2 -> SM operand stream at 64 B/clk at the full MMA rate.
+// Accumulators are double-buffered in TMEM (2 x 256 columns), so the epilogue of one tile
+// (4 warps per CTA, thread = output row = TMEM lane) overlaps the next tile's MMAs.
+// Warps: 0 TMA producer, 1 MMA issuer (leader CTA), 2 TMEM allocator, 4-7 epilogue.
+#include <cmath>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace apb {
+namespace gemm {
+
+using namespace apb::sm100;
+
+constexpr int BM = 128;              // output rows per CTA (256 per pair)
+constexpr int BN = 256;              // output columns per tile
+constexpr int BK = 64;               // K block: one 128-byte swizzle atom
+constexpr int STAGES = 6;
+constexpr int kThreads = 256;
+constexpr int kABytes = BM * BK * 2;          // 16 KB
+constexpr int kBBytes = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of the W tile
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kOffBar = STAGES * kStageBytes;
+constexpr int kNumBars = 2 * STAGES + 4;      // full / empty per stage, TMEM full / empty x 2
+constexpr int kOffTmem = kOffBar + kNumBars * 8;
+constexpr int kOffInv = (kOffTmem + 16 + 7) / 8 * 8;  // fp64 RoPE inverse frequencies [64]
+constexpr int kSmem = kOffInv + 64 * 8 + 1024;
+constexpr int kGroupM = 8;                    // raster: 8 M-tiles share each W column block in turn
+static_assert(kSmem <= 232448, "shared memory");
+
+struct Params {
+  int64_t M;
+  int N, K;
+  uint16_t* c;          // output (ACT for SWIGLU) rows, ldc elements apart
+  int64_t ldc;
+  int epi;              // apb_gemm_epilogue
+  float beta;           // RESIDUAL
+  int rope_cols, head_dim;
+  const int32_t* positions;
+  int64_t pos_offset;
+  double log2_theta;
+  int num_m, num_n, num_tiles, nkb;
+};
+
+__device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
+  const int per_group = kGroupM * p.num_n;
+  const int g = t / per_group, first_m = g * kGroupM;
+  const int gs = min(kGroupM, p.num_m - first_m);
+  const int r = t - g * per_group;
+  mb = first_m + r % gs;
+  nb = r / gs;
+}
+
+__device__ __forceinline__ float bf16_round(float x) {
+  return __uint_as_float(static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(x))) << 16);
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) { return pack_bf16x2(lo, hi); }
+
+// 32 bf16 results of one thread (one row, 32 consecutive columns) -> 4 x 16-byte stores
+__device__ __forceinline__ void store32(uint16_t* dst, const float (&v)[32], int ncols) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q * 8 < ncols)
+      d4[q] = make_uint4(pack2(v[8 * q], v[8 * q + 1]), pack2(v[8 * q + 2], v[8 * q + 3]),
+                         pack2(v[8 * q + 4], v[8 * q + 5]), pack2(v[8 * q + 6], v[8 * q + 7]));
+}
+__device__ __forceinline__ void load32(const uint16_t* src, float (&v)[32], int ncols) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = q * 8 < ncols ? s4[q] : make_uint4(0, 0, 0, 0);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[8 * q + 2 * e] = __uint_as_float(w[e] << 16);
+      v[8 * q + 2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+    }
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_w, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + kOffBar;
+  auto bFull = [&](int s) { return bar0 + 8u * s; };
+  auto bEmpty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto bTFull = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
+  auto bTEmpty = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  double* inv = reinterpret_cast<double*>(smem + kOffInv);
+
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
+  const uint32_t rank = cluster_ctarank();  // 0: the MMA-issuing (leader) CTA of the pair
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bFull(s), 1);   // leader: its own expect_tx; both CTAs' TMA bytes land here
+      mbar_init(bEmpty(s), 1);  // one multicast commit from the leader's MMA thread
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bTFull(b), 1);
+      mbar_init(bTEmpty(b), 8);  // leader: one lane of each of the 2 x 4 epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(smem_u32(tmem_ptr));
+  if (p.epi == APB_EPI_ROPE && threadIdx.x < p.head_dim / 2)
+    inv[threadIdx.x] = exp2(-p.log2_theta * (2.0 * threadIdx.x) / p.head_dim);
+  tc_fence_before();
+  cluster_sync();  // barrier inits and the TMEM address visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem = warp_uniform(*tmem_ptr);
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer (both CTAs)
+    const uint32_t full_leader0 = mapa_shared(bFull(0), 0);
+    int it = 0;
+    for (int t = pair; t < p.num_tiles; t += npairs) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      const int arow = mb * 2 * BM + rank * BM, wrow = nb * BN + rank * (BN / 2);
+      for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
+        if (elect_one()) {
+          if (rank == 0) mbar_arrive_expect_tx(bFull(s), 2 * kStageBytes);
+          const uint32_t st = sbase + s * kStageBytes;
+          tma_load_2d_pair(st, &tm_a, full_leader0 + 8u * s, kb * BK, arow);
+          tma_load_2d_pair(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer (leader only)
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN, false, false);
+      int it = 0, tl = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs, ++tl) {
+        const int b = tl & 1;
+        mbar_wait(bTEmpty(b), ((tl >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(bFull(s), (it / STAGES) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t aA = sbase + s * kStageBytes, aB = aA + kABytes;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_ss_pair(tmem + b * BN, sdesc_sw128(aA + k * 32, 16, 1024), sdesc_sw128(aB + k * 32, 16, 1024), idesc,
+                          (kb > 0 || k > 0) ? 1u : 0u);
+            mma_commit_pair_mc(bEmpty(s), 0x3);  // the stage is free in both CTAs
+            if (kb == p.nkb - 1) mma_commit_pair_mc(bTFull(b), 0x3);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================================================================ epilogue (128 threads)
+    const int r = threadIdx.x - 128;  // row within this CTA's half = TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tempty_leader0 = mapa_shared(bTEmpty(0), 0);
+    int tl = 0;
+    for (int t = pair; t < p.num_tiles; t += npairs, ++tl) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      const int b = tl & 1;
+      const int64_t row = (int64_t)mb * 2 * BM + rank * BM + r;
+      const bool row_ok = row < p.M;
+      const int n0 = nb * BN;
+      const uint32_t tacc = tmem + lane_base + b * BN;
+      mbar_wait(bTFull(b), (tl >> 1) & 1);
+      tc_fence_after();
+      double posd = 0.0;
+      if (p.epi == APB_EPI_ROPE)
+        posd = row_ok ? (p.positions ? (double)p.positions[row] : (double)(p.pos_offset + row)) : 0.0;
+      if (p.epi == APB_EPI_SWIGLU) {
+        // gate columns [0,128) and up columns [128,256) of this tile -> act columns n0/2 + [0,128)
+        const int a0 = n0 / 2;
+        uint16_t* dst = p.c + row * p.ldc + a0;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tacc + c * 32, g);
+          tmem_ld32(tacc + 128 + c * 32, u);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float gf = bf16_round(__uint_as_float(g[e])), uf = bf16_round(__uint_as_float(u[e]));
+            v[e] = gf / (1.f + __expf(-gf)) * uf;
+          }
+          if (row_ok) store32(dst + c * 32, v, min(32, p.N / 2 - (a0 + c * 32)));
+        }
+      } else if (p.epi == APB_EPI_ROPE) {
+        // the angles of a row depend only on (position, i < head_dim/2): computed once per tile
+        // per 32-wide i chunk and applied to every head of the tile
+        const int hd = p.head_dim, half = hd / 2;
+        uint16_t* dst = p.c + row * p.ldc + n0;
+#pragma unroll 1
+        for (int c = 0; c < half; c += 32) {
+          float cs[32], sn[32];
+          if (n0 < p.rope_cols) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              double a = posd * inv[c + e];
+              a -= rint(a * 0.15915494309189535) * 6.283185307179586;  // |a| <= pi
+              __sincosf(static_cast<float>(a), &sn[e], &cs[e]);
+            }
+          }
+#pragma unroll 1
+          for (int h0 = 0; h0 < BN; h0 += hd) {
+            const bool rot = n0 + h0 < p.rope_cols;  // warp-uniform
+            uint32_t x1[32], x2[32];
+            tmem_ld32(tacc + h0 + c, x1);
+            tmem_ld32(tacc + h0 + half + c, x2);
+            tmem_wait_ld();
+            float o1[32], o2[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const float f1 = bf16_round(__uint_as_float(x1[e])), f2 = bf16_round(__uint_as_float(x2[e]));
+              o1[e] = rot ? f1 * cs[e] - f2 * sn[e] : f1;
+              o2[e] = rot ? f2 * cs[e] + f1 * sn[e] : f2;
+            }
+            if (row_ok) {
+              store32(dst + h0 + c, o1, min(32, p.N - (n0 + h0 + c)));
+              store32(dst + h0 + half + c, o2, min(32, p.N - (n0 + h0 + half + c)));
+            }
+          }
+        }
+      } else {
+        uint16_t* dst = p.c + row * p.ldc + n0;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          const int ncols = min(32, p.N - (n0 + c));
+          float old[32];
+          if (p.epi == APB_EPI_RESIDUAL && row_ok && ncols > 0) load32(dst + c, old, ncols);
+          uint32_t acc[32];
+          tmem_ld32(tacc + c, acc);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float prod = bf16_round(__uint_as_float(acc[e]));
+            v[e] = p.epi == APB_EPI_RESIDUAL ? p.beta * old[e] + prod : prod;
+          }
+          if (row_ok && ncols > 0) store32(dst + c, v, ncols);
+        }
+      }
+      // this tile's accumulator is in registers / stored: release the TMEM buffer to the leader
+      tc_fence_before();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_leader0 + 8u * b);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs done: no MMA reads the peer's smem, no arrive targets an exited CTA
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
+}  // namespace gemm
+
+apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
+  using namespace gemm;
+  CUtensorMap ta, tw;
+  {
+    uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.M};
+    uint64_t str[1] = {(uint64_t)g.lda * 2};
+    uint32_t box[2] = {BK, BM};
+    if (!make_tmap_bf16(&ta, g.a, 2, dims, str, box)) return APB_ERR_CUDA;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.N};
+    uint64_t str[1] = {(uint64_t)g.ldw * 2};
+    uint32_t box[2] = {BK, BN / 2};
+    if (!make_tmap_bf16(&tw, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
+  }
+  Params p{};
+  p.M = g.M;
+  p.N = g.N;
+  p.K = g.K;
+  p.c = static_cast<uint16_t*>(g.c);
+  p.ldc = g.ldc;
+  p.epi = g.epi;
+  p.beta = g.beta;
+  p.rope_cols = g.rope_cols;
+  p.head_dim = g.head_dim > 0 ? g.head_dim : 128;
+  p.positions = g.positions;
+  p.pos_offset = g.pos_offset;
+  p.log2_theta = g.theta > 0.f ? std::log2((double)g.theta) : 0.0;
+  p.num_m = (int)((g.M + 2 * BM - 1) / (2 * BM));
+  p.num_n = (g.N + BN - 1) / BN;
+  p.num_tiles = p.num_m * p.num_n;
+  p.nkb = (g.K + BK - 1) / BK;
+  static std::atomic<uint64_t> smem_set{0};
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel), kSmem, smem_set)) return st;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int pairs = std::min(p.num_tiles, sms / 2);
+  gemm_kernel<<<2 * pairs, kThreads, kSmem, stream>>>(ta, tw, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+}  // namespace apb

@@ -66,8 +66,23 @@ apb_status launch_rope(int64_t rows, int n_heads, int d, void* x, int64_t row_st
                        int64_t pos_offset, double theta, cudaStream_t stream);
 apb_status launch_swiglu(int64_t rows, int inter, const void* gu, int64_t gs, void* out, int64_t os,
                          cudaStream_t stream);
-apb_status launch_gemm_bf16(int64_t M, int N, int K, const void* a, int64_t lda, const void* w, int64_t ldw, void* c,
-                            int64_t ldc, float beta, void* ws, size_t ws_bytes, cudaStream_t stream);
+struct GemmArgs {
+  int64_t M;
+  int N, K;
+  const void* a;
+  int64_t lda;
+  const void* w;
+  int64_t ldw;
+  void* c;
+  int64_t ldc;
+  int epi;  // apb_gemm_epilogue
+  float beta;
+  int rope_cols, head_dim;
+  float theta;
+  const int32_t* positions;
+  int64_t pos_offset;
+};
+apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream);
 apb_status launch_random_scores(uint64_t seed, uint64_t c0, int64_t count, float* scores, cudaStream_t stream);
 apb_status launch_share_scores(float* scores, int hk, int l_b, cudaStream_t stream);
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores,

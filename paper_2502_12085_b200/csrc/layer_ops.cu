@@ -5,15 +5,11 @@
 //   rope_kernel     in-place rotate-half RoPE on the Q and K heads of each qkv row, 16-byte
 //                   accesses (reading G19: position = caller array, or pos_offset + row)   HBM-bound
 //   swiglu_kernel   a = SiLU(g) * u for [g | u] rows                      HBM-bound
-//   apb_gemm_bf16   C = A W^T (+ beta C): cuBLASLt, bf16 in / fp32 accumulate / bf16 out — a
-//                   plain library GEMM (the projections carry no APB-specific structure)
+//   (the projection GEMMs and their fused epilogues are in gemm_sm100.cu)
 //
 // All element math is fp32; every output is rounded once to bf16 (reading G9).
-#include <cublasLt.h>
 #include <cuda_bf16.h>
 
-#include <mutex>
-#include <unordered_map>
 
 #include "internal.h"
 
@@ -75,7 +71,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const uint16_t* __restrict
 
 // kRopeRows rows per CTA: the d/2 inverse frequencies theta^(-2i/d) once per CTA in fp64; per row
 // the angles pos * inv_freq are reduced mod 2*pi in fp64 (positions reach 10^6: fp32 angles would
-// be off by O(0.1) rad), then sin/cos in fp32.  Each thread rotates 8 consecutive pairs
+// be off by O(0.1) rad), then sin/cos in fp32 (__sincosf on the reduced angle; the fused ROPE
+// epilogue of apb_gemm computes the same bits).  Each thread rotates 8 consecutive pairs
 // (x_i, x_{i+d/2}) of one head with 16-byte loads / stores (d % 16 == 0), else one pair.
 constexpr int kRopeRows = 4;
 __global__ void __launch_bounds__(256) rope_kernel(uint16_t* __restrict__ x, int64_t row_stride, int64_t rows,
@@ -95,7 +92,7 @@ __global__ void __launch_bounds__(256) rope_kernel(uint16_t* __restrict__ x, int
     double a = pos * inv[i];
     a -= rint(a * 0.15915494309189535) * 6.283185307179586;  // |a| <= pi
     float sn, c;
-    sincosf(static_cast<float>(a), &sn, &c);
+    __sincosf(static_cast<float>(a), &sn, &c);  // |a| <= pi: MUFU sin/cos, abs. error ~2^-21 << bf16's 2^-9
     cs[rr][0][i] = c;
     cs[rr][1][i] = sn;
   }
@@ -187,75 +184,6 @@ apb_status launch_swiglu(int64_t rows, int inter, const void* gu, int64_t gs, vo
                                                             static_cast<uint16_t*>(out), os, rows);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("swiglu launch: ") + cudaGetErrorString(e));
-  count_launch();
-  return APB_OK;
-}
-
-// ---------------------------------------------------------------- cuBLASLt GEMM
-namespace {
-struct GemmKey {
-  int64_t M, lda, ldw, ldc;
-  int32_t N, K;
-  bool beta;
-  size_t ws;
-  bool operator==(const GemmKey& o) const {
-    return M == o.M && lda == o.lda && ldw == o.ldw && ldc == o.ldc && N == o.N && K == o.K && beta == o.beta &&
-           ws == o.ws;
-  }
-};
-struct GemmKeyHash {
-  size_t operator()(const GemmKey& k) const {
-    size_t h = std::hash<int64_t>()(k.M);
-    for (int64_t v : {k.lda, k.ldw, k.ldc, (int64_t)k.N, (int64_t)k.K, (int64_t)k.beta, (int64_t)k.ws})
-      h = h * 1000003u ^ std::hash<int64_t>()(v);
-    return h;
-  }
-};
-struct GemmPlan {
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
-  cublasLtMatmulAlgo_t algo;
-};
-std::mutex g_gemm_mu;
-cublasLtHandle_t g_lt = nullptr;
-std::unordered_map<GemmKey, GemmPlan, GemmKeyHash> g_plans;
-}  // namespace
-
-apb_status launch_gemm_bf16(int64_t M, int N, int K, const void* a, int64_t lda, const void* w, int64_t ldw, void* c,
-                            int64_t ldc, float beta, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  // Row-major C[M][N] = A[M][K] W[N][K]^T  <=>  column-major C^T (N x M) = W^T(op T on the
-  // K x N column-major view of W) * A (K x M column-major view of A).
-  std::lock_guard<std::mutex> lock(g_gemm_mu);
-  if (!g_lt && cublasLtCreate(&g_lt) != CUBLAS_STATUS_SUCCESS) return fail(APB_ERR_CUDA, "cublasLtCreate failed");
-  const GemmKey key{M, lda, ldw, ldc, N, K, beta != 0.f, ws_bytes};
-  auto it = g_plans.find(key);
-  if (it == g_plans.end()) {
-    GemmPlan pl;
-    bool ok = cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS;
-    const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-    ok = ok && cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)) == CUBLAS_STATUS_SUCCESS;
-    ok = ok && cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)) == CUBLAS_STATUS_SUCCESS;
-    ok = ok && cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_16BF, K, N, ldw) == CUBLAS_STATUS_SUCCESS;
-    ok = ok && cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_16BF, K, M, lda) == CUBLAS_STATUS_SUCCESS;
-    ok = ok && cublasLtMatrixLayoutCreate(&pl.c, CUDA_R_16BF, N, M, ldc) == CUBLAS_STATUS_SUCCESS;
-    cublasLtMatmulPreference_t pref = nullptr;
-    ok = ok && cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS;
-    ok = ok && cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes,
-                                                    sizeof(ws_bytes)) == CUBLAS_STATUS_SUCCESS;
-    cublasLtMatmulHeuristicResult_t res;
-    int n = 0;
-    ok = ok && cublasLtMatmulAlgoGetHeuristic(g_lt, pl.op, pl.a, pl.b, pl.c, pl.c, pref, 1, &res, &n) ==
-                   CUBLAS_STATUS_SUCCESS && n > 0;
-    if (pref) cublasLtMatmulPreferenceDestroy(pref);
-    if (!ok) return fail(APB_ERR_CUDA, "cuBLASLt: no bf16 GEMM algorithm for this shape");
-    pl.algo = res.algo;
-    it = g_plans.emplace(key, pl).first;
-  }
-  const GemmPlan& pl = it->second;
-  const float alpha = 1.f;
-  cublasStatus_t st = cublasLtMatmul(g_lt, pl.op, &alpha, w, pl.a, a, pl.b, &beta, c, pl.c, c, pl.c, &pl.algo, ws,
-                                     ws_bytes, stream);
-  if (st != CUBLAS_STATUS_SUCCESS) return fail(APB_ERR_CUDA, "cublasLtMatmul failed: status " + std::to_string((int)st));
   count_launch();
   return APB_OK;
 }
