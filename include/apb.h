@@ -75,7 +75,7 @@ typedef struct {
 /* Retaining-head weights of one layer (hidden size d_hidden = 1024 at P:798).
  *   z = W1 x + b1,  a = SiLU(z),  o = W2 a + b2,  s[j] = max_{c in group j} o[c]   (G2, G4)
  *  d_in      must equal (n_heads + 2 n_kv_heads) * head_dim (x = [Q_t | K_t | V_t])
- *  d_hidden  multiple of 128
+ *  d_hidden  multiple of 256
  *  n_out     n_kv_heads (identity pool) or n_heads (max over each KV head's query group)
  *  w1  bf16 [d_hidden][d_in] row-major (device);  b1 fp32 [d_hidden] or NULL;
  *  w2  fp32 [n_out][d_hidden] row-major;          b2 fp32 [n_out] or NULL.            */
@@ -102,11 +102,18 @@ typedef enum { APB_WS_RETAIN = 0, APB_WS_SELECT = 1, APB_WS_ATTENTION = 2 } apb_
 /* ---------------------------------------------------------------- step 1: scoring
  * scores[j][t] (fp32 [n_kv_heads][l_b]) for block rows t = L_A .. L_A+l_b-1 of q/k/v.
  * Kernel: tcgen05 GEMM (A = [Q|K|V] rows via three TMA maps, B = W1) with a fused fp32
- * epilogue (b1, SiLU, W2 dot, b2, group max).  Deterministic (no atomics).          */
+ * epilogue (b1, SiLU, W2 dot), then b2 and the group max.  Deterministic (no atomics).
+ * ws: caller-owned device workspace of apb_retain_workspace_size() bytes (16-byte aligned;
+ * fp32 partial W2 sums [d_hidden/256][l_b][n_out]).  With it the CTA-pair GEMM runs (each
+ * pair 256 tokens x 256 hidden units, the [Q|K|V] rows read from HBM about once); with ws ==
+ * NULL (or too small) a single-CTA kernel (128 tokens x all of d_hidden) computes the same
+ * definition in its own fixed summation order.  d_hidden % 256 == 0 and n_out <= 64, else
+ * APB_ERR_UNSUPPORTED.                                                                   */
 apb_status apb_retain_score(const apb_dims* dims, const apb_retain_weights* w,
                             const void* q, const void* k, const void* v,
                             int64_t q_row_stride, int64_t kv_row_stride,
                             float* scores, void* ws, size_t ws_bytes, apb_stream_t stream);
+apb_status apb_retain_workspace_size(const apb_dims* dims, const apb_retain_weights* w, size_t* bytes);
 
 /* ---------------------------------------------------------------- step 2: select + compact
  * For each KV head j: idx[j] = the l_p' block indices with the largest scores[j][.]

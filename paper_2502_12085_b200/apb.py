@@ -33,7 +33,7 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
             "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic",
             "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check", "apb_comm_abort",
-            "apb_exchange_partials_cyclic", "apb_gemm")
+            "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size")
 
 
 class ApbError(RuntimeError):
@@ -110,13 +110,14 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_comm_check.argtypes = [vp]
     lib.apb_comm_abort.argtypes = [vp]
     lib.apb_exchange_partials_cyclic.argtypes = [vp, i32, i64, vp, vp]
+    lib.apb_retain_workspace_size.argtypes = [dp, ctypes.POINTER(_Weights), ctypes.POINTER(sz)]
     lib.apb_gemm.argtypes = [i64, i32, i32, vp, i64, vp, i64, vp, i64, ctypes.POINTER(_GemmEpi), vp]
     for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
               "apb_comm_get_unique_id", "apb_comm_init", "apb_comm_destroy", "apb_workspace_size",
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size",
               "apb_exchange_passing_cyclic", "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check",
-              "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm"):
+              "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -273,7 +274,17 @@ def check_dims(dims: Dims) -> None:
     _check(load().apb_check_dims(ctypes.byref(d)), "apb_check_dims")
 
 
-def retain_score(dims: Dims, w: RetainWeights, q, k, v, scores, stream=None) -> None:
+def retain_workspace_size(dims: Dims, w: RetainWeights) -> int:
+    out = ctypes.c_size_t(0)
+    d, wc = dims.c(), w.c()
+    _check(load().apb_retain_workspace_size(ctypes.byref(d), ctypes.byref(wc), ctypes.byref(out)),
+           "apb_retain_workspace_size")
+    return out.value
+
+
+def retain_score(dims: Dims, w: RetainWeights, q, k, v, scores, stream=None, ws="auto") -> None:
+    """ws: device workspace (apb_retain_workspace_size bytes) for the CTA-pair GEMM; "auto"
+    allocates it (torch caching allocator, on q's device); None runs the single-CTA kernel."""
     _check_qkv(dims, q, k, v)
     _need_numel(scores, "scores", torch.float32, dims.n_kv_heads * dims.l_b)
     _need(w.w1, "w1", torch.bfloat16, dense=True)
@@ -283,10 +294,13 @@ def retain_score(dims: Dims, w: RetainWeights, q, k, v, scores, stream=None) -> 
             _need(b, nm, torch.float32, dense=True)
     if w.w2.dim() != 2 or w.w2.shape[1] != w.w1.shape[0]:
         raise ApbError(ERR_CONTRACT, "w2", "must be [n_out][d_hidden]")
+    if isinstance(ws, str):
+        ws = torch.empty(max(retain_workspace_size(dims, w), 16), dtype=torch.uint8, device=q.device)
     d, wc = dims.c(), w.c()
     _check(load().apb_retain_score(ctypes.byref(d), ctypes.byref(wc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                   _rowstride(q, "q"), _rowstride(k, "k"), scores.data_ptr(), None, 0,
-                                   _stream(stream)), "apb_retain_score")
+                                   _rowstride(q, "q"), _rowstride(k, "k"), scores.data_ptr(), _ptr(ws),
+                                   0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+           "apb_retain_score")
 
 
 def select_topk(dims: Dims, scores, k, v, indices, send, stream=None) -> None:

@@ -245,11 +245,21 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
 }
 
 // ---------------------------------------------------------------- step 1: scoring
+static size_t retain_ws_bytes(const apb_dims* d, const apb_retain_weights* w) {
+  return (size_t)((w->d_hidden + 255) / 256) * (size_t)d->l_b * (size_t)w->n_out * sizeof(float);
+}
+
+extern "C" apb_status apb_retain_workspace_size(const apb_dims* d, const apb_retain_weights* w, size_t* bytes) {
+  if (!bytes || !w) return fail(APB_ERR_CONTRACT, "bytes/weights is NULL");
+  apb_status st = check_dims(d);
+  if (st) return st;
+  *bytes = retain_ws_bytes(d, w);
+  return APB_OK;
+}
+
 extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weights* w, const void* q, const void* k,
                                        const void* v, int64_t q_row_stride, int64_t kv_row_stride, float* scores,
                                        void* ws, size_t ws_bytes, apb_stream_t stream) {
-  (void)ws;
-  (void)ws_bytes;
   apb_status st = check_dims(d);
   if (st) return st;
   if (!w) return fail(APB_ERR_CONTRACT, "weights is NULL");
@@ -292,6 +302,18 @@ extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weigh
     uint64_t str[1] = {(uint64_t)kv_row_stride * 2};
     if (!make_tmap_bf16(&tk, k, 2, dims, str, box)) return APB_ERR_CUDA;
     if (!make_tmap_bf16(&tv, v, 2, dims, str, box)) return APB_ERR_CUDA;
+  }
+  // the CTA-pair GEMM (pair = 256 tokens x 256 hidden units, partials reduced by a fixed-order
+  // finalize) whenever the caller provides its workspace, unless APB_SCORE_PLAN selects one of the
+  // round-1 single-CTA plans ("legacy" / "s3" / "p2", kept for A/B timing)
+  const char* plan = std::getenv("APB_SCORE_PLAN");
+  const bool legacy = plan && plan[0] != '\0';
+  if (!legacy && ws && ws_bytes >= retain_ws_bytes(d, w) && aligned16(ws)) {
+    uint64_t dims[2] = {(uint64_t)w->d_in, (uint64_t)w->d_hidden};
+    uint64_t str[1] = {(uint64_t)w->d_in * 2};
+    uint32_t wbox[2] = {64, 128};  // this CTA's half (128 rows) of a 256-row W1 tile
+    if (!make_tmap_bf16(&tw, w->w1, 2, dims, str, wbox)) return APB_ERR_CUDA;
+    return launch_score_gemm(p, tq, tk, tv, tw, static_cast<float*>(ws), reinterpret_cast<cudaStream_t>(stream));
   }
   {
     uint64_t dims[2] = {(uint64_t)w->d_in, (uint64_t)w->d_hidden};

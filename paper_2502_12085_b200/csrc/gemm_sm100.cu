@@ -43,7 +43,13 @@ constexpr int kNumBars = 2 * STAGES + 4;      // full / empty per stage, TMEM fu
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kOffInv = (kOffTmem + 16 + 7) / 8 * 8;  // fp64 RoPE inverse frequencies [64]
 constexpr int kSmem = kOffInv + 64 * 8 + 1024;
+// retaining-head scoring (SCORE): a W2 slice [32 outputs][256 hidden] fp32 and b1 [256]
+constexpr int kOffW2 = kOffInv + 64 * 8;
+constexpr int kOffB1 = kOffW2 + 32 * BN * 4;
+constexpr int kSmemScore = kOffB1 + BN * 4 + 1024;
+static_assert(kSmemScore <= 232448, "shared memory (score)");
 constexpr int kGroupM = 8;                    // raster: 8 M-tiles share each W column block in turn
+constexpr int kEpiScore = 100;                // internal epilogue: retaining-head partial scores
 static_assert(kSmem <= 232448, "shared memory");
 
 struct Params {
@@ -58,6 +64,14 @@ struct Params {
   int64_t pos_offset;
   double log2_theta;
   int num_m, num_n, num_tiles, nkb;
+  // A from up to three row-aligned maps ([Q | K | V] for the retaining head): K blocks [0, kq) from
+  // map 0, [kq, kqk) from map 1, the rest from map 2; A's row coordinate is a_row0 + row
+  int kq, kqk, a_row0;
+  // SCORE: partial[nb][row][n_out] = W2[:, nb*256 .. +256] SiLU(acc + b1[...])  (fp32)
+  const float* b1;
+  const float* w2;
+  int n_out, d_hidden;
+  float* part;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
@@ -98,7 +112,8 @@ __device__ __forceinline__ void load32(const uint16_t* src, float (&v)[32], int 
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_w, const Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a1,
+                const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_w, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
@@ -139,14 +154,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int t = pair; t < p.num_tiles; t += npairs) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
-      const int arow = mb * 2 * BM + rank * BM, wrow = nb * BN + rank * (BN / 2);
+      const int arow = p.a_row0 + mb * 2 * BM + rank * BM, wrow = nb * BN + rank * (BN / 2);
       for (int kb = 0; kb < p.nkb; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
         if (elect_one()) {
           if (rank == 0) mbar_arrive_expect_tx(bFull(s), 2 * kStageBytes);
           const uint32_t st = sbase + s * kStageBytes;
-          tma_load_2d_pair(st, &tm_a, full_leader0 + 8u * s, kb * BK, arow);
+          if (kb < p.kq)
+            tma_load_2d_pair(st, &tm_a, full_leader0 + 8u * s, kb * BK, arow);
+          else if (kb < p.kqk)
+            tma_load_2d_pair(st, &tm_a1, full_leader0 + 8u * s, (kb - p.kq) * BK, arow);
+          else
+            tma_load_2d_pair(st, &tm_a2, full_leader0 + 8u * s, (kb - p.kqk) * BK, arow);
           tma_load_2d_pair(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow);
         }
         __syncwarp();
@@ -197,7 +217,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       double posd = 0.0;
       if (p.epi == APB_EPI_ROPE)
         posd = row_ok ? (p.positions ? (double)p.positions[row] : (double)(p.pos_offset + row)) : 0.0;
-      if (p.epi == APB_EPI_SWIGLU) {
+      if (p.epi == kEpiScore) {
+        // retaining head (reading G2): a = SiLU(z + b1) for this tile's 256 hidden
+        // units, partial o[oc] = sum_h W2[oc][h] a_h in fp32 (fixed order: chunks of 32 in
+        // column order, packed FFMA2 pairs) -> part[nb][row][oc]; score_finalize_kernel sums the
+        // d_hidden / 256 partials in nb order.  32 outputs per pass over the TMEM tile.
+        float* w2s = reinterpret_cast<float*>(smem + kOffW2);
+        float* b1s = reinterpret_cast<float*>(smem + kOffB1);
+        named_bar_sync(1, 128);  // the previous tile's readers of w2s / b1s are done
+        b1s[r] = p.b1 ? __ldg(p.b1 + n0 + r) : 0.f;
+        b1s[r + 128] = p.b1 ? __ldg(p.b1 + n0 + 128 + r) : 0.f;
+#pragma unroll 1
+        for (int og = 0; og < p.n_out; og += 32) {
+          const int no = min(32, p.n_out - og);
+          if (og > 0) named_bar_sync(1, 128);
+          for (int idx = r; idx < no * (BN / 4); idx += 128) {
+            const int oc = idx / (BN / 4), c4 = idx % (BN / 4);
+            reinterpret_cast<float4*>(w2s + oc * BN)[c4] =
+                __ldg(reinterpret_cast<const float4*>(p.w2 + (size_t)(og + oc) * p.d_hidden + n0) + c4);
+          }
+          named_bar_sync(1, 128);
+          float o[32];
+#pragma unroll
+          for (int oc = 0; oc < 32; ++oc) o[oc] = 0.f;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t zr[32];
+            tmem_ld32(tacc + c, zr);
+            tmem_wait_ld();
+            uint64_t a2[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float z0 = __uint_as_float(zr[2 * e]) + b1s[c + 2 * e];
+              const float z1 = __uint_as_float(zr[2 * e + 1]) + b1s[c + 2 * e + 1];
+              a2[e] = f2_pack(__fdividef(z0, 1.f + __expf(-z0)), __fdividef(z1, 1.f + __expf(-z1)));
+            }
+#pragma unroll
+            for (int oc = 0; oc < 32; ++oc) {
+              if (oc < no) {
+                const ulonglong2* w = reinterpret_cast<const ulonglong2*>(w2s + oc * BN + c);
+                uint64_t acc01 = 0ull, acc23 = 0ull;
+#pragma unroll
+                for (int e4 = 0; e4 < 8; ++e4) {
+                  const ulonglong2 wv = w[e4];
+                  acc01 = ffma2(wv.x, a2[2 * e4], acc01);
+                  acc23 = ffma2(wv.y, a2[2 * e4 + 1], acc23);
+                }
+                float x0, x1, y0, y1;
+                f2_unpack(acc01, x0, x1);
+                f2_unpack(acc23, y0, y1);
+                o[oc] += (x0 + x1) + (y0 + y1);
+              }
+            }
+          }
+          if (row_ok) {
+            float* dst = p.part + ((int64_t)nb * p.M + row) * p.n_out + og;
+#pragma unroll
+            for (int oc = 0; oc < 32; ++oc)
+              if (oc < no) dst[oc] = o[oc];
+          }
+        }
+      } else if (p.epi == APB_EPI_SWIGLU) {
         // gate columns [0,128) and up columns [128,256) of this tile -> act columns n0/2 + [0,128)
         const int a0 = n0 / 2;
         uint16_t* dst = p.c + row * p.ldc + a0;
@@ -286,6 +366,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtensorMap& ta1, const CUtensorMap& ta2,
+                                const CUtensorMap& tw, int smem, cudaStream_t stream) {
+  p.num_m = (int)((p.M + 2 * BM - 1) / (2 * BM));
+  p.num_n = (p.N + BN - 1) / BN;
+  p.num_tiles = p.num_m * p.num_n;
+  p.nkb = (p.K + BK - 1) / BK;
+  static std::atomic<uint64_t> smem_set{0};
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel), kSmemScore, smem_set)) return st;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int pairs = std::min(p.num_tiles, sms / 2);
+  gemm_kernel<<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
+  count_launch();
+  return APB_OK;
+}
+
+// score_finalize_kernel: o[oc] = b2[oc] + sum_nb part[nb][t][oc] (nb order), s[j][t] = max over the
+// r = n_out / hk outputs of KV head j (reading G4).  One thread per block token.
+__global__ void __launch_bounds__(256) score_finalize_kernel(const float* __restrict__ part, int l_b, int n_parts,
+                                                             int n_out, int hk, const float* __restrict__ b2,
+                                                             float* __restrict__ scores) {
+  const int t = blockIdx.x * 256 + threadIdx.x;
+  if (t >= l_b) return;
+  const int rr = n_out / hk;
+  for (int j = 0; j < hk; ++j) {
+    float m = -INFINITY;
+    for (int c = 0; c < rr; ++c) {
+      const int oc = j * rr + c;
+      float o = 0.f;
+      for (int nb = 0; nb < n_parts; ++nb) o += __ldg(part + ((int64_t)nb * l_b + t) * n_out + oc);
+      m = fmaxf(m, o + (b2 ? __ldg(b2 + oc) : 0.f));
+    }
+    scores[(int64_t)j * l_b + t] = m;
+  }
+}
+
 }  // namespace gemm
 
 apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
@@ -316,19 +435,32 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   p.positions = g.positions;
   p.pos_offset = g.pos_offset;
   p.log2_theta = g.theta > 0.f ? std::log2((double)g.theta) : 0.0;
-  p.num_m = (int)((g.M + 2 * BM - 1) / (2 * BM));
-  p.num_n = (g.N + BN - 1) / BN;
-  p.num_tiles = p.num_m * p.num_n;
-  p.nkb = (g.K + BK - 1) / BK;
-  static std::atomic<uint64_t> smem_set{0};
-  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel), kSmem, smem_set)) return st;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int pairs = std::min(p.num_tiles, sms / 2);
-  gemm_kernel<<<2 * pairs, kThreads, kSmem, stream>>>(ta, tw, p);
+  p.kq = p.kqk = (g.K + BK - 1) / BK;
+  return launch_params(p, ta, ta, ta, tw, kSmem, stream);
+}
+
+apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const CUtensorMap& tw1, float* part, cudaStream_t stream) {
+  using namespace gemm;
+  Params p{};
+  p.M = sp.l_b;
+  p.N = sp.d_hidden;
+  p.K = sp.d_in;
+  p.epi = kEpiScore;
+  p.kq = sp.kq;
+  p.kqk = sp.kq + sp.kk;
+  p.a_row0 = sp.L_A;
+  p.b1 = sp.b1;
+  p.w2 = sp.w2;
+  p.n_out = sp.n_out;
+  p.d_hidden = sp.d_hidden;
+  p.part = part;
+  if (apb_status st = launch_params(p, tq, tk, tv, tw1, kSmemScore, stream)) return st;
+  const int n_parts = (sp.d_hidden + BN - 1) / BN;
+  score_finalize_kernel<<<(sp.l_b + 255) / 256, 256, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
+                                                                   sp.scores);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("score_finalize launch: ") + cudaGetErrorString(e));
   count_launch();
   return APB_OK;
 }

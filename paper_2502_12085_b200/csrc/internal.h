@@ -58,6 +58,10 @@ struct ScoreParams {
 };
 apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream);
+// CTA-pair GEMM form (gemm_sm100.cu): partials [d_hidden/256][l_b][n_out] in `part`, then a
+// fixed-order finalize (tw1: box {64, 128})
+apb_status launch_score_gemm(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const CUtensorMap& tw1, float* part, cudaStream_t stream);
 
 // ---------------------------------------------------------------- selection + compaction
 apb_status launch_rmsnorm(int64_t rows, int dim, const void* x, int64_t xs, const void* w, float eps, void* y,

@@ -279,6 +279,7 @@ static apb_status launch(const ScoreParams& p, const CUtensorMap& tq, const CUte
 apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream) {
   // APB_SCORE_PLAN (timing experiments): "s3" forces the 3-stage plan, "p2" two chunks per pass
+  // (any other value, e.g. "legacy": the default single-CTA plan)
   const char* plan = std::getenv("APB_SCORE_PLAN");
   const bool force3 = plan && plan[0] == 's' && plan[1] == '3';
   const bool pass2 = plan && plan[0] == 'p' && plan[1] == '2';

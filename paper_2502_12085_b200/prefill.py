@@ -79,6 +79,7 @@ class PrefillRank:
         self.scores = {h: torch.empty((hk, b.l_b), dtype=torch.float32, device=self.device) for h in hosts}
         self.indices = {h: torch.empty((hk, max(lpp, 1)), dtype=torch.int32, device=self.device) for h in hosts}
         self.ws = {}
+        self.score_ws = {}  # retaining-head partial sums, sized by the weights on first use
         for h in hosts:
             n = apb.workspace_size(b.with_host(h), apb.WS_ATTENTION)
             self.ws[h] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device) if n else None
@@ -111,8 +112,11 @@ class PrefillRank:
             self._op("score", h, stream, lambda: apb.random_scores(d, self.seed, layer_idx, self.scores[h],
                                                                    stream=stream))
         else:
+            n = apb.retain_workspace_size(d, weights)
+            if self.score_ws.get(h) is None or self.score_ws[h].numel() < n:
+                self.score_ws[h] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device)
             self._op("score", h, stream, lambda: apb.retain_score(d, weights, x.q, x.k, x.v, self.scores[h],
-                                                                  stream=stream))
+                                                                  stream=stream, ws=self.score_ws[h]))
         if self.shared_set:
             apb.share_scores(d, self.scores[h], stream=stream)
         self._op("select_compact", h, stream, lambda: apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h],

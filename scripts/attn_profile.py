@@ -65,7 +65,8 @@ def main():
         w = apb.RetainWeights(w1=(torch.randn((cfg.d_hidden, cfg.d_in), generator=g, device=dev) * cfg.d_in ** -0.5).bfloat16(),
                               w2=torch.randn((cfg.hq, cfg.d_hidden), generator=g, device=dev) * cfg.d_hidden ** -0.5)
         s = torch.empty((cfg.hk, d.l_b), device=dev)
-        fn = lambda: apb.retain_score(d, w, q, k, v, s)  # noqa: E731
+        sws = torch.empty(apb.retain_workspace_size(d, w), dtype=torch.uint8, device=dev)
+        fn = lambda: apb.retain_score(d, w, q, k, v, s, ws=sws)  # noqa: E731
         flops = workload.score_flops(d.l_b, cfg.d_in, cfg.d_hidden, cfg.hq)
     else:
         phase = {"local": apb.PHASE_LOCAL, "passing": apb.PHASE_PASSING, "all": apb.PHASE_ALL}[a.phase]

@@ -29,8 +29,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", type=int, default=20480)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--square", type=int, default=0, help="also time an NxNxN STORE GEMM (e.g. 8192)")
     a = ap.parse_args()
     apb.load()
+    if a.square:
+        n = a.square
+        g0 = torch.Generator(device="cuda")
+        g0.manual_seed(1)
+        A = torch.randn(n, n, generator=g0, device="cuda").to(torch.bfloat16)
+        B = torch.randn(n, n, generator=g0, device="cuda").to(torch.bfloat16)
+        C = torch.empty(n, n, dtype=torch.bfloat16, device="cuda")
+        t_o = timed(lambda: apb.gemm(A, B, C, apb.EPI_STORE), a.iters)
+        t_r = timed(lambda: torch.matmul(A, B.T), a.iters)
+        f = 2.0 * n ** 3
+        print(f"square {n}: apb {t_o:.3f} ms {f / t_o / 1e9:.1f} TF/s | cuBLAS {t_r:.3f} ms {f / t_r / 1e9:.1f} TF/s")
     M, H, I, hq, hk, d = a.rows, 4096, 14336, 32, 8, 128
     g = torch.Generator(device="cuda")
     g.manual_seed(0)

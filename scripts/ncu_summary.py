@@ -26,7 +26,7 @@ def launches(path):
               "second": 1e6, "s": 1e6}.get(r[ui], 1.0)
         agg[name][0] += 1
         agg[name][1] += v
-    ours = {k: v for k, v in agg.items() if any(s in k for s in ("apb", "attn::", "score::", "sel::", "layer::", "dec::"))}
+    ours = {k: v for k, v in agg.items() if any(s in k for s in ("apb", "attn::", "score::", "sel::", "layer::", "dec::", "gemm::"))}
     tot = sum(v for _, v in agg.values())
     tot_ours = sum(v for _, v in ours.values())
     print(f"# ncu launch list ({path}); gpu__time_duration.sum, --clock-control none, serialised + cold-cache")

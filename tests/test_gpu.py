@@ -150,11 +150,14 @@ def test_attention_uniform_closed_form():
 
 # ----------------------------------------------------------------------------- scoring / selection
 
-@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3"])
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3", "yi-heads"])
 @pytest.mark.parametrize("n_out", ["hq", "hk"])
 def test_retain_score_parity(name, n_out):
     from paper_2502_12085_b200 import apb
-    cfg = CASES[name].replace(d_hidden=1024)
+    # yi-heads: 56 query heads (n_out = 56 > 32: two 32-output passes of the pair-GEMM epilogue),
+    # l_b = 700 (a ragged last 256-row pair tile)
+    cfg = (CASES[name] if name in CASES else
+           synth.Config("yi-heads", 20, n=1400, H=2, l_a=64, l_p=100, hq=56, hk=8, d=64)).replace(d_hidden=1024)
     w = synth.retain_weights(cfg, 0, n_out=cfg.hq if n_out == "hq" else cfg.hk)
     for h in range(cfg.H):
         x = synth.host_qkv(cfg, 0, h)
@@ -175,14 +178,16 @@ def test_retain_score_parity(name, n_out):
 
 @pytest.mark.parametrize("plan", ["s3", "p2"])
 def test_retain_score_plans_bit_identical(plan, monkeypatch):
-    """The scoring kernel's pipeline plans (3- or 4-stage ring, one or two hidden chunks per pass
-    over the A rows) run the same MMAs in the same K order and the same epilogue: bit-identical."""
+    """The single-CTA scoring kernel's pipeline plans (APB_SCORE_PLAN: 3- or 4-stage ring, one or
+    two hidden chunks per pass over the A rows) run the same MMAs in the same K order and the same
+    epilogue: bit-identical.  (The default CTA-pair GEMM sums in its own fixed order: checked
+    against the oracle and for run-to-run determinism in test_retain_score_parity.)"""
     from paper_2502_12085_b200 import apb
     cfg = CASES["d128-ragged"].replace(d_hidden=1024)
     w = synth.retain_weights(cfg, 0, n_out=cfg.hq)
     x = synth.host_qkv(cfg, 0, 1)
     out = []
-    for env in ("", plan):
+    for env in ("legacy", plan):
         monkeypatch.setenv("APB_SCORE_PLAN", env)
         s = torch.empty((cfg.hk, cfg.l_b), dtype=torch.float32, device="cuda")
         apb.retain_score(dims_of(cfg, 1), weights_dev(w), dev(x["q"]), dev(x["k"]), dev(x["v"]), s)
