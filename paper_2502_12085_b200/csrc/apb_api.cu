@@ -249,10 +249,21 @@ static size_t retain_ws_bytes(const apb_dims* d, const apb_retain_weights* w) {
   return (size_t)((w->d_hidden + 255) / 256) * (size_t)d->l_b * (size_t)w->n_out * sizeof(float);
 }
 
+static apb_status check_retain_weights(const apb_dims* d, const apb_retain_weights* w) {
+  if (!w) return fail(APB_ERR_CONTRACT, "weights is NULL");
+  const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
+  if (w->d_in != (hq + 2 * hk) * D) return fail(APB_ERR_CONFIG, "d_in must equal (n_heads + 2 n_kv_heads) * head_dim");
+  if (w->n_out != hk && w->n_out != hq) return fail(APB_ERR_CONFIG, "n_out must be n_kv_heads or n_heads");
+  if (w->d_hidden < 256 || w->d_hidden % 256) return fail(APB_ERR_UNSUPPORTED, "d_hidden must be a multiple of 256");
+  if (w->n_out > 64) return fail(APB_ERR_UNSUPPORTED, "n_out must be <= 64");
+  return APB_OK;
+}
+
 extern "C" apb_status apb_retain_workspace_size(const apb_dims* d, const apb_retain_weights* w, size_t* bytes) {
-  if (!bytes || !w) return fail(APB_ERR_CONTRACT, "bytes/weights is NULL");
+  if (!bytes) return fail(APB_ERR_CONTRACT, "bytes is NULL");
   apb_status st = check_dims(d);
   if (st) return st;
+  if ((st = check_retain_weights(d, w))) return st;
   *bytes = retain_ws_bytes(d, w);
   return APB_OK;
 }
@@ -262,12 +273,8 @@ extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weigh
                                        void* ws, size_t ws_bytes, apb_stream_t stream) {
   apb_status st = check_dims(d);
   if (st) return st;
-  if (!w) return fail(APB_ERR_CONTRACT, "weights is NULL");
+  if ((st = check_retain_weights(d, w))) return st;
   const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
-  if (w->d_in != (hq + 2 * hk) * D) return fail(APB_ERR_CONFIG, "d_in must equal (n_heads + 2 n_kv_heads) * head_dim");
-  if (w->n_out != hk && w->n_out != hq) return fail(APB_ERR_CONFIG, "n_out must be n_kv_heads or n_heads");
-  if (w->d_hidden < 256 || w->d_hidden % 256) return fail(APB_ERR_UNSUPPORTED, "d_hidden must be a multiple of 256");
-  if (w->n_out > 64) return fail(APB_ERR_UNSUPPORTED, "n_out must be <= 64");
   if (!w->w1 || !aligned16(w->w1) || !w->w2) return fail(APB_ERR_CONTRACT, "w1/w2 NULL or misaligned");
   if ((st = check_rows(q, q_row_stride, (int64_t)hq * D, "q"))) return st;
   if ((st = check_rows(k, kv_row_stride, (int64_t)hk * D, "k"))) return st;
