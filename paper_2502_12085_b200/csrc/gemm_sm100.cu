@@ -20,7 +20,9 @@
 // Accumulators are double-buffered in TMEM (2 x 256 columns), so the epilogue of one tile
 // (4 warps per CTA, thread = output row = TMEM lane) overlaps the next tile's MMAs.
 // Warps: 0 TMA producer, 1 MMA issuer (leader CTA), 2 TMEM allocator, 4-7 epilogue.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -48,7 +50,7 @@ constexpr int kOffW2 = kOffInv + 64 * 8;
 constexpr int kOffB1 = kOffW2 + 32 * BN * 4;
 constexpr int kSmemScore = kOffB1 + BN * 4 + 1024;
 static_assert(kSmemScore <= 232448, "shared memory (score)");
-constexpr int kGroupM = 8;                    // raster: 8 M-tiles share each W column block in turn
+constexpr double kL2Budget = 48.0 * (1 << 20);  // bytes of a raster group's resident operand rows
 constexpr int kEpiScore = 100;                // internal epilogue: retaining-head partial scores
 static_assert(kSmem <= 232448, "shared memory");
 
@@ -64,6 +66,7 @@ struct Params {
   int64_t pos_offset;
   double log2_theta;
   int num_m, num_n, num_tiles, nkb;
+  int raster_n, group;  // raster: groups of `group` M-tiles (N fastest... see tile_coords) or N-tiles
   // A from up to three row-aligned maps ([Q | K | V] for the retaining head): K blocks [0, kq) from
   // map 0, [kq, kqk) from map 1, the rest from map 2; A's row coordinate is a_row0 + row
   int kq, kqk, a_row0;
@@ -74,13 +77,19 @@ struct Params {
   float* part;
 };
 
+// Tile raster.  Row-grouped (raster_n = 0): a group of `group` M-tiles sweeps every N-tile, so its A
+// rows stay in L2 while W streams through once per group.  Column-grouped (raster_n = 1): a group
+// of N-tiles sweeps every M-tile (W stays, A streams once per group).  launch_params picks the
+// order and group size with the smaller estimated DRAM traffic for the L2 budget.
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
-  const int per_group = kGroupM * p.num_n;
-  const int g = t / per_group, first_m = g * kGroupM;
-  const int gs = min(kGroupM, p.num_m - first_m);
+  const int outer = p.raster_n ? p.num_n : p.num_m, inner = p.raster_n ? p.num_m : p.num_n;
+  const int per_group = p.group * inner;
+  const int g = t / per_group, first = g * p.group;
+  const int gs = min(p.group, outer - first);
   const int r = t - g * per_group;
-  mb = first_m + r % gs;
-  nb = r / gs;
+  const int o = first + r % gs, i = r / gs;
+  mb = p.raster_n ? i : o;
+  nb = p.raster_n ? o : i;
 }
 
 __device__ __forceinline__ float bf16_round(float x) {
@@ -372,6 +381,21 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
   p.num_n = (p.N + BN - 1) / BN;
   p.num_tiles = p.num_m * p.num_n;
   p.nkb = (p.K + BK - 1) / BK;
+  {
+    // estimated DRAM bytes: row groups read A once and W once per group; column groups the reverse
+    const double row_block = 2.0 * BM * p.K * 2.0, col_block = (double)BN * p.K * 2.0;
+    const int gm = std::max(1, std::min(p.num_m, (int)(kL2Budget / row_block)));
+    const int gn = std::max(1, std::min(p.num_n, (int)(kL2Budget / col_block)));
+    const double a_bytes = (double)p.M * p.K * 2.0, w_bytes = (double)p.N * p.K * 2.0;
+    const double traf_m = a_bytes + w_bytes * ((p.num_m + gm - 1) / gm);
+    const double traf_n = w_bytes + a_bytes * ((p.num_n + gn - 1) / gn);
+    p.raster_n = traf_n < traf_m ? 1 : 0;
+    p.group = p.raster_n ? gn : gm;
+    if (const char* env = std::getenv("APB_GEMM_GROUP")) {  // timing experiments: "m8", "n4", ...
+      p.raster_n = env[0] == 'n';
+      p.group = std::max(1, std::atoi(env + 1));
+    }
+  }
   static std::atomic<uint64_t> smem_set{0};
   if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel), kSmemScore, smem_set)) return st;
   int dev = 0, sms = 148;

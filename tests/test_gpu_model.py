@@ -231,13 +231,29 @@ def test_apb_layer_whole_and_anchor_consistency():
         # same math on the same bits; cuBLAS may pick a different algorithm for a different M,
         # so allow accumulation-order differences (a few bf16 ulp)
         check(out[h][:cfg.l_a], out[0][:cfg.l_a], f"anchor rows host {h}", rel=4 * ULP, abs_=1e-2)
-    res = OL.apb_layer([synth.bf16_bits_to_f64(b) for b in x_bits], [cfg.L_A(h) for h in range(cfg.H)], lw_np,
-                       {k: rw[k] for k in ("w1", "b1", "w2", "b2")}, cfg.l_p, cfg.hq, cfg.hk, cfg.d)
+    xs64 = [synth.bf16_bits_to_f64(b) for b in x_bits]
+    L_As = [cfg.L_A(h) for h in range(cfg.H)]
+    rwd = {k: rw[k] for k in ("w1", "b1", "w2", "b2")}
+    # (a) the oracle's own pipeline (its own scores and Top-l_p): near-tie swaps of the passing set
+    # are legitimate (rule (ii)), so only a loose bound holds element-wise
+    res = OL.apb_layer(xs64, L_As, lw_np, rwd, cfg.l_p, cfg.hq, cfg.hk, cfg.d)
     for h in range(cfg.H):
         err = np.abs(out[h] - res["out"][h])
         scale = np.abs(res["out"][h]).mean()
-        print(f"host {h}: max {err.max():.3e} mean {err.mean():.3e} (|out| mean {scale:.3f})")
+        print(f"oracle selection, host {h}: max {err.max():.3e} mean {err.mean():.3e} (|out| mean {scale:.3f})")
         assert err.mean() <= 2e-2 * scale and err.max() <= 0.25 * scale + 0.1
+    # (b) the oracle fed the GPU's scores (its Top-l_p on them is the GPU's set bit for bit, rule
+    # (i)): the same passing keys, so what remains is rounding — bf16 flips of single elements
+    # (<= 1 ulp) at the G20 points and the attention tolerance (2e-2 max / 2e-3 mean), carried
+    # through W_o and the FFN.  Bound: mean <= 4e-3 |out|, max <= 4 bf16 ulp of max |out| + 0.1
+    gpu_scores = [rank.hot.scores[h].cpu().double().numpy() for h in range(cfg.H)]
+    res2 = OL.apb_layer(xs64, L_As, lw_np, rwd, cfg.l_p, cfg.hq, cfg.hk, cfg.d, compressor_scores=gpu_scores)
+    for h in range(cfg.H):
+        err = np.abs(out[h] - res2["out"][h])
+        scale = np.abs(res2["out"][h]).mean()
+        mx = np.abs(res2["out"][h]).max()
+        print(f"GPU selection, host {h}: max {err.max():.3e} mean {err.mean():.3e} (|out| mean {scale:.3f}, max {mx:.2f})")
+        assert err.mean() <= 4e-3 * scale and err.max() <= 4 * ULP * mx + 0.1
 
 
 def test_apb_layer_random_compressor_runs():
