@@ -410,22 +410,43 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
 }
 
 // score_finalize_kernel: o[oc] = b2[oc] + sum_nb part[nb][t][oc] (nb order), s[j][t] = max over the
-// r = n_out / hk outputs of KV head j (reading G4).  One thread per block token.
-__global__ void __launch_bounds__(256) score_finalize_kernel(const float* __restrict__ part, int l_b, int n_parts,
+// r = n_out / hk outputs of KV head j (reading G4).  One thread per block token; a token's n_out
+// partials are contiguous, read as float4 when n_out % 4 == 0 (every paper config).
+__global__ void __launch_bounds__(128) score_finalize_kernel(const float* __restrict__ part, int l_b, int n_parts,
                                                              int n_out, int hk, const float* __restrict__ b2,
                                                              float* __restrict__ scores) {
-  const int t = blockIdx.x * 256 + threadIdx.x;
+  const int t = blockIdx.x * 128 + threadIdx.x;
   if (t >= l_b) return;
   const int rr = n_out / hk;
-  for (int j = 0; j < hk; ++j) {
-    float m = -INFINITY;
-    for (int c = 0; c < rr; ++c) {
-      const int oc = j * rr + c;
+  float m = -INFINITY;
+  auto emit = [&](int oc, float o) {  // outputs arrive in oc order
+    m = fmaxf(m, o + (b2 ? __ldg(b2 + oc) : 0.f));
+    if ((oc + 1) % rr == 0) {
+      scores[(int64_t)(oc / rr) * l_b + t] = m;
+      m = -INFINITY;
+    }
+  };
+  if ((n_out & 3) == 0) {
+    for (int c4 = 0; c4 < n_out / 4; ++c4) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int nb = 0; nb < n_parts; ++nb) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)nb * l_b + t) * n_out) + c4);
+        a.x += v.x;
+        a.y += v.y;
+        a.z += v.z;
+        a.w += v.w;
+      }
+      emit(4 * c4, a.x);
+      emit(4 * c4 + 1, a.y);
+      emit(4 * c4 + 2, a.z);
+      emit(4 * c4 + 3, a.w);
+    }
+  } else {
+    for (int oc = 0; oc < n_out; ++oc) {
       float o = 0.f;
       for (int nb = 0; nb < n_parts; ++nb) o += __ldg(part + ((int64_t)nb * l_b + t) * n_out + oc);
-      m = fmaxf(m, o + (b2 ? __ldg(b2 + oc) : 0.f));
+      emit(oc, o);
     }
-    scores[(int64_t)j * l_b + t] = m;
   }
 }
 
@@ -481,7 +502,7 @@ apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const
   p.part = part;
   if (apb_status st = launch_params(p, tq, tk, tv, tw1, kSmemScore, stream)) return st;
   const int n_parts = (sp.d_hidden + BN - 1) / BN;
-  score_finalize_kernel<<<(sp.l_b + 255) / 256, 256, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
+  score_finalize_kernel<<<(sp.l_b + 127) / 128, 128, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
                                                                    sp.scores);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("score_finalize launch: ") + cudaGetErrorString(e));

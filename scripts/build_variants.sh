@@ -9,7 +9,7 @@ for spec in "$@"; do
   name="${spec%%=*}"; defs="${spec#*=}"
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
     -Xcompiler -fPIC -shared $defs -I include -o build_variants_$name.so \
-    paper_2502_12085_b200/csrc/*.cu -ldl -lcublasLt &
+    paper_2502_12085_b200/csrc/*.cu -ldl &
 done
 wait
 ls -la build_variants_*.so

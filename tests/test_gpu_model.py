@@ -245,7 +245,8 @@ def test_apb_layer_whole_and_anchor_consistency():
     # (b) the oracle fed the GPU's scores (its Top-l_p on them is the GPU's set bit for bit, rule
     # (i)): the same passing keys, so what remains is rounding — bf16 flips of single elements
     # (<= 1 ulp) at the G20 points and the attention tolerance (2e-2 max / 2e-3 mean), carried
-    # through W_o and the FFN.  Bound: mean <= 4e-3 |out|, max <= 4 bf16 ulp of max |out| + 0.1
+    # through W_o and the FFN.  Bound: mean <= 3e-3 |out|, max <= 2 bf16 ulp of max |out| + 1e-2
+    # (B200, toy: max 3.1e-2 = one ulp at |out| in [4, 8), mean 1.7e-3 at |out| mean 0.94)
     gpu_scores = [rank.hot.scores[h].cpu().double().numpy() for h in range(cfg.H)]
     res2 = OL.apb_layer(xs64, L_As, lw_np, rwd, cfg.l_p, cfg.hq, cfg.hk, cfg.d, compressor_scores=gpu_scores)
     for h in range(cfg.H):
@@ -253,7 +254,7 @@ def test_apb_layer_whole_and_anchor_consistency():
         scale = np.abs(res2["out"][h]).mean()
         mx = np.abs(res2["out"][h]).max()
         print(f"GPU selection, host {h}: max {err.max():.3e} mean {err.mean():.3e} (|out| mean {scale:.3f}, max {mx:.2f})")
-        assert err.mean() <= 4e-3 * scale and err.max() <= 4 * ULP * mx + 0.1
+        assert err.mean() <= 3e-3 * scale and err.max() <= 2 * ULP * mx + 1e-2
 
 
 def test_apb_layer_random_compressor_runs():
