@@ -44,9 +44,12 @@ constexpr int kOffBar = STAGES * kStageBytes;
 constexpr int kNumBars = 2 * STAGES + 4;      // full / empty per stage, TMEM full / empty x 2
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kOffInv = (kOffTmem + 16 + 7) / 8 * 8;  // fp64 RoPE inverse frequencies [64]
-constexpr int kSmem = kOffInv + 64 * 8 + 1024;
+// output staging for the TMA stores: two 128-row x 32-column bf16 boxes (64-byte swizzle)
+constexpr int kOffStage = (kOffInv + 64 * 8 + 1023) / 1024 * 1024;
+constexpr int kStageOut = BM * 32 * 2;
+constexpr int kSmem = kOffStage + 2 * kStageOut + 1024;
 // retaining-head scoring (SCORE): a W2 slice [32 outputs][256 hidden] fp32 and b1 [256]
-constexpr int kOffW2 = kOffInv + 64 * 8;
+constexpr int kOffW2 = kOffStage;  // the SCORE epilogue stores no tiles: it reuses the staging area
 constexpr int kOffB1 = kOffW2 + 32 * BN * 4;
 constexpr int kSmemScore = kOffB1 + BN * 4 + 1024;
 static_assert(kSmemScore <= 232448, "shared memory (score)");
@@ -97,15 +100,6 @@ __device__ __forceinline__ float bf16_round(float x) {
 }
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) { return pack_bf16x2(lo, hi); }
 
-// 32 bf16 results of one thread (one row, 32 consecutive columns) -> 4 x 16-byte stores
-__device__ __forceinline__ void store32(uint16_t* dst, const float (&v)[32], int ncols) {
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (q * 8 < ncols)
-      d4[q] = make_uint4(pack2(v[8 * q], v[8 * q + 1]), pack2(v[8 * q + 2], v[8 * q + 3]),
-                         pack2(v[8 * q + 4], v[8 * q + 5]), pack2(v[8 * q + 6], v[8 * q + 7]));
-}
 __device__ __forceinline__ void load32(const uint16_t* src, float (&v)[32], int ncols) {
   const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
@@ -122,7 +116,8 @@ __device__ __forceinline__ void load32(const uint16_t* src, float (&v)[32], int 
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a1,
-                const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_w, const Params p) {
+                const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_w,
+                const __grid_constant__ CUtensorMap tm_c, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
@@ -212,6 +207,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int r = threadIdx.x - 128;  // row within this CTA's half = TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tempty_leader0 = mapa_shared(bTEmpty(0), 0);
+    const uint32_t sstage = sbase + kOffStage;
+    int chunk_ctr = 0;
+    // one 128-row x 32-column bf16 box of this CTA's rows -> shared memory (64-byte swizzle: the
+    // 16-byte chunk q of row r lands at q ^ ((r >> 1) & 3), conflict-free) -> one TMA store by
+    // thread 0 (out-of-range rows / columns are clipped by the tensor map).  Two buffers: a buffer
+    // is rewritten only after the store issued from it two boxes earlier has read it.
+    auto stage_store = [&](const float (&v)[32], int col, int row0) {
+      const int buf = chunk_ctr & 1;
+      if (r == 0) bulk_wait_group_read<1>();
+      named_bar_sync(2, 128);
+      const uint32_t rowaddr = sstage + buf * kStageOut + r * 64;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + ((q ^ ((r >> 1) & 3)) << 4)),
+                     "r"(pack2(v[8 * q], v[8 * q + 1])), "r"(pack2(v[8 * q + 2], v[8 * q + 3])),
+                     "r"(pack2(v[8 * q + 4], v[8 * q + 5])), "r"(pack2(v[8 * q + 6], v[8 * q + 7]))
+                     : "memory");
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (r == 0) {
+        tma_store_2d(&tm_c, sstage + buf * kStageOut, col, row0);
+        bulk_commit_group();
+      }
+      ++chunk_ctr;
+    };
     int tl = 0;
     for (int t = pair; t < p.num_tiles; t += npairs, ++tl) {
       int mb, nb;
@@ -289,7 +309,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else if (p.epi == APB_EPI_SWIGLU) {
         // gate columns [0,128) and up columns [128,256) of this tile -> act columns n0/2 + [0,128)
         const int a0 = n0 / 2;
-        uint16_t* dst = p.c + row * p.ldc + a0;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t g[32], u[32];
@@ -302,13 +321,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const float gf = bf16_round(__uint_as_float(g[e])), uf = bf16_round(__uint_as_float(u[e]));
             v[e] = gf / (1.f + __expf(-gf)) * uf;
           }
-          if (row_ok) store32(dst + c * 32, v, min(32, p.N / 2 - (a0 + c * 32)));
+          stage_store(v, a0 + c * 32, (int)(row - r));
         }
       } else if (p.epi == APB_EPI_ROPE) {
         // the angles of a row depend only on (position, i < head_dim/2): computed once per tile
         // per 32-wide i chunk and applied to every head of the tile
         const int hd = p.head_dim, half = hd / 2;
-        uint16_t* dst = p.c + row * p.ldc + n0;
 #pragma unroll 1
         for (int c = 0; c < half; c += 32) {
           float cs[32], sn[32];
@@ -334,10 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               o1[e] = rot ? f1 * cs[e] - f2 * sn[e] : f1;
               o2[e] = rot ? f2 * cs[e] + f1 * sn[e] : f2;
             }
-            if (row_ok) {
-              store32(dst + h0 + c, o1, min(32, p.N - (n0 + h0 + c)));
-              store32(dst + h0 + half + c, o2, min(32, p.N - (n0 + h0 + half + c)));
-            }
+            stage_store(o1, n0 + h0 + c, (int)(row - r));
+            stage_store(o2, n0 + h0 + half + c, (int)(row - r));
           }
         }
       } else {
@@ -356,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const float prod = bf16_round(__uint_as_float(acc[e]));
             v[e] = p.epi == APB_EPI_RESIDUAL ? p.beta * old[e] + prod : prod;
           }
-          if (row_ok && ncols > 0) store32(dst + c, v, ncols);
+          if (ncols > 0) stage_store(v, n0 + c, (int)(row - r));
         }
       }
       // this tile's accumulator is in registers / stored: release the TMEM buffer to the leader
@@ -364,6 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_leader0 + 8u * b);
     }
+    if (r == 0) bulk_wait_group<0>();  // every TMA store of this CTA has completed
   }
 
   tc_fence_before();
@@ -376,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtensorMap& ta1, const CUtensorMap& ta2,
-                                const CUtensorMap& tw, int smem, cudaStream_t stream) {
+                                const CUtensorMap& tw, const CUtensorMap& tc, int smem, cudaStream_t stream) {
   p.num_m = (int)((p.M + 2 * BM - 1) / (2 * BM));
   p.num_n = (p.N + BN - 1) / BN;
   p.num_tiles = p.num_m * p.num_n;
@@ -402,7 +419,7 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int pairs = std::min(p.num_tiles, sms / 2);
-  gemm_kernel<<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, p);
+  gemm_kernel<<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, tc, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   count_launch();
@@ -481,7 +498,15 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   p.pos_offset = g.pos_offset;
   p.log2_theta = g.theta > 0.f ? std::log2((double)g.theta) : 0.0;
   p.kq = p.kqk = (g.K + BK - 1) / BK;
-  return launch_params(p, ta, ta, ta, tw, kSmem, stream);
+  CUtensorMap tc;
+  {
+    const uint64_t ncols = g.epi == APB_EPI_SWIGLU ? (uint64_t)g.N / 2 : (uint64_t)g.N;
+    uint64_t dims[2] = {ncols, (uint64_t)g.M};
+    uint64_t str[1] = {(uint64_t)g.ldc * 2};
+    uint32_t box[2] = {32, BM};
+    if (!make_tmap_bf16(&tc, g.c, 2, dims, str, box, 64)) return APB_ERR_CUDA;
+  }
+  return launch_params(p, ta, ta, ta, tw, tc, kSmem, stream);
 }
 
 apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -500,7 +525,7 @@ apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const
   p.n_out = sp.n_out;
   p.d_hidden = sp.d_hidden;
   p.part = part;
-  if (apb_status st = launch_params(p, tq, tk, tv, tw1, kSmemScore, stream)) return st;
+  if (apb_status st = launch_params(p, tq, tk, tv, tw1, tw1 /* no tile stores */, kSmemScore, stream)) return st;
   const int n_parts = (sp.d_hidden + BN - 1) / BN;
   score_finalize_kernel<<<(sp.l_b + 127) / 128, 128, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
                                                                    sp.scores);

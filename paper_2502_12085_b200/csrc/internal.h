@@ -24,7 +24,7 @@ apb_status set_max_smem_once(const void* func, int bytes, std::atomic<uint64_t>&
 // TMA descriptor encoding through the driver entry point (no -lcuda at link time).
 // Returns false (and sets the error) if the driver call fails.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                    const uint64_t* strides_bytes, const uint32_t* box);
+                    const uint64_t* strides_bytes, const uint32_t* box, int swizzle_bytes = 128);
 
 // ---------------------------------------------------------------- attention
 struct AttnParams {
