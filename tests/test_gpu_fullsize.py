@@ -13,11 +13,13 @@ oracle.attention_blas, pinned in tests/test_oracle.py):
              an oracle score within 1e-3 of tau_j (the l_p'-th largest oracle score), every host
   gathered   bit-exact vs the oracle's compaction of the GPU's indices, every slot
   attention  >= 4096 rows of the critical host (every 128-row tile boundary +-1, every segment's
-             first / last rows, random rows) and >= 1024 rows of every other host, all heads:
+             first / last rows, random rows) and >= 1024 rows of every other host (every 1024th
+             row boundary +-1, segment ends, random rows), all heads:
              max|dO| <= 2e-2, mean|dO| <= 2e-3, |d lse| <= 1e-2 (north_star)
 
 Also: the same layer under D3 (attention sink + planted needles, the retrieval structure of the
-paper's RULER / InfiniteBench workloads), and the 32K config with EVERY row of every host.
+paper's RULER / InfiniteBench workloads), the 32K config with EVERY row of every host, and the
+Qwen-2.5-14B and Yi-34B-200K configs (ordered schedule, fewer sampled rows).
 Paper passages: Top-l_p and compaction P:177-180 (Alg. apb_prefill); masked attention
 eq:apb P:203-221.
 """
@@ -121,7 +123,8 @@ def check_attention_rows(cfg, hosts, gathered, outs, n_crit, n_other, rng, label
     """outs: list of {host: io} from the schedules under test, compared with one oracle result."""
     for h in range(cfg.H):
         x = hosts[h]
-        rows = sample_rows(x["L_A"], cfg.l_b, n_crit if h == cfg.H - 1 else n_other, rng)
+        crit = h == cfg.H - 1  # every 128-row tile boundary on the critical host, every 1024th elsewhere
+        rows = sample_rows(x["L_A"], cfg.l_b, n_crit if crit else n_other, rng, tile_every=128 if crit else 1024)
         pk, pv = oracle.passing(gathered, h)
         O_or, lse_or = oracle.attention_blas(x["q"], x["k"], x["v"], x["L_A"], pk, pv, rows)
         ridx = torch.from_numpy(rows).cuda()
@@ -174,3 +177,13 @@ def test_llama8b_128k_d3_sink_needles():
 def test_llama8b_32k_all_rows():
     """BASELINE's 32K row (l_a = 1K, l_p = 512): EVERY query row of every host, both schedules."""
     _full_protocol(synth.CONFIGS["llama8b-32k"], n_crit=1 << 30, n_other=1 << 30)
+
+
+@pytest.mark.parametrize("name,n_crit,n_other", [("qwen14b-128k", 1024, 256), ("yi34b-200k", 768, 192)])
+def test_other_configs_full_protocol(name, n_crit, n_other):
+    """BASELINE configs[2] and [3] at full size in the N = 1 bench schedule: Qwen-2.5-14B (g = 5,
+    n_out = 40: two 32-output epilogue passes) and Yi-34B-200K (g = 7, n_out = 56, l_b = 25600,
+    d_in = 9216): every score of every host, selection rules (i) and (ii), the gathered buffer,
+    and sampled attention rows (every 128-row tile boundary of the critical host included).  The
+    512K / 1M rows' attention is checked by test_gpu.py::test_full_size_max_sampled."""
+    _full_protocol(synth.CONFIGS[name], n_crit=n_crit, n_other=n_other, schedules=("ordered",))
