@@ -33,29 +33,34 @@ namespace gemm {
 using namespace apb::sm100;
 
 constexpr int BM = 128;              // output rows per CTA (256 per pair)
-constexpr int BN = 256;              // output columns per tile
 constexpr int BK = 64;               // K block: one 128-byte swizzle atom
-constexpr int STAGES = 6;
 constexpr int kThreads = 256;
 constexpr int kABytes = BM * BK * 2;          // 16 KB
-constexpr int kBBytes = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of the W tile
-constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kOffBar = STAGES * kStageBytes;
-constexpr int kNumBars = 2 * STAGES + 4;      // full / empty per stage, TMEM full / empty x 2
-constexpr int kOffTmem = kOffBar + kNumBars * 8;
-constexpr int kOffInv = (kOffTmem + 16 + 7) / 8 * 8;  // fp64 RoPE inverse frequencies [64]
-// output staging for the TMA stores: two 128-row x 32-column bf16 boxes (64-byte swizzle)
-constexpr int kOffStage = (kOffInv + 64 * 8 + 1023) / 1024 * 1024;
-constexpr int kStageOut = BM * 32 * 2;
-constexpr int kSmem = kOffStage + 2 * kStageOut + 1024;
-// retaining-head scoring (SCORE): a W2 slice [32 outputs][256 hidden] fp32 and b1 [256]
-constexpr int kOffW2 = kOffStage;  // the SCORE epilogue stores no tiles: it reuses the staging area
-constexpr int kOffB1 = kOffW2 + 32 * BN * 4;
-constexpr int kSmemScore = kOffB1 + BN * 4 + 1024;
-static_assert(kSmemScore <= 232448, "shared memory (score)");
+constexpr int kStageOut = BM * 32 * 2;        // one 128-row x 32-column bf16 output box
+// Tile shape: a pair owns 256 rows x BN columns (BN = 256; the retaining-head scoring can also run
+// BN = 128 — 6.9 instead of 3.5 waves, but measured slower: see score_tile_n).
+template <int BN_>
+struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int kBBytes = (BN / 2) * BK * 2;  // this CTA's half of the W tile
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int STAGES = (192 * 1024) / kStageBytes;  // 6 (BN 256) or 8 (BN 128)
+  static constexpr int kOffBar = STAGES * kStageBytes;
+  static constexpr int kNumBars = 2 * STAGES + 4;  // full / empty per stage, TMEM full / empty x 2
+  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
+  static constexpr int kOffInv = (kOffTmem + 16 + 7) / 8 * 8;  // fp64 RoPE inverse frequencies [64]
+  // output staging for the TMA stores: two 128-row x 32-column bf16 boxes (64-byte swizzle)
+  static constexpr int kOffStage = (kOffInv + 64 * 8 + 1023) / 1024 * 1024;
+  static constexpr int kSmem = kOffStage + 2 * kStageOut + 1024;
+  // retaining-head scoring (SCORE): a W2 slice [32 outputs][BN hidden] fp32 and b1 [BN]
+  static constexpr int kOffW2 = kOffStage;  // the SCORE epilogue stores no tiles: reuses the staging area
+  static constexpr int kOffB1 = kOffW2 + 32 * BN * 4;
+  static constexpr int kSmemScore = kOffB1 + BN * 4 + 1024;
+  static constexpr int kTmemCols = 2 * BN >= 512 ? 512 : 256;
+  static_assert(kSmemScore <= 232448 && kSmem <= 232448, "shared memory");
+};
 constexpr double kL2Budget = 48.0 * (1 << 20);  // bytes of a raster group's resident operand rows
-constexpr int kEpiScore = 100;                // internal epilogue: retaining-head partial scores
-static_assert(kSmem <= 232448, "shared memory");
+constexpr int kEpiScore = 100;                  // internal epilogue: retaining-head partial scores
 
 struct Params {
   int64_t M;
@@ -114,10 +119,16 @@ __device__ __forceinline__ void load32(const uint16_t* src, float (&v)[32], int 
   }
 }
 
+template <int BN_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a1,
                 const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_w,
                 const __grid_constant__ CUtensorMap tm_c, const Params p) {
+  using C = Cfg<BN_>;
+  constexpr int BN = C::BN, STAGES = C::STAGES, kBBytes = C::kBBytes, kStageBytes = C::kStageBytes;
+  constexpr int kOffBar = C::kOffBar, kOffTmem = C::kOffTmem, kOffInv = C::kOffInv, kOffStage = C::kOffStage;
+  constexpr int kOffW2 = C::kOffW2, kOffB1 = C::kOffB1;
+  (void)kBBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
@@ -142,7 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc_pair<512>(smem_u32(tmem_ptr));
+  if (warp == 2) tmem_alloc_pair<C::kTmemCols>(smem_u32(tmem_ptr));
   if (p.epi == APB_EPI_ROPE && threadIdx.x < p.head_dim / 2)
     inv[threadIdx.x] = exp2(-p.log2_theta * (2.0 * threadIdx.x) / p.head_dim);
   tc_fence_before();
@@ -254,8 +265,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float* w2s = reinterpret_cast<float*>(smem + kOffW2);
         float* b1s = reinterpret_cast<float*>(smem + kOffB1);
         named_bar_sync(1, 128);  // the previous tile's readers of w2s / b1s are done
-        b1s[r] = p.b1 ? __ldg(p.b1 + n0 + r) : 0.f;
-        b1s[r + 128] = p.b1 ? __ldg(p.b1 + n0 + 128 + r) : 0.f;
+        for (int i = r; i < BN; i += 128) b1s[i] = p.b1 ? __ldg(p.b1 + n0 + i) : 0.f;
 #pragma unroll 1
         for (int og = 0; og < p.n_out; og += 32) {
           const int no = min(32, p.n_out - og);
@@ -388,12 +398,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();  // both CTAs done: no MMA reads the peer's smem, no arrive targets an exited CTA
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc_pair<512>(tmem);
+    tmem_dealloc_pair<C::kTmemCols>(tmem);
   }
 }
 
+template <int BN>
 static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtensorMap& ta1, const CUtensorMap& ta2,
-                                const CUtensorMap& tw, const CUtensorMap& tc, int smem, cudaStream_t stream) {
+                                const CUtensorMap& tw, const CUtensorMap& tc, bool score, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  const int smem = score ? C::kSmemScore : C::kSmem;
   p.num_m = (int)((p.M + 2 * BM - 1) / (2 * BM));
   p.num_n = (p.N + BN - 1) / BN;
   p.num_tiles = p.num_m * p.num_n;
@@ -414,12 +427,13 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
     }
   }
   static std::atomic<uint64_t> smem_set{0};
-  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel), kSmemScore, smem_set)) return st;
+  if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel<BN>), C::kSmemScore, smem_set))
+    return st;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int pairs = std::min(p.num_tiles, sms / 2);
-  gemm_kernel<<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, tc, p);
+  gemm_kernel<BN><<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, tc, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   count_launch();
@@ -481,7 +495,7 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   {
     uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.N};
     uint64_t str[1] = {(uint64_t)g.ldw * 2};
-    uint32_t box[2] = {BK, BN / 2};
+    uint32_t box[2] = {BK, 128};  // this CTA's half of a 256-column W tile
     if (!make_tmap_bf16(&tw, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
   }
   Params p{};
@@ -506,7 +520,18 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
     uint32_t box[2] = {32, BM};
     if (!make_tmap_bf16(&tc, g.c, 2, dims, str, box, 64)) return APB_ERR_CUDA;
   }
-  return launch_params(p, ta, ta, ta, tw, tc, kSmem, stream);
+  return launch_params<256>(p, ta, ta, ta, tw, tc, false, stream);
+}
+
+// Hidden-unit tile of the scoring GEMM: 256 (default) or 128 (APB_SCORE_BN=128).  Measured on the
+// L8 host: 0.176 ms with 256 vs 0.189 ms with 128 — the 128-wide tiles remove the wave
+// quantisation (6.9 instead of 3.5 waves) but load 1.5x the operand bytes per FLOP.
+int score_tile_n() {
+  static const int bn = [] {
+    const char* e = std::getenv("APB_SCORE_BN");
+    return (e && std::atoi(e) == 128) ? 128 : 256;
+  }();
+  return bn;
 }
 
 apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -525,8 +550,11 @@ apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const
   p.n_out = sp.n_out;
   p.d_hidden = sp.d_hidden;
   p.part = part;
-  if (apb_status st = launch_params(p, tq, tk, tv, tw1, tw1 /* no tile stores */, kSmemScore, stream)) return st;
-  const int n_parts = (sp.d_hidden + BN - 1) / BN;
+  const int bn = score_tile_n();
+  apb_status st = bn == 128 ? launch_params<128>(p, tq, tk, tv, tw1, tw1 /* no tile stores */, true, stream)
+                            : launch_params<256>(p, tq, tk, tv, tw1, tw1, true, stream);
+  if (st) return st;
+  const int n_parts = (sp.d_hidden + bn - 1) / bn;
   score_finalize_kernel<<<(sp.l_b + 127) / 128, 128, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
                                                                    sp.scores);
   cudaError_t e = cudaGetLastError();
