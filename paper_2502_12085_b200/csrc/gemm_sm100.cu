@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <string>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -74,6 +75,7 @@ struct Params {
   int64_t pos_offset;
   double log2_theta;
   int num_m, num_n, num_tiles, nkb;
+  int hint_w, hint_c;   // L2 policies: W loads evict_last, C stores evict_first (APB_GEMM_HINTS)
   int raster_n, group;  // raster: groups of `group` M-tiles (N fastest... see tile_coords) or N-tiles
   // A from up to three row-aligned maps ([Q | K | V] for the retaining head): K blocks [0, kq) from
   // map 0, [kq, kqk) from map 1, the rest from map 2; A's row coordinate is a_row0 + row
@@ -165,6 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ================================================================ TMA producer (both CTAs)
     const uint32_t full_leader0 = mapa_shared(bFull(0), 0);
+    const uint64_t pol_last = policy_evict_last();
     int it = 0;
     for (int t = pair; t < p.num_tiles; t += npairs) {
       int mb, nb;
@@ -182,7 +185,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d_pair(st, &tm_a1, full_leader0 + 8u * s, (kb - p.kq) * BK, arow);
           else
             tma_load_2d_pair(st, &tm_a2, full_leader0 + 8u * s, (kb - p.kqk) * BK, arow);
-          tma_load_2d_pair(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow);
+          if (p.hint_w)  // the operand the raster keeps resident in L2 for the whole group
+            tma_load_2d_pair_hint(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow, pol_last);
+          else
+            tma_load_2d_pair(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow);
         }
         __syncwarp();
       }
@@ -219,6 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tempty_leader0 = mapa_shared(bTEmpty(0), 0);
     const uint32_t sstage = sbase + kOffStage;
+    const uint64_t pol_first = policy_evict_first();
     int chunk_ctr = 0;
     // one 128-row x 32-column bf16 box of this CTA's rows -> shared memory (64-byte swizzle: the
     // 16-byte chunk q of row r lands at q ^ ((r >> 1) & 3), conflict-free) -> one TMA store by
@@ -238,7 +245,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
       if (r == 0) {
-        tma_store_2d(&tm_c, sstage + buf * kStageOut, col, row0);
+        // output lines are not re-read by this kernel: first candidates for eviction, so the
+        // operand rows the raster keeps resident stay in L2
+        if (p.hint_c) tma_store_2d_hint(&tm_c, sstage + buf * kStageOut, col, row0, pol_first);
+        else tma_store_2d(&tm_c, sstage + buf * kStageOut, col, row0);
         bulk_commit_group();
       }
       ++chunk_ctr;
@@ -425,6 +435,12 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
       p.raster_n = env[0] == 'n';
       p.group = std::max(1, std::atoi(env + 1));
     }
+  }
+  {
+    const char* h = std::getenv("APB_GEMM_HINTS");  // timing experiments: "wc" (default), "w", "c", "none"
+    const std::string hs = h ? h : "wc";
+    p.hint_w = hs.find('w') != std::string::npos;
+    p.hint_c = hs.find('c') != std::string::npos;
   }
   static std::atomic<uint64_t> smem_set{0};
   if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel<BN>), C::kSmemScore, smem_set))
