@@ -419,7 +419,9 @@ def main():
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
                 "kernel": "apb_attention_kernel<128" + (", paired: 2-CTA clusters multicasting K/V"
                                                          if cfg.d == 128
-                                                         and os.environ.get("APB_ATTN_PAIR", "1")[:1] != "0"
+                                                         and os.environ.get("APB_ATTN_PAIR", "")[:1] != "0"
+                                                         and (not pr.split_phases
+                                                              or os.environ.get("APB_ATTN_PAIR", "")[:1] == "1")
                                                          else "") + "> ("
                 + ("LOCAL + PASSING launches" if pr.split_phases
                                                            else "one ordered PHASE_ALL launch per host") + ")",

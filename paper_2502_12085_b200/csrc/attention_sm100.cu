@@ -792,9 +792,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Paired (2-CTA cluster, multicast K/V) launch: on by default where it applies (D = 128, g % 4 == 0);
 // APB_ATTN_PAIR=0 in the environment selects the single-CTA kernel (A/B timing).
 // Read per launch (a getenv per multi-ms launch) so a test can compare both kernels in one process.
-static bool pair_enabled() {
+// Paired 2-CTA clusters: by default for the one-pass PHASE_ALL launch (the N = 1 schedule: 0.6 %
+// faster and ~50 W lower on the L8 critical host); the LOCAL / PASSING launches of the N > 1
+// schedule run unpaired (L8 critical host, queued: LOCAL 2.86 vs 2.93 ms, PASSING 3.34 vs 3.35 ms).
+// APB_ATTN_PAIR=0: never; APB_ATTN_PAIR=1: every phase.
+static bool pair_enabled(int phase) {
   const char* e = std::getenv("APB_ATTN_PAIR");
-  return !(e && e[0] == '0');
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return phase == APB_PHASE_ALL;
 }
 
 template <int D, bool PAIR>
@@ -851,7 +857,7 @@ apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, c
   // clusters pair items 2c and 2c+1: both must belong to the same (segment, KV head), i.e. every
   // segment holds an even number of items per KV head (decode_item: per_head = ceil(units / 2))
   const bool even_heads = (p.n_local_items / p.hk) % 2 == 0 && (p.n_anchor_items / p.hk) % 2 == 0;
-  if (D == 128 && even_heads && attn::pair_enabled()) return attn::launch_impl<128, true>(p, tq, tk, tv, tg, stream);
+  if (D == 128 && even_heads && attn::pair_enabled(p.phase)) return attn::launch_impl<128, true>(p, tq, tk, tv, tg, stream);
 #endif
   if (D == 128) return attn::launch_impl<128, false>(p, tq, tk, tv, tg, stream);
   if (D == 64) return attn::launch_impl<64, false>(p, tq, tk, tv, tg, stream);
