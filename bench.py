@@ -63,7 +63,11 @@ def parse():
     ap.add_argument("--schedule", choices=["auto", "split", "ordered"], default="auto",
                     help="auto: LOCAL/PASSING split around the exchange only when N > 1")
     ap.add_argument("--same-device", action="store_true",
-                    help="debug: every rank uses cuda:0 (multi-rank logic on a single GPU)")
+                    help="every rank uses cuda:0 (the multi-rank schedule on a single GPU; with the default peer "
+                         "exchange the ranks really exchange their compressed blocks through CUDA IPC)")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "peer"], default="auto",
+                    help="N > 1 exchange: NCCL AllGather, or peer memory (CUDA IPC: the AllGather fused into the "
+                         "compaction, apb_peers_*); auto = peer with --same-device, else nccl")
     ap.add_argument("--dist", choices=["D1", "D2"], default="D1",
                     help="Q/K/V distribution: D1 N(0,1) (the paper's synthetic timing input) or D2 'peaky' "
                          "(Q, K ~ N(0, 2^2): logit std 4, more online-softmax rescales)")
@@ -316,17 +320,23 @@ def main():
     base = apb.Dims(n=cfg.n, H=H, host=0, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
                     head_dim=cfg.d, l_q=cfg.l_q)
     hosts = hosts_of_rank(H, world, rank, args.host_layout)
-    comm = None
-    if world > 1 and not args.same_device:
+    comm = peers = None
+    exchange = args.exchange if args.exchange != "auto" else ("peer" if args.same_device else "nccl")
+    if world > 1 and exchange == "peer":
+        peers = apb.Peers(base, world, rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, peers.handle)
+        peers.open(handles)
+    elif world > 1 and not args.same_device:
         uid = [apb.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = apb.Comm(uid[0], world, rank)
     split = None if args.schedule == "auto" else (args.schedule == "split")
     if args.same_device and world > 1 and split is None:
-        split = True  # the multi-rank schedule (the exchange itself is skipped in this mode)
+        split = True  # the multi-rank schedule (a real exchange with --exchange peer, the default here)
     pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True, split_phases=split,
                      compressor=args.compressor, shared_set=args.shared_set, seed=2502,
-                     same_device=args.same_device)
+                     same_device=args.same_device and peers is None, peers=peers)
 
     # ---- synthetic inputs: D1 N(0,1) Q/K/V (the paper's timing input is synthetic random
     # input), two alternating layer buffer sets, random-init retaining heads.
@@ -454,6 +464,7 @@ def main():
                                                + (" [shared index set]" if args.shared_set else "")
                                                + (" [D2 peaky Q/K]" if args.dist == "D2" else "")),
                                host_layout=host_layout_desc(world, H, args.host_layout),
+                               **({"exchange": exchange} if world > 1 else {}),
                                **({"same_device": True} if args.same_device else {})),
                 "attn_peak_frac": {"critical_host": round(crit * layers / (ms_per_step / 1e3) / 1e12 / peak_tf, 4)
                                    if world == H else None,
@@ -467,6 +478,8 @@ def main():
     if comm is not None:
         comm.check()
         comm.close()
+    if peers is not None:
+        peers.close()  # after the barrier above: no rank still pushes into this buffer
     if world > 1:
         dist.destroy_process_group()
 

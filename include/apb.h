@@ -241,6 +241,38 @@ apb_status apb_exchange_plan(const apb_dims* dims, int32_t nranks, int32_t rank,
                              int32_t max_rounds, int64_t* send_offset, int64_t* recv_offset, int64_t* count,
                              int32_t* n_rounds);
 
+/* ---- the exchange over peer memory (one node: NVLink / NVSwitch P2P through CUDA IPC) ----
+ * An alternative to apb_exchange_passing that fuses the AllGather into the compaction
+ * (P:194-197): libapb allocates each rank's exchange buffer — two `gathered` buffers
+ * bf16 [H][2][n_kv_heads][l_p'][head_dim] alternated by layer parity (epoch & 1), plus flag words
+ * — and apb_select_topk_peers stores every selected K/V row of host `dims->host` straight into
+ * that slot of EVERY rank's buffer, then publishes `epoch` in every rank's flag for the slot.
+ *   apb_peers_create  allocate this rank's buffer; returns its 64-byte CUDA IPC handle
+ *   apb_peers_open    map every other rank's buffer from the [nranks][64] handles (the caller
+ *                     all-gathers the handles, e.g. torch.distributed.all_gather_object)
+ *   apb_peers_gathered  this rank's gathered buffer for a parity (device pointer, library-owned)
+ *   apb_select_topk_peers  apb_select_topk with the fused push; epoch >= 1 increases by one per
+ *                     layer; it first waits until every rank released epoch - 2 (same buffer)
+ *   apb_peers_wait    enqueue a wait until slots [0, n_slots) of gathered[epoch & 1] hold epoch
+ *                     (before the PASSING attention that reads them)
+ *   apb_peers_release enqueue "this rank finished reading epoch" on every rank (after PASSING)
+ *   apb_peers_destroy free (after a barrier: no rank may still write into this buffer)
+ * Ownership: the buffers are library-owned; callers read gathered through the returned pointer.
+ * Errors: APB_ERR_CONFIG (nranks outside [1, 8], not dividing H, dims not matching), APB_ERR_CONTRACT
+ * (NULL / unopened), APB_ERR_CUDA (allocation, IPC, launch).  Waits are device-side spins: every
+ * rank must keep issuing its pushes and releases, as in any collective.                        */
+typedef struct apb_peers apb_peers;
+apb_status apb_peers_create(const apb_dims* dims, int32_t nranks, int32_t rank, apb_peers** out,
+                            uint8_t ipc_handle[64]);
+apb_status apb_peers_open(apb_peers* peers, const uint8_t* handles);
+apb_status apb_peers_gathered(const apb_peers* peers, int32_t parity, void** gathered);
+apb_status apb_select_topk_peers(const apb_dims* dims, const float* scores, const void* k, const void* v,
+                                 int64_t kv_row_stride, int32_t* indices, apb_peers* peers, int32_t epoch,
+                                 apb_stream_t stream);
+apb_status apb_peers_wait(apb_peers* peers, int32_t n_slots, int32_t epoch, apb_stream_t stream);
+apb_status apb_peers_release(apb_peers* peers, int32_t epoch, apb_stream_t stream);
+apb_status apb_peers_destroy(apb_peers* peers);
+
 /* Polls the communicator for an asynchronous NCCL error (ncclCommGetAsyncError): a failure of
  * an already-enqueued collective (peer lost, network error) surfaces here as APB_ERR_NCCL with
  * the NCCL message in apb_last_error().  apb_exchange_passing{,_cyclic} poll before and after

@@ -33,7 +33,9 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials", "apb_exchange_partials",
             "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size", "apb_exchange_passing_cyclic",
             "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check", "apb_comm_abort",
-            "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size")
+            "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size",
+            "apb_peers_create", "apb_peers_open", "apb_peers_gathered", "apb_select_topk_peers", "apb_peers_wait",
+            "apb_peers_release", "apb_peers_destroy")
 
 
 class ApbError(RuntimeError):
@@ -110,6 +112,13 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_comm_check.argtypes = [vp]
     lib.apb_comm_abort.argtypes = [vp]
     lib.apb_exchange_partials_cyclic.argtypes = [vp, i32, i64, vp, vp]
+    lib.apb_peers_create.argtypes = [dp, i32, i32, ctypes.POINTER(vp), ctypes.c_char_p]
+    lib.apb_peers_open.argtypes = [vp, ctypes.c_char_p]
+    lib.apb_peers_gathered.argtypes = [vp, i32, ctypes.POINTER(vp)]
+    lib.apb_select_topk_peers.argtypes = [dp, vp, vp, vp, i64, vp, vp, i32, vp]
+    lib.apb_peers_wait.argtypes = [vp, i32, i32, vp]
+    lib.apb_peers_release.argtypes = [vp, i32, vp]
+    lib.apb_peers_destroy.argtypes = [vp]
     lib.apb_retain_workspace_size.argtypes = [dp, ctypes.POINTER(_Weights), ctypes.POINTER(sz)]
     lib.apb_gemm.argtypes = [i64, i32, i32, vp, i64, vp, i64, vp, i64, ctypes.POINTER(_GemmEpi), vp]
     for f in ("apb_random_scores", "apb_share_scores", "apb_rmsnorm", "apb_rope", "apb_swiglu", "apb_gemm_bf16", "apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_attention_fwd",
@@ -117,7 +126,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
               "apb_check_dims", "apb_decode_attention", "apb_decode_workspace_size", "apb_merge_partials",
               "apb_exchange_partials", "apb_decode_attention_hosts", "apb_decode_hosts_workspace_size",
               "apb_exchange_passing_cyclic", "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check",
-              "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size"):
+              "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size",
+              "apb_peers_create", "apb_peers_open", "apb_peers_gathered", "apb_select_topk_peers", "apb_peers_wait",
+              "apb_peers_release", "apb_peers_destroy"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -444,6 +455,61 @@ class Comm:
         if self._h:
             _check(load().apb_comm_destroy(self._h), "apb_comm_destroy")
             self._h = ctypes.c_void_p()
+
+
+class _CudaBuffer:
+    """A library-owned device buffer exposed through __cuda_array_interface__ (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class Peers:
+    """apb_peers: the passing-block exchange over peer memory (CUDA IPC within one node), the
+    AllGather fused into the compaction.  Construct on every rank, all-gather `handle` (64 bytes)
+    across ranks, then call open(handles)."""
+
+    def __init__(self, dims: Dims, nranks: int, rank: int):
+        self._h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(64)
+        d = dims.c()
+        _check(load().apb_peers_create(ctypes.byref(d), nranks, rank, ctypes.byref(self._h), buf), "apb_peers_create")
+        self.handle = buf.raw
+        self.nranks, self.rank, self.dims = nranks, rank, dims
+
+    def open(self, handles: list[bytes]) -> None:
+        _check(load().apb_peers_open(self._h, b"".join(handles)), "apb_peers_open")
+
+    def gathered(self, parity: int) -> torch.Tensor:
+        """This rank's gathered buffer for a parity, as a bf16 [H][2][hk][l_p'][d] tensor view."""
+        ptr = ctypes.c_void_p()
+        _check(load().apb_peers_gathered(self._h, parity, ctypes.byref(ptr)), "apb_peers_gathered")
+        d = self.dims
+        shape = (d.H, 2, d.n_kv_heads, d.l_pp, d.head_dim)
+        t = torch.as_tensor(_CudaBuffer(ptr.value, shape, "<i2"), device="cuda")
+        return t.view(torch.bfloat16)
+
+    def select_topk(self, dims: Dims, scores, k, v, indices, epoch: int, stream=None) -> None:
+        _need_numel(scores, "scores", torch.float32, dims.n_kv_heads * dims.l_b)
+        if _rowstride(k, "k") != _rowstride(v, "v"):
+            raise ApbError(ERR_CONTRACT, "k/v", "K and V must share one row stride")
+        _need_numel(indices, "indices", torch.int32, dims.n_kv_heads * dims.l_pp)
+        d = dims.c()
+        _check(load().apb_select_topk_peers(ctypes.byref(d), scores.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                            _rowstride(k, "k"), indices.data_ptr(), self._h, epoch, _stream(stream)),
+               "apb_select_topk_peers")
+
+    def wait(self, n_slots: int, epoch: int, stream=None) -> None:
+        _check(load().apb_peers_wait(self._h, n_slots, epoch, _stream(stream)), "apb_peers_wait")
+
+    def release(self, epoch: int, stream=None) -> None:
+        _check(load().apb_peers_release(self._h, epoch, _stream(stream)), "apb_peers_release")
+
+    def close(self) -> None:
+        if self._h:
+            h, self._h = self._h, ctypes.c_void_p()
+            _check(load().apb_peers_destroy(h), "apb_peers_destroy")
 
 
 def exchange_passing(comm: Comm | None, dims: Dims, gathered, stream=None, cyclic: bool = False) -> None:

@@ -90,9 +90,22 @@ struct GemmArgs {
 apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream);
 apb_status launch_random_scores(uint64_t seed, uint64_t c0, int64_t count, float* scores, cudaStream_t stream);
 apb_status launch_share_scores(float* scores, int hk, int l_b, cudaStream_t stream);
+// Destinations of the compaction: one local slot, or (peer exchange) the same slot in every rank's
+// IPC-mapped buffer plus a completion flag per rank.
+constexpr int kMaxPeers = 8;
+struct GatherDst {
+  int n;
+  uint16_t* send[kMaxPeers];  // slot base ([2][hk][l_p'][d]) in each destination
+  int32_t* flag[kMaxPeers];   // nullptr: no signal; else set to `epoch` once the launch's stores landed
+  uint32_t* counter;          // CTA-completion counter (this rank's device memory)
+  int32_t epoch;
+};
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores,
                                  const void* k, const void* v, int64_t kv_row_stride, int32_t* indices,
-                                 void* send, cudaStream_t stream);
+                                 void* send, cudaStream_t stream, const GatherDst* push = nullptr);
+// peer exchange helpers (peers.cu)
+apb_status launch_wait_flags(const int32_t* flags, int n, int32_t epoch, cudaStream_t stream);
+apb_status launch_publish(int32_t* const* dsts, int n, int32_t epoch, cudaStream_t stream);
 
 // ---------------------------------------------------------------- decode (Alg. apb_decode)
 constexpr int kDecodeRowsMax = 64;  // t_new * (n_heads / n_kv_heads) per KV head

@@ -422,11 +422,15 @@ __global__ void __launch_bounds__(kFT) select_reg_kernel(const float* __restrict
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// send[kv][j][m][:] = (kv ? V : K)[L_A + idx[j][m]][j][:]; grid (ceil(lp / rows_per_cta), hk, 2)
+// send[kv][j][m][:] = (kv ? V : K)[L_A + idx[j][m]][j][:]; grid (ceil(lp / rows_per_cta), hk, 2).
+// With a peer push (GatherDst.n > 1 or flags set) every row is stored into the same slot of every
+// rank's buffer (CUDA IPC mappings: NVLink / NVSwitch stores) — the AllGather fused into the
+// compaction — and the launch's last CTA then publishes `epoch` in every rank's flag word for this
+// slot (release at system scope, after every CTA's stores were fenced at system scope).
 template <int D>
 __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ k,
                                                      const uint16_t* __restrict__ v, int64_t kv_row_stride, int L_A,
-                                                     int lp, int hk, uint16_t* __restrict__ send) {
+                                                     int lp, int hk, const GatherDst dst) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the select grid's indices are visible
   constexpr int kVec = D / 8;                         // 16-byte vectors per row
   constexpr int kBatch = 8;
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
   const int j = blockIdx.y, kv = blockIdx.z;
   const int r0 = blockIdx.x * kRows;
   const uint16_t* src = (kv ? v : k) + (int64_t)j * D;
-  uint4* dst = reinterpret_cast<uint4*>(send + (((int64_t)kv * hk + j) * lp) * D);
+  const int64_t off = (((int64_t)kv * hk + j) * lp) * D;  // elements into a slot
   uint4 buf[kBatch];
   int rr[kBatch];
 #pragma unroll
@@ -445,9 +449,25 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
     if (r < lp)
       buf[q] = __ldg(reinterpret_cast<const uint4*>(src + (L_A + (int64_t)__ldg(idx + (int64_t)j * lp + r)) * kv_row_stride) + c);
   }
+  for (int d = 0; d < dst.n; ++d) {
+    uint4* out = reinterpret_cast<uint4*>(dst.send[d] + off);
 #pragma unroll
-  for (int q = 0; q < kBatch; ++q)
-    if (rr[q] >= 0) dst[(int64_t)rr[q] * kVec + (q * 256 + threadIdx.x) % kVec] = buf[q];
+    for (int q = 0; q < kBatch; ++q)
+      if (rr[q] >= 0) out[(int64_t)rr[q] * kVec + (q * 256 + threadIdx.x) % kVec] = buf[q];
+  }
+  if (dst.flag[0] != nullptr) {
+    __threadfence_system();  // this thread's peer stores are visible system-wide
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t n_ctas = gridDim.x * gridDim.y * gridDim.z;
+      const uint32_t done = atomicAdd(dst.counter, 1u) + 1u;
+      if (done % n_ctas == 0) {  // the last CTA of this launch: every CTA's stores are fenced
+        __threadfence_system();
+        for (int d = 0; d < dst.n; ++d)
+          asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(dst.flag[d]), "r"(dst.epoch) : "memory");
+      }
+    }
+  }
 }
 
 template <bool kSmem>
@@ -463,7 +483,7 @@ static apb_status launch_fast(const float* scores, int l_b, int lp, int hk, int3
 
 template <int D>
 static cudaError_t launch_gather(const int32_t* idx, const void* k, const void* v, int64_t kv_row_stride, int L_A,
-                                 int lp, int hk, void* send, cudaStream_t stream) {
+                                 int lp, int hk, const GatherDst& dst, cudaStream_t stream) {
   constexpr int kRows = 256 * 8 / (D / 8);
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3((lp + kRows - 1) / kRows, hk, 2);
@@ -475,16 +495,16 @@ static cudaError_t launch_gather(const int32_t* idx, const void* k, const void* 
   c.attrs = &attr;
   c.numAttrs = 1;
   return cudaLaunchKernelEx(&c, gather_kernel<D>, idx, static_cast<const uint16_t*>(k),
-                            static_cast<const uint16_t*>(v), kv_row_stride, L_A, lp, hk, static_cast<uint16_t*>(send));
+                            static_cast<const uint16_t*>(v), kv_row_stride, L_A, lp, hk, dst);
 }
 
 }  // namespace sel
 
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores, const void* k,
                                  const void* v, int64_t kv_row_stride, int32_t* indices, void* send,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const GatherDst* push) {
   const char* env = std::getenv("APB_SELECT");
-  if (!(env && env[0] == 'l')) {
+  if (push || !(env && env[0] == 'l')) {
     apb_status st = APB_OK;
     if (l_b <= 16 * sel::kFT)
       sel::select_reg_kernel<16><<<hk, sel::kFT, 0, stream>>>(scores, l_b, lp, indices);
@@ -497,12 +517,18 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("select launch: ") + cudaGetErrorString(e));
     const char* dbg = std::getenv("APB_SELECT_DBG");  // timing experiments only: 1 = no gather
-    if (dbg && dbg[0] == '1') {
+    if (dbg && dbg[0] == '1' && !push) {
       count_launch(1);
       return APB_OK;
     }
-    e = D == 128 ? sel::launch_gather<128>(indices, k, v, kv_row_stride, L_A, lp, hk, send, stream)
-                 : sel::launch_gather<64>(indices, k, v, kv_row_stride, L_A, lp, hk, send, stream);
+    GatherDst local{};
+    if (!push) {
+      local.n = 1;
+      local.send[0] = static_cast<uint16_t*>(send);
+    }
+    const GatherDst& dst = push ? *push : local;
+    e = D == 128 ? sel::launch_gather<128>(indices, k, v, kv_row_stride, L_A, lp, hk, dst, stream)
+                 : sel::launch_gather<64>(indices, k, v, kv_row_stride, L_A, lp, hk, dst, stream);
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gather launch: ") + cudaGetErrorString(e));
     count_launch(2);
     return APB_OK;

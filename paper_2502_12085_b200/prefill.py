@@ -41,7 +41,7 @@ class PrefillRank:
     def __init__(self, base: apb.Dims, hosts: list[int], comm: apb.Comm | None = None,
                  device: torch.device | str = "cuda", skip_unused_last: bool = False,
                  split_phases: bool | None = None, compressor: str = "retain", shared_set: bool = False,
-                 seed: int = 0, same_device: bool = False):
+                 seed: int = 0, same_device: bool = False, peers: "apb.Peers | None" = None):
         """base: problem dims (its `host` field is ignored); hosts: host indices this rank owns
         (contiguous, in order).  skip_unused_last: do not score/select host H-1 — its
         compressed block is ignored by every host, so outputs are unchanged.
@@ -52,15 +52,24 @@ class PrefillRank:
         max over KV heads instead of per-KV-head sets (reading G3).
         same_device: debug only — allow owning a strict subset of the hosts WITHOUT a multi-rank
         communicator (the passing slots of hosts owned elsewhere are then never filled, so the
-        outputs are not APB's; used to exercise the N > 1 schedule on one GPU)."""
+        outputs are not APB's; used to exercise the N > 1 schedule on one GPU).
+        peers: an opened apb.Peers — the exchange over peer memory (CUDA IPC) instead of NCCL: the
+        compaction pushes every selected row into every rank's buffer (apb_select_topk_peers), the
+        PASSING launch waits for its slots on the device, then releases the buffer (two buffers
+        alternate by layer).  Implies the LOCAL / PASSING split."""
         if compressor not in ("retain", "random"):
             raise ValueError(f"compressor must be 'retain' or 'random', not {compressor!r}")
         self.compressor, self.shared_set, self.seed = compressor, shared_set, seed
         self.base, self.hosts, self.comm = base, list(hosts), comm
         self.device = torch.device(device)
         self.skip_unused_last = skip_unused_last
-        self.split_phases = (comm is not None and comm.nranks > 1) if split_phases is None else split_phases
-        nr = comm.nranks if comm is not None else 1
+        self.peers, self.epoch = peers, 0
+        if peers is not None and comm is not None:
+            raise ValueError("pass either a NCCL communicator or peers, not both")
+        if split_phases is None:
+            split_phases = peers is not None or (comm is not None and comm.nranks > 1)
+        self.split_phases = split_phases
+        nr = comm.nranks if comm is not None else (peers.nranks if peers is not None else 1)
         if nr > 1 and not self.split_phases:
             # the ordered one-pass schedule waits only on this rank's own slot events, never on
             # the AllGather that fills the other ranks' slots: it is a single-rank schedule
@@ -75,7 +84,11 @@ class PrefillRank:
             raise ValueError("owned hosts must be a contiguous block or the cyclic set r, r+N, ...")
         b = base
         lpp, hk, hq, d = b.l_pp, b.n_kv_heads, b.n_heads, b.head_dim
-        self.gathered = torch.zeros((b.H, 2, hk, lpp, d), dtype=torch.bfloat16, device=self.device)
+        if peers is not None:  # two library-owned buffers, alternated by layer parity
+            self.peer_gathered = [peers.gathered(0), peers.gathered(1)]
+            self.gathered = self.peer_gathered[0]
+        else:
+            self.gathered = torch.zeros((b.H, 2, hk, lpp, d), dtype=torch.bfloat16, device=self.device)
         self.scores = {h: torch.empty((hk, b.l_b), dtype=torch.float32, device=self.device) for h in hosts}
         self.indices = {h: torch.empty((hk, max(lpp, 1)), dtype=torch.int32, device=self.device) for h in hosts}
         self.ws = {}
@@ -119,6 +132,11 @@ class PrefillRank:
                                                                   stream=stream, ws=self.score_ws[h]))
         if self.shared_set:
             apb.share_scores(d, self.scores[h], stream=stream)
+        if self.peers is not None:  # select + compaction pushed into every rank's buffer
+            self._op("select_compact", h, stream, lambda: self.peers.select_topk(d, self.scores[h], x.k, x.v,
+                                                                                 self.indices[h], self.epoch,
+                                                                                 stream=stream))
+            return
         self._op("select_compact", h, stream, lambda: apb.select_topk(d, self.scores[h], x.k, x.v, self.indices[h],
                                                                       self.gathered[h], stream=stream))
 
@@ -133,7 +151,10 @@ class PrefillRank:
                 self._compress_host(h, io, weights, layer_idx, stream)
 
     def exchange(self, stream=None) -> None:
-        """Step 3: in-place AllGather(s) of the packed [2][hk][l_p'][d] slots."""
+        """Step 3: in-place AllGather(s) of the packed [2][hk][l_p'][d] slots (with peers the
+        exchange already happened inside the compaction)."""
+        if self.peers is not None:
+            return
         self._op("exchange", -1, stream, lambda: apb.exchange_passing(self.comm, self.base, self.gathered,
                                                                       stream=stream, cyclic=self.cyclic))
 
@@ -184,13 +205,22 @@ class PrefillRank:
                     stream=main)))
             main.wait_stream(self.side)  # the last host's compression still reads io[h].k/v
             return
+        if self.peers is not None:
+            self.epoch += 1
+            self.gathered = self.peer_gathered[self.epoch & 1]
         self.side.wait_stream(main)  # this layer's inputs are produced on the main stream
         self.compress(io, weights, self.side, layer_idx)
         self.exchange(self.side)
         self.ev_exchanged.record(self.side)
         timed(lambda: self.attention(io, apb.PHASE_LOCAL, main))
-        main.wait_event(self.ev_exchanged)
+        if self.peers is not None:
+            # device-side wait for the slots this rank's hosts read (hosts < max owned host)
+            self.peers.wait(max(self.hosts), self.epoch, stream=main)
+        else:
+            main.wait_event(self.ev_exchanged)
         timed(lambda: self.attention(io, apb.PHASE_PASSING, main))
+        if self.peers is not None:
+            self.peers.release(self.epoch, stream=main)
         # the side stream's buffers (scores, gathered) are reused next layer only after main
         # has consumed them: next layer's side.wait_stream(main) orders that.  Conversely the
         # caller may overwrite io's Q/K/V once main is past this point.
