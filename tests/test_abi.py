@@ -221,3 +221,17 @@ def test_fails_loudly_without_gpu(lib):
 def test_exchange_single_rank_is_noop(lib):
     # comm == NULL (one rank) is a legal no-op that never touches memory
     apb.exchange_passing(None, _dims(), _FakeT(0x10000, (4, 2, 2, 64, 64)), stream=0)
+
+
+def test_peers_contract_errors(lib):
+    """apb_peers_*: configuration errors before any allocation; unopened peers are rejected."""
+    import ctypes as C
+    h = C.c_void_p()
+    buf = C.create_string_buffer(64)
+    d = _dims().c()
+    assert lib.apb_peers_create(C.byref(d), 9, 0, C.byref(h), buf) == apb.ERR_CONFIG   # > 8 ranks
+    assert lib.apb_peers_create(C.byref(d), 3, 0, C.byref(h), buf) == apb.ERR_CONFIG   # 3 does not divide H = 4
+    assert lib.apb_peers_create(C.byref(d), 2, 2, C.byref(h), buf) == apb.ERR_CONFIG   # rank out of range
+    assert lib.apb_peers_wait(None, 1, 1, None) == apb.ERR_CONTRACT
+    assert lib.apb_peers_release(None, 1, None) == apb.ERR_CONTRACT
+    assert lib.apb_peers_destroy(None) == apb.OK
