@@ -181,7 +181,7 @@ def main(args=None):
     achieved = flops / (ms_per_step / 1e3) / 1e12
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": None,
-                "kernel": "whole step (cuBLASLt projections/FFN + apb attention + apb scoring), useful FLOPs",
+                "kernel": "whole step (libapb tcgen05 GEMMs with fused epilogues + apb attention + apb scoring), useful FLOPs",
                 "peak_source": f"bf16_tflops_sustained, {peak_src}",
                 "flops_per_step": flops, "flops_split": {"gemm": f_gemm, "retain_score": f_score, "attention": f_attn}}
 
