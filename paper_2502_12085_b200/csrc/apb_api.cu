@@ -250,8 +250,9 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
 
 // ---------------------------------------------------------------- step 1: scoring
 static size_t retain_ws_bytes(const apb_dims* d, const apb_retain_weights* w) {
-  // one fp32 partial per 128 hidden units (the finer of the two scoring tile widths)
-  return (size_t)((w->d_hidden + 127) / 128) * (size_t)d->l_b * (size_t)w->n_out * sizeof(float);
+  // one fp32 partial slot per half tile of hidden units (score_tile_n() / 2 = 128 by default)
+  const int unit = score_tile_n() / 2;
+  return (size_t)((w->d_hidden + unit - 1) / unit) * (size_t)d->l_b * (size_t)w->n_out * sizeof(float);
 }
 
 static apb_status check_retain_weights(const apb_dims* d, const apb_retain_weights* w) {
@@ -325,7 +326,10 @@ extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weigh
     uint64_t str[1] = {(uint64_t)w->d_in * 2};
     uint32_t wbox[2] = {64, (uint32_t)score_tile_n() / 2};  // this CTA's half of a W1 tile
     if (!make_tmap_bf16(&tw, w->w1, 2, dims, str, wbox)) return APB_ERR_CUDA;
-    return launch_score_gemm(p, tq, tk, tv, tw, static_cast<float*>(ws), reinterpret_cast<cudaStream_t>(stream));
+    CUtensorMap twh;
+    uint32_t whbox[2] = {64, (uint32_t)score_tile_n() / 4};  // ... of a half tile (the tail wave)
+    if (!make_tmap_bf16(&twh, w->w1, 2, dims, str, whbox)) return APB_ERR_CUDA;
+    return launch_score_gemm(p, tq, tk, tv, tw, twh, static_cast<float*>(ws), reinterpret_cast<cudaStream_t>(stream));
   }
   {
     uint64_t dims[2] = {(uint64_t)w->d_in, (uint64_t)w->d_hidden};

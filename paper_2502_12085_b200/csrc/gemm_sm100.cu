@@ -75,6 +75,7 @@ struct Params {
   int64_t pos_offset;
   double log2_theta;
   int num_m, num_n, num_tiles, nkb;
+  int n_items, n_full;  // work items; items >= n_full are half tiles (BN/2 columns, the tail wave)
   int hint_w, hint_c;   // L2 policies: W loads evict_last, C stores evict_first (APB_GEMM_HINTS)
   int raster_n, group;  // raster: groups of `group` M-tiles (N fastest... see tile_coords) or N-tiles
   // A from up to three row-aligned maps ([Q | K | V] for the retaining head): K blocks [0, kq) from
@@ -102,6 +103,20 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int
   nb = p.raster_n ? o : i;
 }
 
+// Work item -> tile (+ half: -1 = the whole BN-wide tile, 0 / 1 = its left / right BN/2 columns).
+// The tiles of a final partial wave are split in two halves (launch_params), so that wave is
+// half as long: 256 scoring tiles on 74 pairs run in 3.5 instead of 4 tile-times.
+__device__ __forceinline__ void item_coords(const Params& p, int item, int& mb, int& nb, int& half) {
+  if (item < p.n_full) {
+    tile_coords(p, item, mb, nb);
+    half = -1;
+  } else {
+    const int r = item - p.n_full;
+    tile_coords(p, p.n_full + r / 2, mb, nb);
+    half = r & 1;
+  }
+}
+
 __device__ __forceinline__ float bf16_round(float x) {
   return __uint_as_float(static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(x))) << 16);
 }
@@ -125,7 +140,8 @@ template <int BN_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a1,
                 const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_w,
-                const __grid_constant__ CUtensorMap tm_c, const Params p) {
+                const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_wh,
+                const Params p) {
   using C = Cfg<BN_>;
   constexpr int BN = C::BN, STAGES = C::STAGES, kBBytes = C::kBBytes, kStageBytes = C::kStageBytes;
   constexpr int kOffBar = C::kOffBar, kOffTmem = C::kOffTmem, kOffInv = C::kOffInv, kOffStage = C::kOffStage;
@@ -169,15 +185,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t full_leader0 = mapa_shared(bFull(0), 0);
     const uint64_t pol_last = policy_evict_last();
     int it = 0;
-    for (int t = pair; t < p.num_tiles; t += npairs) {
-      int mb, nb;
-      tile_coords(p, t, mb, nb);
-      const int arow = p.a_row0 + mb * 2 * BM + rank * BM, wrow = nb * BN + rank * (BN / 2);
+    for (int t = pair; t < p.n_items; t += npairs) {
+      int mb, nb, half;
+      item_coords(p, t, mb, nb, half);
+      const int arow = p.a_row0 + mb * 2 * BM + rank * BM;
+      const int wrow = half < 0 ? nb * BN + rank * (BN / 2) : nb * BN + half * (BN / 2) + rank * (BN / 4);
+      const uint32_t stage_tx = half < 0 ? 2 * kStageBytes : 2 * (kABytes + kBBytes / 2);
       for (int kb = 0; kb < p.nkb; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(bEmpty(s), ((it / STAGES) & 1) ^ 1);
         if (elect_one()) {
-          if (rank == 0) mbar_arrive_expect_tx(bFull(s), 2 * kStageBytes);
+          if (rank == 0) mbar_arrive_expect_tx(bFull(s), stage_tx);
           const uint32_t st = sbase + s * kStageBytes;
           if (kb < p.kq)
             tma_load_2d_pair(st, &tm_a, full_leader0 + 8u * s, kb * BK, arow);
@@ -185,7 +203,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d_pair(st, &tm_a1, full_leader0 + 8u * s, (kb - p.kq) * BK, arow);
           else
             tma_load_2d_pair(st, &tm_a2, full_leader0 + 8u * s, (kb - p.kqk) * BK, arow);
-          if (p.hint_w)  // the operand the raster keeps resident in L2 for the whole group
+          if (half >= 0)  // this CTA's quarter of the W tile (BN/4 rows) for a half-tile item
+            tma_load_2d_pair(st + kABytes, &tm_wh, full_leader0 + 8u * s, kb * BK, wrow);
+          else if (p.hint_w)  // the operand the raster keeps resident in L2 for the whole group
             tma_load_2d_pair_hint(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow, pol_last);
           else
             tma_load_2d_pair(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow);
@@ -196,9 +216,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ================================================================ MMA issuer (leader only)
     if (rank == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN, false, false);
+      constexpr uint32_t idesc_full = idesc_bf16_f32(2 * BM, BN, false, false);
+      constexpr uint32_t idesc_half = idesc_bf16_f32(2 * BM, BN / 2, false, false);
       int it = 0, tl = 0;
-      for (int t = pair; t < p.num_tiles; t += npairs, ++tl) {
+      for (int t = pair; t < p.n_items; t += npairs, ++tl) {
+        const uint32_t idesc = t < p.n_full ? idesc_full : idesc_half;
         const int b = tl & 1;
         mbar_wait(bTEmpty(b), ((tl >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -254,13 +276,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ++chunk_ctr;
     };
     int tl = 0;
-    for (int t = pair; t < p.num_tiles; t += npairs, ++tl) {
-      int mb, nb;
-      tile_coords(p, t, mb, nb);
+    for (int t = pair; t < p.n_items; t += npairs, ++tl) {
+      int mb, nb, half;
+      item_coords(p, t, mb, nb, half);
       const int b = tl & 1;
       const int64_t row = (int64_t)mb * 2 * BM + rank * BM + r;
       const bool row_ok = row < p.M;
-      const int n0 = nb * BN;
+      const int n0 = nb * BN + (half > 0 ? BN / 2 : 0);
+      const int bne = half < 0 ? BN : BN / 2;  // columns of this item (half tiles: SCORE only)
       const uint32_t tacc = tmem + lane_base + b * BN;
       mbar_wait(bTFull(b), (tl >> 1) & 1);
       tc_fence_after();
@@ -268,20 +291,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (p.epi == APB_EPI_ROPE)
         posd = row_ok ? (p.positions ? (double)p.positions[row] : (double)(p.pos_offset + row)) : 0.0;
       if (p.epi == kEpiScore) {
-        // retaining head (reading G2): a = SiLU(z + b1) for this tile's 256 hidden
-        // units, partial o[oc] = sum_h W2[oc][h] a_h in fp32 (fixed order: chunks of 32 in
-        // column order, packed FFMA2 pairs) -> part[nb][row][oc]; score_finalize_kernel sums the
-        // d_hidden / 256 partials in nb order.  32 outputs per pass over the TMEM tile.
+        // retaining head (reading G2): a = SiLU(z + b1) for this item's hidden units
+        // (BN, or BN/2 for a half-tile item), partial o[oc] = sum_h W2[oc][h] a_h in fp32 (fixed
+        // order: chunks of 32 in column order, packed FFMA2 pairs) -> part[slot][row][oc] with one
+        // slot per BN/2 hidden units (a whole tile writes its sum to its first slot and zeros to the
+        // second); score_finalize_kernel sums the slots in order.  32 outputs per pass over TMEM.
         float* w2s = reinterpret_cast<float*>(smem + kOffW2);
         float* b1s = reinterpret_cast<float*>(smem + kOffB1);
         named_bar_sync(1, 128);  // the previous tile's readers of w2s / b1s are done
-        for (int i = r; i < BN; i += 128) b1s[i] = p.b1 ? __ldg(p.b1 + n0 + i) : 0.f;
+        for (int i = r; i < bne; i += 128) b1s[i] = p.b1 ? __ldg(p.b1 + n0 + i) : 0.f;
+        const int slot = n0 / (BN / 2);
 #pragma unroll 1
         for (int og = 0; og < p.n_out; og += 32) {
           const int no = min(32, p.n_out - og);
           if (og > 0) named_bar_sync(1, 128);
-          for (int idx = r; idx < no * (BN / 4); idx += 128) {
-            const int oc = idx / (BN / 4), c4 = idx % (BN / 4);
+          for (int idx = r; idx < no * (bne / 4); idx += 128) {
+            const int oc = idx / (bne / 4), c4 = idx % (bne / 4);
             reinterpret_cast<float4*>(w2s + oc * BN)[c4] =
                 __ldg(reinterpret_cast<const float4*>(p.w2 + (size_t)(og + oc) * p.d_hidden + n0) + c4);
           }
@@ -290,7 +315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int oc = 0; oc < 32; ++oc) o[oc] = 0.f;
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = 0; c < bne; c += 32) {
             uint32_t zr[32];
             tmem_ld32(tacc + c, zr);
             tmem_wait_ld();
@@ -320,10 +345,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
           if (row_ok) {
-            float* dst = p.part + ((int64_t)nb * p.M + row) * p.n_out + og;
+            float* dst = p.part + ((int64_t)slot * p.M + row) * p.n_out + og;
+            float* dst2 = p.part + ((int64_t)(slot + 1) * p.M + row) * p.n_out + og;
 #pragma unroll
             for (int oc = 0; oc < 32; ++oc)
-              if (oc < no) dst[oc] = o[oc];
+              if (oc < no) {
+                dst[oc] = o[oc];
+                if (half < 0) dst2[oc] = 0.f;
+              }
           }
         }
       } else if (p.epi == APB_EPI_SWIGLU) {
@@ -414,7 +443,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int BN>
 static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtensorMap& ta1, const CUtensorMap& ta2,
-                                const CUtensorMap& tw, const CUtensorMap& tc, bool score, cudaStream_t stream) {
+                                const CUtensorMap& tw, const CUtensorMap& tc, const CUtensorMap* twh, bool score,
+                                cudaStream_t stream) {
   using C = Cfg<BN>;
   const int smem = score ? C::kSmemScore : C::kSmem;
   p.num_m = (int)((p.M + 2 * BM - 1) / (2 * BM));
@@ -448,8 +478,17 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int pairs = std::min(p.num_tiles, sms / 2);
-  gemm_kernel<BN><<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, tc, p);
+  const int npairs = sms / 2;
+  p.n_items = p.n_full = p.num_tiles;
+  const int tail = p.num_tiles % npairs;
+  const char* split_env = std::getenv("APB_GEMM_TAIL_SPLIT");  // timing experiments: "0" disables
+  if (twh && tail > 0 && 2 * tail <= npairs && p.num_tiles > npairs && !(split_env && split_env[0] == '0')) {
+    // a partial last wave: its tiles run as half tiles (twice as many, half as long)
+    p.n_full = p.num_tiles - tail;
+    p.n_items = p.n_full + 2 * tail;
+  }
+  const int pairs = std::min(p.n_items, npairs);
+  gemm_kernel<BN><<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, tc, twh ? *twh : tw, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   count_launch();
@@ -536,7 +575,7 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
     uint32_t box[2] = {32, BM};
     if (!make_tmap_bf16(&tc, g.c, 2, dims, str, box, 64)) return APB_ERR_CUDA;
   }
-  return launch_params<256>(p, ta, ta, ta, tw, tc, false, stream);
+  return launch_params<256>(p, ta, ta, ta, tw, tc, nullptr, false, stream);
 }
 
 // Hidden-unit tile of the scoring GEMM: 256 (default) or 128 (APB_SCORE_BN=128).  Measured on the
@@ -551,7 +590,8 @@ int score_tile_n() {
 }
 
 apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, const CUtensorMap& tw1, float* part, cudaStream_t stream) {
+                             const CUtensorMap& tv, const CUtensorMap& tw1, const CUtensorMap& tw1h, float* part,
+                             cudaStream_t stream) {
   using namespace gemm;
   Params p{};
   p.M = sp.l_b;
@@ -567,10 +607,10 @@ apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const
   p.d_hidden = sp.d_hidden;
   p.part = part;
   const int bn = score_tile_n();
-  apb_status st = bn == 128 ? launch_params<128>(p, tq, tk, tv, tw1, tw1 /* no tile stores */, true, stream)
-                            : launch_params<256>(p, tq, tk, tv, tw1, tw1, true, stream);
+  apb_status st = bn == 128 ? launch_params<128>(p, tq, tk, tv, tw1, tw1 /* no tile stores */, &tw1h, true, stream)
+                            : launch_params<256>(p, tq, tk, tv, tw1, tw1, &tw1h, true, stream);
   if (st) return st;
-  const int n_parts = (sp.d_hidden + bn - 1) / bn;
+  const int n_parts = (sp.d_hidden + bn / 2 - 1) / (bn / 2);  // one partial slot per bn/2 hidden units
   score_finalize_kernel<<<(sp.l_b + 127) / 128, 128, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
                                                                    sp.scores);
   cudaError_t e = cudaGetLastError();

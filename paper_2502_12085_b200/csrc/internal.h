@@ -58,11 +58,13 @@ struct ScoreParams {
 };
 apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream);
-// CTA-pair GEMM form (gemm_sm100.cu): partials [d_hidden/BN][l_b][n_out] in `part`, then a
-// fixed-order finalize (tw1: box {64, BN/2}, BN = score_tile_n())
+// CTA-pair GEMM form (gemm_sm100.cu): partials [d_hidden/(BN/2)][l_b][n_out] in `part`, then a
+// fixed-order finalize (tw1: box {64, BN/2}, tw1h: box {64, BN/4} for the half tiles of the last
+// wave; BN = score_tile_n())
 int score_tile_n();  // hidden units per scoring GEMM tile (128 or 256)
 apb_status launch_score_gemm(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, const CUtensorMap& tw1, float* part, cudaStream_t stream);
+                             const CUtensorMap& tv, const CUtensorMap& tw1, const CUtensorMap& tw1h, float* part,
+                             cudaStream_t stream);
 
 // ---------------------------------------------------------------- selection + compaction
 apb_status launch_rmsnorm(int64_t rows, int dim, const void* x, int64_t xs, const void* w, float eps, void* y,
