@@ -408,7 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else {
         uint16_t* dst = p.c + row * p.ldc + n0;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < bne; c += 32) {
           const int ncols = min(32, p.N - (n0 + c));
           float old[32];
           if (p.epi == APB_EPI_RESIDUAL && row_ok && ncols > 0) load32(dst + c, old, ncols);
@@ -567,6 +567,16 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   p.pos_offset = g.pos_offset;
   p.log2_theta = g.theta > 0.f ? std::log2((double)g.theta) : 0.0;
   p.kq = p.kqk = (g.K + BK - 1) / BK;
+  // STORE / RESIDUAL can run the tiles of a partial last wave as half tiles (SWIGLU's tile holds
+  // gate and up halves, ROPE's whole heads: they keep whole tiles)
+  CUtensorMap twh;
+  const bool halves = g.epi == APB_EPI_STORE || g.epi == APB_EPI_RESIDUAL;
+  if (halves) {
+    uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.N};
+    uint64_t str[1] = {(uint64_t)g.ldw * 2};
+    uint32_t box[2] = {BK, 64};
+    if (!make_tmap_bf16(&twh, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
+  }
   CUtensorMap tc;
   {
     const uint64_t ncols = g.epi == APB_EPI_SWIGLU ? (uint64_t)g.N / 2 : (uint64_t)g.N;
@@ -575,7 +585,7 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
     uint32_t box[2] = {32, BM};
     if (!make_tmap_bf16(&tc, g.c, 2, dims, str, box, 64)) return APB_ERR_CUDA;
   }
-  return launch_params<256>(p, ta, ta, ta, tw, tc, nullptr, false, stream);
+  return launch_params<256>(p, ta, ta, ta, tw, tc, halves ? &twh : nullptr, false, stream);
 }
 
 // Hidden-unit tile of the scoring GEMM: 256 (default) or 128 (APB_SCORE_BN=128).  Measured on the
