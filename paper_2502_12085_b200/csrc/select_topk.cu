@@ -309,6 +309,35 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wtot) 
   return incl - v + wtot[32 + warp];
 }
 
+// Block exclusive scan of one 32-bit value per thread (NT threads, NT/32 <= 32 warps).
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan_n(uint32_t v, uint32_t* wtot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kW = NT / 32;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wt = lane < kW ? wtot[lane] : 0u;
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kW) wtot[32 + lane] = wi - wt;
+  }
+  __syncthreads();
+  const uint32_t r = incl - v + wtot[32 + warp];
+  __syncthreads();  // wtot may be reused right after
+  return r;
+}
+
 // Register variant (l_b <= 1024 * KPT, every paper config): thread t holds the keys of indices
 // [t*KPT, (t+1)*KPT) in registers.  Digit 1 (bits 31..21) histograms every key; the keys in the
 // chosen bin are then compacted into a shared candidate list (one block scan, no contended
@@ -470,6 +499,255 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- cluster select + fused gather
+// select_cluster_kernel<KPT>: one cluster of kCC = 8 CTAs (512 threads each) per KV head; CTA c of
+// the cluster owns the contiguous index range [c*per, (c+1)*per) of the head's l_b scores, KPT
+// order-preserving keys per thread in registers.  The three radix digits (bits 31..21, 20..10,
+// 9..0) are counted in a private shared histogram per CTA; after one cluster barrier every CTA
+// sums the 8 histograms through distributed shared memory (ld.shared::cluster.v4, fixed order, so
+// every CTA derives the same bin) and runs the suffix search locally — no CTA waits on another
+// beyond the barrier.  The ordered output: per-CTA (> T, == T) totals are exchanged the same way,
+// each thread writes its ascending indices at its global position (ties -> lower index, reading
+// G5), and after a last cluster barrier (release / acquire at cluster scope: the indices written
+// to global by the other CTAs are visible) CTA c copies rows [c*lp/8, (c+1)*lp/8) of the send slot
+// — the gather is spread evenly over the cluster whatever the positions of the selected keys.
+// One launch replaces select + gather; 8 * hk CTAs share the select's latency-bound phases and the
+// 2 * hk * l_p' * d * 2 B copy.
+using namespace apb::sm100;
+constexpr int kCC = 8;     // CTAs per cluster (one cluster per KV head)
+constexpr int kCT = 512;   // threads per CTA
+
+// Suffix search over nb = kCT * BPT bins whose counts thread t holds for bins [t*BPT, t*BPT+BPT).
+template <int BPT>
+__device__ __forceinline__ void find_bin_regs(const uint32_t (&c)[BPT], uint32_t kk, uint32_t* wtot, uint32_t* sh_bin,
+                                              uint32_t* sh_k) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = kCT / 32;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) mine += c[q];
+  uint32_t incl = mine;  // suffix within the warp (lanes >= lane)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
+    if (lane + o < 32) incl += y;
+  }
+  if (lane == 0) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {  // exclusive suffix over the warp totals
+    const uint32_t wt = lane < kW ? wtot[lane] : 0u;
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, wi, o);
+      if (lane + o < 32) wi += y;
+    }
+    if (lane < kW) wtot[32 + lane] = wi - wt;
+  }
+  __syncthreads();
+  uint32_t above = incl - mine + wtot[32 + warp];  // keys in bins above this thread's bins
+#pragma unroll
+  for (int q = BPT - 1; q >= 0; --q) {
+    if (above < kk && above + c[q] >= kk) {
+      *sh_bin = (uint32_t)(tid * BPT + q);
+      *sh_k = kk - above;
+    }
+    above += c[q];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint4 ld_dsmem_v4(uint32_t cluster_addr) {
+  uint4 r;
+  // not volatile / no memory clobber: the cluster barriers order these loads, and the compiler may
+  // then keep several in flight
+  asm("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(cluster_addr));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t cluster_addr) {
+  uint32_t r;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(r) : "r"(cluster_addr) : "memory");
+  return r;
+}
+
+template <int KPT, int D>
+__global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCT, 1)
+    select_cluster_kernel(const float* __restrict__ scores, int l_b, int lp, int32_t* __restrict__ indices,
+                          const uint16_t* __restrict__ k, const uint16_t* __restrict__ v, int64_t kv_row_stride,
+                          int L_A, int hk, const GatherDst dst) {
+  __shared__ __align__(16) uint32_t hist[3][2048];
+  __shared__ uint32_t wtot[64];
+  __shared__ uint32_t tot[2];  // this CTA's (> T, == T) counts
+  __shared__ uint32_t sh_bin, sh_k;
+  const int tid = threadIdx.x;
+  const uint32_t c = cluster_ctarank();
+  const int j = blockIdx.y;
+  const float* s = scores + (int64_t)j * l_b;
+  const int per = ((l_b + kCC - 1) / kCC + 3) & ~3;
+  const int lo = min(l_b, (int)c * per), hi = min(l_b, lo + per);
+  const int e0 = lo + tid * KPT;
+  uint32_t key[KPT];
+  if (e0 + KPT <= hi && (l_b & 3) == 0) {
+#pragma unroll
+    for (int e = 0; e < KPT; e += 4) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(s + e0 + e));
+      key[e] = order_key(f.x);
+      key[e + 1] = order_key(f.y);
+      key[e + 2] = order_key(f.z);
+      key[e + 3] = order_key(f.w);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) key[e] = e0 + e < hi ? order_key(__ldg(s + e0 + e)) : 0u;
+  }
+  const int nmine = max(0, min(KPT, hi - e0));
+  for (int b = tid; b < 3 * 2048; b += kCT) (&hist[0][0])[b] = 0;
+  __syncthreads();
+
+  uint32_t prefix = 0, kk = (uint32_t)lp;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int shift = d == 0 ? 21 : (d == 1 ? 10 : 0);
+    const uint32_t pmask = d == 0 ? 0u : (d == 1 ? 0xFFE00000u : 0xFFFFFC00u);
+    const uint32_t dmask = d == 2 ? 0x3FFu : 0x7FFu;
+#pragma unroll
+    for (int e = 0; e < KPT; ++e)
+      if (e < nmine && (key[e] & pmask) == prefix) atomicAdd(&hist[d][(key[e] >> shift) & dmask], 1u);
+    cluster_sync();  // every CTA's digit-d histogram is complete
+    constexpr int kBpt = 4;  // 2048 bins / 512 threads (digit 3: 1024 bins, the upper half stays 0)
+    uint32_t cnt[kBpt] = {0u, 0u, 0u, 0u};
+    const uint32_t local = smem_u32(&hist[d][tid * kBpt]);
+    uint4 q[kCC];  // all 8 remote loads in flight before the first add
+#pragma unroll
+    for (int r = 0; r < kCC; ++r) q[r] = ld_dsmem_v4(mapa_shared(local, (uint32_t)r));
+#pragma unroll
+    for (int r = 0; r < kCC; ++r) {
+      cnt[0] += q[r].x;
+      cnt[1] += q[r].y;
+      cnt[2] += q[r].z;
+      cnt[3] += q[r].w;
+    }
+    find_bin_regs<kBpt>(cnt, kk, wtot, &sh_bin, &sh_k);
+    prefix |= sh_bin << shift;
+    kk = sh_k;
+  }
+  const uint32_t T = prefix, need_eq = kk;  // key of the l_p'-th largest score; ties taken
+
+  // ---- ordered output: this CTA's position among the cluster's (> T, == T) counts
+  uint32_t gt = 0, eq = 0;
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    gt += (e < nmine && key[e] > T);
+    eq += (e < nmine && key[e] == T);
+  }
+  const uint32_t before = block_excl_scan_n<kCT>((gt << 16) | eq, wtot);
+  if (tid == kCT - 1) {
+    tot[0] = (before >> 16) + gt;
+    tot[1] = (before & 0xFFFFu) + eq;
+  }
+  cluster_sync();
+  uint32_t g_cta = 0, e_cta = 0;
+  if (tid < 32) {  // the totals of the CTAs before this one
+    uint32_t gg = 0, ee = 0;
+    if (tid < (int)c) {
+      gg = ld_dsmem_u32(mapa_shared(smem_u32(&tot[0]), (uint32_t)tid));
+      ee = ld_dsmem_u32(mapa_shared(smem_u32(&tot[1]), (uint32_t)tid));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gg += __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+      ee += __shfl_xor_sync(0xFFFFFFFFu, ee, o);
+    }
+    if (tid == 0) {
+      wtot[0] = gg;
+      wtot[1] = ee;
+    }
+  }
+  __syncthreads();
+  g_cta = wtot[0];
+  e_cta = wtot[1];
+  const uint32_t e_before = e_cta + (before & 0xFFFFu);
+  uint32_t pos = g_cta + (before >> 16) + min(need_eq, e_before);
+  uint32_t erank = e_before;
+  int32_t* out = indices + (int64_t)j * lp;
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    if (e < nmine) {
+      bool sel = key[e] > T;
+      if (key[e] == T) sel = erank++ < need_eq;
+      if (sel) out[pos++] = e0 + e;
+    }
+  }
+  cluster_sync();  // release / acquire at cluster scope: every CTA's indices are visible
+
+  // ---- gather: output rows [c*lp/8, (c+1)*lp/8) of K and V of head j into every destination
+  constexpr int kVec = D / 8;  // 16-byte vectors per row
+  constexpr int kBatch = 16;   // vectors per thread in flight (one batch at L8: 2 x 256 rows x 16)
+  const int r_lo = (int)(((int64_t)lp * c) / kCC), r_hi = (int)(((int64_t)lp * (c + 1)) / kCC);
+  const int nr = r_hi - r_lo;
+  const int n_vec = 2 * nr * kVec;  // K rows then V rows
+  for (int u0 = 0; u0 < n_vec; u0 += kBatch * kCT) {
+    int32_t src[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {  // the batch's source indices first: one L2 latency
+      const int u = u0 + q * kCT + tid;
+      const int w = u < nr * kVec ? u : u - nr * kVec;
+      src[q] = u < n_vec ? __ldcg(out + r_lo + w / kVec) : 0;
+    }
+    uint4 buf[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {  // then every row load: one HBM latency
+      const int u = u0 + q * kCT + tid;
+      if (u < n_vec) {
+        const int kv = u >= nr * kVec;
+        const int cv = u % kVec;
+        const uint16_t* row = (kv ? v : k) + (L_A + (int64_t)src[q]) * kv_row_stride + (int64_t)j * D;
+        buf[q] = __ldg(reinterpret_cast<const uint4*>(row) + cv);
+      }
+    }
+    for (int dd = 0; dd < dst.n; ++dd) {
+      uint4* o = reinterpret_cast<uint4*>(dst.send[dd]);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) {
+        const int u = u0 + q * kCT + tid;
+        if (u < n_vec) {
+          const int kv = u >= nr * kVec;
+          const int w = kv ? u - nr * kVec : u;
+          o[((((int64_t)kv * hk + j) * lp + r_lo) * D) / 8 + w] = buf[q];
+        }
+      }
+    }
+  }
+  if (dst.flag[0] != nullptr) {
+    __threadfence_system();  // this thread's peer stores are visible system-wide
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t n_ctas = gridDim.x * gridDim.y * gridDim.z;
+      const uint32_t done = atomicAdd(dst.counter, 1u) + 1u;
+      if (done % n_ctas == 0) {  // the last CTA of this launch: every CTA's stores are fenced
+        __threadfence_system();
+        for (int dd = 0; dd < dst.n; ++dd)
+          asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(dst.flag[dd]), "r"(dst.epoch) : "memory");
+      }
+    }
+  }
+}
+
+template <int KPT>
+static cudaError_t launch_cluster(int D, const float* scores, int l_b, int lp, int hk, int32_t* indices,
+                                  const void* k, const void* v, int64_t kv_row_stride, int L_A, const GatherDst& dst,
+                                  cudaStream_t stream) {
+  const dim3 grid(kCC, hk);
+  if (D == 128)
+    select_cluster_kernel<KPT, 128><<<grid, kCT, 0, stream>>>(scores, l_b, lp, indices, static_cast<const uint16_t*>(k),
+                                                             static_cast<const uint16_t*>(v), kv_row_stride, L_A, hk, dst);
+  else
+    select_cluster_kernel<KPT, 64><<<grid, kCT, 0, stream>>>(scores, l_b, lp, indices, static_cast<const uint16_t*>(k),
+                                                            static_cast<const uint16_t*>(v), kv_row_stride, L_A, hk, dst);
+  return cudaGetLastError();
+}
+
 template <bool kSmem>
 static apb_status launch_fast(const float* scores, int l_b, int lp, int hk, int32_t* indices, cudaStream_t stream) {
   static std::atomic<uint64_t> smem_set{0};
@@ -504,6 +782,27 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
                                  const void* v, int64_t kv_row_stride, int32_t* indices, void* send,
                                  cudaStream_t stream, const GatherDst* push) {
   const char* env = std::getenv("APB_SELECT");
+  GatherDst local{};
+  if (!push) {
+    local.n = 1;
+    local.send[0] = static_cast<uint16_t*>(send);
+  }
+  const GatherDst& dst = push ? *push : local;
+  // l_b > 32K (the 512K / 1M configs): one launch, an 8-CTA cluster per KV head (select + gather;
+  // 1M host: 30.8 vs 106.6 us for the staged single-CTA select + gather).  Up to 32K the single-CTA
+  // register select + PDL gather is faster (L8: 14.6 vs 21.8 us queued): the cluster's three
+  // distributed-shared-memory histogram reductions (8 x 2048 bins read by every CTA) cost ~2 us
+  // each, more than the single CTA's extra keys.  APB_SELECT=reg / legacy force the other paths.
+  const int per = ((l_b + sel::kCC - 1) / sel::kCC + 3) & ~3;  // keys per cluster CTA
+  if (!(env && (env[0] == 'l' || env[0] == 'r')) && l_b > 32 * sel::kFT && per <= 32 * sel::kCT &&
+      (D == 128 || D == 64)) {
+    cudaError_t e = per <= 16 * sel::kCT
+                        ? sel::launch_cluster<16>(D, scores, l_b, lp, hk, indices, k, v, kv_row_stride, L_A, dst, stream)
+                        : sel::launch_cluster<32>(D, scores, l_b, lp, hk, indices, k, v, kv_row_stride, L_A, dst, stream);
+    if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("select_cluster launch: ") + cudaGetErrorString(e));
+    count_launch(1);
+    return APB_OK;
+  }
   if (push || !(env && env[0] == 'l')) {
     apb_status st = APB_OK;
     if (l_b <= 16 * sel::kFT)
@@ -521,12 +820,6 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
       count_launch(1);
       return APB_OK;
     }
-    GatherDst local{};
-    if (!push) {
-      local.n = 1;
-      local.send[0] = static_cast<uint16_t*>(send);
-    }
-    const GatherDst& dst = push ? *push : local;
     e = D == 128 ? sel::launch_gather<128>(indices, k, v, kv_row_stride, L_A, lp, hk, dst, stream)
                  : sel::launch_gather<64>(indices, k, v, kv_row_stride, L_A, lp, hk, dst, stream);
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gather launch: ") + cudaGetErrorString(e));

@@ -236,18 +236,24 @@ def test_select_sizes(lp, l_b):
     assert np.array_equal(send, oracle.compact(x["k"], x["v"], x["L_A"], idx_or))
 
 
-@pytest.mark.parametrize("lp,l_b,ties", [(2048, 16384, False), (2048, 16384, True), (64, 512, True), (3000, 400000, True)])
+@pytest.mark.parametrize("lp,l_b,ties", [(2048, 16384, False), (2048, 16384, True), (64, 512, True), (3000, 400000, True),
+                                         (2048, 131072, True), (4096, 131076, False), (129, 1001, True),
+                                         (1000, 1000, True), (25, 26, False), (8192, 65536, True),
+                                         (2048, 40001, False), (40000, 40000, True)])
 def test_select_cluster_equals_legacy(lp, l_b, ties, monkeypatch):
-    """The one-launch cluster select + compaction and the round-1 two-kernel path (APB_SELECT=legacy)
-    produce identical indices and send payloads (both bit-exact integer logic)."""
+    """The default path (l_b <= 32K: single-CTA register select + PDL gather; up to 128K: one-launch
+    8-CTA cluster select + gather; beyond: staged select), the single-CTA paths (APB_SELECT=reg)
+    and the round-1 two-kernel path (APB_SELECT=legacy) produce identical indices and send payloads
+    (all bit-exact integer logic)."""
     cfg = synth.Config("sel", 19, n=l_b * 2, H=2, l_a=8, l_p=lp, hq=8, hk=4, d=128, d_hidden=256)
     x = synth.host_qkv(cfg, 0, 1)
     sc = synth.random_scores(cfg, 0, 1, ties=ties)
     res = []
-    for env in ("", "legacy"):
+    for env in ("", "reg", "legacy"):
         monkeypatch.setenv("APB_SELECT", env)
         res.append(_select_gpu(cfg, 1, x, sc))
-    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    for r in res[1:]:
+        assert np.array_equal(res[0][0], r[0]) and np.array_equal(res[0][1], r[1])
 
 
 # ----------------------------------------------------------------------------- whole layer

@@ -121,3 +121,34 @@ def test_peer_exchange_two_ranks_one_gpu(layout):
             O_or, _ = oracle.attention(x["q"], x["k"], x["v"], x["L_A"], pk, pv)
             err = np.abs(outs[h][0] - O_or)
             assert err.max() <= 2e-2 and err.mean() <= 2e-3, (layer, h, err.max(), err.mean())
+
+
+@pytest.mark.parametrize("l_b,lp", [(2048, 256), (40000, 2048), (131072, 2048)])
+def test_peer_push_single_rank_matches_oracle(l_b, lp):
+    """The compaction's peer push (apb_select_topk_peers) at l_b in both select regimes (single-CTA
+    register select + PDL gather up to 32K; the 8-CTA cluster kernel beyond): a one-rank Peers
+    (its own buffer is its only destination); indices bit-exact against the
+    oracle's stable sort, the pushed slot bit-exact against oracle.compact."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2502_12085_b200 import apb
+    cfg = synth.Config("push", 23, n=2 * l_b, H=2, l_a=8, l_p=lp, hq=8, hk=4, d=128, d_hidden=256)
+    x = synth.host_qkv(cfg, 0, 1)
+    sc = synth.random_scores(cfg, 0, 1, ties=True)
+    base = apb.Dims(n=cfg.n, H=cfg.H, host=1, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
+                    head_dim=cfg.d)
+    peers = apb.Peers(base, 1, 0)
+    peers.open([peers.handle])
+    try:
+        s = torch.from_numpy(np.ascontiguousarray(sc, dtype=np.float32)).cuda()
+        idx = torch.full((cfg.hk, cfg.l_pp), -1, dtype=torch.int32, device="cuda")
+        peers.select_topk(base, s, _dev(x["k"]), _dev(x["v"]), idx, 1)
+        torch.cuda.synchronize()
+    except Exception:
+        peers.close()
+        raise
+    idx_or = oracle.select_all_heads(sc.astype(np.float64), cfg.l_p)
+    assert np.array_equal(idx.cpu().numpy(), idx_or)
+    g = peers.gathered(1).view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(g[1], oracle.compact(x["k"], x["v"], x["L_A"], idx_or))
+    peers.close()
