@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--attn-launch", choices=["batched", "per-host"], default="batched",
+                    help="batched: one attention launch per phase over every owned host (apb_attention_fwd_hosts; "
+                         "single rank: compress every host first, then the layer's attention as one launch); "
+                         "per-host: one launch per host (single rank: ordered, compression on a side stream)")
     ap.add_argument("--schedule", choices=["auto", "split", "ordered"], default="auto",
                     help="auto: LOCAL/PASSING split around the exchange only when N > 1")
     ap.add_argument("--same-device", action="store_true",
@@ -336,7 +340,7 @@ def main():
         split = True  # the multi-rank schedule (a real exchange with --exchange peer, the default here)
     pr = PrefillRank(base, hosts, comm, dev, skip_unused_last=True, split_phases=split,
                      compressor=args.compressor, shared_set=args.shared_set, seed=2502,
-                     same_device=args.same_device and peers is None, peers=peers)
+                     same_device=args.same_device and peers is None, peers=peers, batched=args.attn_launch == "batched")
 
     # ---- synthetic inputs: D1 N(0,1) Q/K/V (the paper's timing input is synthetic random
     # input), two alternating layer buffer sets, random-init retaining heads.
@@ -433,8 +437,10 @@ def main():
                                                          and (not pr.split_phases
                                                               or os.environ.get("APB_ATTN_PAIR", "")[:1] == "1")
                                                          else "") + "> ("
-                + ("LOCAL + PASSING launches" if pr.split_phases
-                                                           else "one ordered PHASE_ALL launch per host") + ")",
+                + (("one LOCAL + one PASSING launch over the rank's hosts" if pr.batched
+                    else "LOCAL + PASSING launches") if pr.split_phases
+                   else ("one PHASE_ALL launch per layer over every host" if pr.batched
+                         else "one ordered PHASE_ALL launch per host")) + ")",
                 "peak_source": f"bf16_tflops_sustained, {peak_src}",
                 "flops_per_step": flops_rank * layers,
                 "executed_mma_flops_per_step": executed_rank * layers,
@@ -489,9 +495,10 @@ NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (hardware fact; no measured
 
 def op_breakdown(pr, step, cfg, H, hosts, layers, world, peaks, barrier):
     """Per-step device time of every libapb op of this rank (CUDA events around each call on the
-    stream it runs on; one extra untimed step), beside its roofline lower bound.  Side-stream
-    ops (score, select_compact, exchange) overlap the attention: these are op times, not a
-    partition of ms_per_step."""
+    stream it runs on; one extra untimed step), beside its roofline lower bound.  With a side
+    stream (N > 1, or --attn-launch per-host) score / select_compact / exchange overlap the
+    attention: these are op times, not a partition of ms_per_step (at N = 1 batched they run
+    serially on the main stream, before the layer's attention launch)."""
     pr.trace = []
     barrier()
     step()
@@ -516,12 +523,12 @@ def op_breakdown(pr, step, cfg, H, hosts, layers, world, peaks, barrier):
             e["lower_bound_ms"] += sel_bytes / hbm * 1e3
         elif name == "exchange":
             e["lower_bound_ms"] += recv / (NVLINK_GBS * 1e9) * 1e3
-        else:
-            L_A = 0 if h == 0 else cfg.l_q + cfg.l_a
-            f_all = workload.attention_flops(cfg.n, H, h, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q)
-            f_pass = 4 * cfg.d * cfg.hq * l_b * h * lpp
-            f = {"attn_all": f_all, "attn_local": f_all - f_pass, "attn_passing": f_pass}[name]
-            e["lower_bound_ms"] += f / tf * 1e3
+        else:  # one host, or (h = -1) one batched launch over every owned host
+            for hh in (hosts if h < 0 else [h]):
+                f_all = workload.attention_flops(cfg.n, H, hh, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q)
+                f_pass = 4 * cfg.d * cfg.hq * l_b * hh * lpp
+                f = {"attn_all": f_all, "attn_local": f_all - f_pass, "attn_passing": f_pass}[name]
+                e["lower_bound_ms"] += f / tf * 1e3
     for name, e in out.items():
         e["us_per_launch"] = round(1e3 * e["ms_per_step"] / max(e["launches"], 1), 2)
         e["frac_of_bound"] = round(e["lower_bound_ms"] / e["ms_per_step"], 4) if e["ms_per_step"] > 0 else None

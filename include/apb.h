@@ -299,6 +299,24 @@ apb_status apb_attention_fwd(const apb_dims* dims, const void* q, const void* k,
                              void* out, int64_t out_row_stride, float* lse, apb_phase phase,
                              void* ws, size_t ws_bytes, apb_stream_t stream);
 
+/* The same attention for n (1..8) hosts of ONE rank in one kernel launch — exactly the n
+ * apb_attention_fwd calls, with one grid over every host's work items, so the per-host launch
+ * ramp and tail are paid once (Alg. apb_prefill P:728 runs on every host; a rank that owns
+ * several hosts, N < H, runs them all).
+ *  dims[i]    host i's dims: every field equal across the n entries except `host`, and no host
+ *             twice (else APB_ERR_CONFIG).
+ *  q/k/v/out/lse/ws/ws_bytes: HOST arrays of n per-host values, each as in apb_attention_fwd
+ *             (lse and ws/ws_bytes may be NULL arrays: no lse / no workspace); strides shared.
+ *  gathered   the one passing buffer every host reads (its own slots 0..host-1).
+ * Validation is per host, as apb_attention_fwd; nothing is launched unless every host passes.
+ * Items run heaviest host first (the lightest host's items form the launch's tail).
+ * Outputs are bit-identical to the per-host calls.                                           */
+apb_status apb_attention_fwd_hosts(int32_t n, const apb_dims* dims, const void* const* q,
+                                   const void* const* k, const void* const* v, int64_t q_row_stride,
+                                   int64_t kv_row_stride, const void* gathered, void* const* out,
+                                   int64_t out_row_stride, float* const* lse, apb_phase phase,
+                                   void* const* ws, const size_t* ws_bytes, apb_stream_t stream);
+
 /* ---------------------------------------------------------------- decode step
  * Alg. apb_decode ("Accu"): after prefill every host holds its block's KV cache
  * (P:675-678).  For t new tokens (t = 1 when generating; the whole query chunk on the first

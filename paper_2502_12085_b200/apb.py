@@ -35,7 +35,7 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check", "apb_comm_abort",
             "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size",
             "apb_peers_create", "apb_peers_open", "apb_peers_gathered", "apb_select_topk_peers", "apb_peers_wait",
-            "apb_peers_release", "apb_peers_destroy")
+            "apb_peers_release", "apb_peers_destroy", "apb_attention_fwd_hosts")
 
 
 class ApbError(RuntimeError):
@@ -88,6 +88,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.apb_exchange_passing.argtypes = [vp, dp, vp, vp]
     lib.apb_exchange_passing_cyclic.argtypes = [vp, dp, vp, vp]
     lib.apb_attention_fwd.argtypes = [dp, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.c_int, vp, sz, vp]
+    lib.apb_attention_fwd_hosts.argtypes = [i32, dp, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.c_int, vp, vp, vp]
     lib.apb_comm_get_unique_id.argtypes = [ctypes.c_char_p]
     lib.apb_comm_init.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
     lib.apb_comm_destroy.argtypes = [vp]
@@ -128,7 +129,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
               "apb_exchange_passing_cyclic", "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check",
               "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size",
               "apb_peers_create", "apb_peers_open", "apb_peers_gathered", "apb_select_topk_peers", "apb_peers_wait",
-              "apb_peers_release", "apb_peers_destroy"):
+              "apb_peers_release", "apb_peers_destroy", "apb_attention_fwd_hosts"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -361,6 +362,40 @@ def attention_fwd(dims: Dims, q, k, v, gathered, out, lse=None, phase: int = PHA
                                     _rowstride(k, "k"), _ptr(gathered), out.data_ptr(), _rowstride(out, "out"),
                                     _ptr(lse), phase, _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                                     _stream(stream)), "apb_attention_fwd")
+
+
+def attention_fwd_hosts(dims: list[Dims], q: list, k: list, v: list, gathered, out: list, lse: list | None = None,
+                        phase: int = PHASE_ALL, ws: list | None = None, stream=None) -> None:
+    """apb_attention_fwd_hosts: the attention of several hosts (dims[i].host) in one launch —
+    the same results as one attention_fwd call per host."""
+    n = len(dims)
+    if not (1 <= n <= 8) or not (len(q) == len(k) == len(v) == len(out) == n):
+        raise ApbError(ERR_CONTRACT, "hosts", "1..8 hosts with one q/k/v/out each")
+    if lse is not None and len(lse) != n or ws is not None and len(ws) != n:
+        raise ApbError(ERR_CONTRACT, "hosts", "lse / ws need one entry per host")
+    for i in range(n):
+        _check_qkv(dims[i], q[i], k[i], v[i])
+        _need(out[i], "out", torch.bfloat16, dims[i].rows, dims[i].n_heads * dims[i].head_dim)
+        if lse is not None and lse[i] is not None:
+            _need(lse[i], "lse", torch.float32, dims[i].n_heads, dims[i].rows, dense=True)
+            if lse[i].dim() != 2 or lse[i].shape[1] != dims[i].rows:
+                raise ApbError(ERR_CONTRACT, "lse", f"must be [n_heads][{dims[i].rows}]")
+        if ws is not None and ws[i] is not None:
+            _need(ws[i], "ws", ws[i].dtype, dense=True)
+        if _rowstride(q[i], "q") != _rowstride(q[0], "q") or _rowstride(k[i], "k") != _rowstride(k[0], "k") \
+                or _rowstride(out[i], "out") != _rowstride(out[0], "out"):
+            raise ApbError(ERR_CONTRACT, "hosts", "the hosts' q / kv / out row strides must be equal")
+    if gathered is not None and any(d.P > 0 for d in dims) and phase != PHASE_LOCAL:
+        d0 = dims[0]
+        _need_numel(gathered, "gathered", torch.bfloat16, d0.H * 2 * d0.n_kv_heads * d0.l_pp * d0.head_dim)
+    cd = (_Dims * n)(*[d.c() for d in dims])
+    arr = lambda xs: (ctypes.c_void_p * n)(*[_ptr(x) for x in xs])  # noqa: E731
+    ws_b = None if ws is None else (ctypes.c_size_t * n)(*[0 if w is None else w.numel() * w.element_size() for w in ws])
+    _check(load().apb_attention_fwd_hosts(n, cd, arr(q), arr(k), arr(v), _rowstride(q[0], "q"), _rowstride(k[0], "k"),
+                                          _ptr(gathered), arr(out), _rowstride(out[0], "out"),
+                                          None if lse is None else arr(lse), phase,
+                                          None if ws is None else arr(ws), ws_b, _stream(stream)),
+           "apb_attention_fwd_hosts")
 
 
 # ----------------------------------------------------------------------------- model layer (NEXT #2)

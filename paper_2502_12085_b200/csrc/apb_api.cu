@@ -14,6 +14,8 @@
 #include <cudaTypedefs.h>
 #include <nccl.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace apb {
@@ -161,10 +163,13 @@ extern "C" apb_status apb_workspace_size(const apb_dims* d, apb_ws_kind which, s
 }
 
 // ---------------------------------------------------------------- step 4: attention
-extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const void* k, const void* v,
-                                        int64_t q_row_stride, int64_t kv_row_stride, const void* gathered, void* out,
-                                        int64_t out_row_stride, float* lse, apb_phase phase, void* ws, size_t ws_bytes,
-                                        apb_stream_t stream) {
+// Validation and launch parameters of one host's attention (apb_attention_fwd and each host of
+// apb_attention_fwd_hosts).  *skip: nothing to compute (PASSING without passing keys).
+static apb_status attention_setup(const apb_dims* d, const void* q, const void* k, const void* v, int64_t q_row_stride,
+                                  int64_t kv_row_stride, const void* gathered, void* out, int64_t out_row_stride,
+                                  float* lse, apb_phase phase, void* ws, size_t ws_bytes, AttnParams& p,
+                                  CUtensorMap& tq, CUtensorMap& tk, CUtensorMap& tv, CUtensorMap& tg, bool* skip) {
+  *skip = false;
   apb_status st = check_dims(d);
   if (st) return st;
   if (phase != APB_PHASE_ALL && phase != APB_PHASE_LOCAL && phase != APB_PHASE_PASSING)
@@ -187,10 +192,12 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
   const bool use_ws = has_pass && phase != APB_PHASE_ALL;
   if (use_ws && (ws == nullptr || ws_bytes < need || !aligned16(ws)))
     return fail(APB_ERR_CONTRACT, "attention workspace missing, too small or misaligned");
-  if ((st = check_device())) return st;
-  if (phase == APB_PHASE_PASSING && !has_pass) return APB_OK;  // nothing to merge
+  if (phase == APB_PHASE_PASSING && !has_pass) {  // nothing to merge
+    *skip = true;
+    return APB_OK;
+  }
 
-  AttnParams p{};
+  p = AttnParams{};
   p.L_A = (int)L_A;
   p.l_b = d->l_b;
   p.lp = (int)lpp;
@@ -223,7 +230,6 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
   }
 
   if (const char* dbg = std::getenv("APB_DEBUG_SKIP")) p.dbg_skip = std::atoi(dbg);  // timing experiments only
-  CUtensorMap tq, tk, tv, tg;
   {
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)rows};
     uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};
@@ -245,7 +251,71 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
   } else {
     tg = tk;  // never dereferenced
   }
-  return launch_attention(D, p, tq, tk, tv, tg, reinterpret_cast<cudaStream_t>(stream));
+  return APB_OK;
+}
+
+extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const void* k, const void* v,
+                                        int64_t q_row_stride, int64_t kv_row_stride, const void* gathered, void* out,
+                                        int64_t out_row_stride, float* lse, apb_phase phase, void* ws, size_t ws_bytes,
+                                        apb_stream_t stream) {
+  AttnParams p;
+  CUtensorMap tq, tk, tv, tg;
+  bool skip = false;
+  apb_status st = attention_setup(d, q, k, v, q_row_stride, kv_row_stride, gathered, out, out_row_stride, lse, phase,
+                                  ws, ws_bytes, p, tq, tk, tv, tg, &skip);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if (skip) return APB_OK;
+  return launch_attention(d->head_dim, p, tq, tk, tv, tg, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" apb_status apb_attention_fwd_hosts(int32_t n, const apb_dims* dims, const void* const* q,
+                                              const void* const* k, const void* const* v, int64_t q_row_stride,
+                                              int64_t kv_row_stride, const void* gathered, void* const* out,
+                                              int64_t out_row_stride, float* const* lse, apb_phase phase,
+                                              void* const* ws, const size_t* ws_bytes, apb_stream_t stream) {
+  if (n < 1 || n > kAttnMaxHosts) return fail(APB_ERR_CONFIG, "n must be in [1, 8]");
+  if (!dims || !q || !k || !v || !out) return fail(APB_ERR_CONTRACT, "dims/q/k/v/out array is NULL");
+  // every host of one launch shares the problem (only `host` differs) and no host appears twice
+  for (int i = 0; i < n; ++i) {
+    const apb_dims& a = dims[i];
+    const apb_dims& b = dims[0];
+    if (a.n != b.n || a.H != b.H || a.l_q != b.l_q || a.l_a != b.l_a || a.l_p != b.l_p || a.n_heads != b.n_heads ||
+        a.n_kv_heads != b.n_kv_heads || a.head_dim != b.head_dim || a.softmax_scale != b.softmax_scale)
+      return fail(APB_ERR_CONFIG, "the hosts of one launch must share every dimension but `host`");
+    for (int j = 0; j < i; ++j)
+      if (dims[j].host == a.host) return fail(APB_ERR_CONFIG, "a host appears twice");
+  }
+  // heaviest host first (host h attends to h * l_p' passing keys): the lightest items form the tail
+  int order[kAttnMaxHosts];
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::sort(order, order + n, [&](int x, int y) { return dims[x].host > dims[y].host; });
+  AttnLaunch La{};
+  La.n = 0;
+  La.item_begin[0] = 0;
+  bool have_g = false;
+  for (int oi = 0; oi < n; ++oi) {
+    const int i = order[oi];
+    CUtensorMap tg;
+    bool skip = false;
+    apb_status st = attention_setup(&dims[i], q[i], k[i], v[i], q_row_stride, kv_row_stride, gathered, out[i],
+                                    out_row_stride, lse ? lse[i] : nullptr, phase, ws ? ws[i] : nullptr,
+                                    ws_bytes ? ws_bytes[i] : 0, La.p[La.n], La.tq[La.n], La.tk[La.n], La.tv[La.n], tg,
+                                    &skip);
+    if (st) return st;
+    if (skip) continue;
+    if (La.p[La.n].n_slots > 0 && phase != APB_PHASE_LOCAL) {
+      La.tg = tg;
+      have_g = true;
+    }
+    La.item_begin[La.n + 1] = La.item_begin[La.n] + La.p[La.n].n_local_items + La.p[La.n].n_anchor_items;
+    ++La.n;
+  }
+  if (!have_g) La.tg = La.tk[0];  // never dereferenced
+  apb_status st = check_device();
+  if (st) return st;
+  if (La.n == 0) return APB_OK;
+  return launch_attention_hosts(dims[0].head_dim, La, (int)phase, reinterpret_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------- step 1: scoring

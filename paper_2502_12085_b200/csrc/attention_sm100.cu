@@ -230,9 +230,16 @@ __device__ __forceinline__ int visible_cols(const AttnParams& p, const Item& it,
 // local commits.
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
-    apb_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
-                         const AttnParams p) {
+    apb_attention_kernel(const __grid_constant__ AttnLaunch La) {
+  // this CTA's host (launch-uniform tables in the parameter space) and its item within the host
+  int hh = 0;
+  while (hh + 1 < La.n && static_cast<int>(blockIdx.x) >= La.item_begin[hh + 1]) ++hh;
+  const AttnParams& p = La.p[hh];
+  const int w_item = static_cast<int>(blockIdx.x) - La.item_begin[hh];
+  const CUtensorMap* tm_q = &La.tq[hh];
+  const CUtensorMap* tm_k = &La.tk[hh];
+  const CUtensorMap* tm_v = &La.tv[hh];
+  const CUtensorMap* tm_g = &La.tg;
   using L = Layout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
@@ -255,9 +262,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtr);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
-  const Item it = decode_item(p, blockIdx.x);
+  const Item it = decode_item(p, w_item);
   // K/V tiles shared with the partner CTA (PAIR): the common prefix of the two walks
-  const int n_shared = PAIR ? min(it.nkv, decode_item(p, blockIdx.x ^ 1).nkv) : 0;
+  const int n_shared = PAIR ? min(it.nkv, decode_item(p, w_item ^ 1).nkv) : 0;  // item_begin[] even
   CTA_TIME(0);
 
   if (threadIdx.x == 0) {
@@ -280,10 +287,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kLoadWarp) {
     tmem_alloc<512>(smem_u32(tmem_ptr));
     if (elect_one()) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      tma_prefetch_desc(&tm_g);
+      tma_prefetch_desc(tm_q);
+      tma_prefetch_desc(tm_k);
+      tma_prefetch_desc(tm_v);
+      tma_prefetch_desc(tm_g);
     }
     __syncwarp();
   }
@@ -315,9 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < it.ntiles; ++t)
           for (int h = 0; h < L::kHalves; ++h)
 #ifndef APB_NO_L2_HINTS
-            tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM, pol_q);
+            tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM, pol_q);
 #else
-            tma_load_3d(sQ + t * L::kTile + h * L::kSub, &tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM);
+            tma_load_3d(sQ + t * L::kTile + h * L::kSub, tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM);
 #endif
       }
       __syncwarp();
@@ -350,16 +357,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int h = static_cast<int>(cluster_ctarank());
               mbar_arrive_expect_tx(bRf(r), L::kTile);
               if (kt.kind == 1)
-                tma_load_4d_mc_hint(sR(r) + h * L::kSub, &tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv, 0x3, pol_kv);
+                tma_load_4d_mc_hint(sR(r) + h * L::kSub, tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv, 0x3, pol_kv);
               else
-                tma_load_3d_mc_hint(sR(r) + h * L::kSub, kv ? &tm_v : &tm_k, bRf(r), h * 64, it.j, row0, 0x3, pol_kv);
+                tma_load_3d_mc_hint(sR(r) + h * L::kSub, kv ? tm_v : tm_k, bRf(r), h * 64, it.j, row0, 0x3, pol_kv);
             } else {
               mbar_arrive_expect_tx(bRf(r), L::kTile);
               for (int h = 0; h < L::kHalves; ++h) {
                 if (kt.kind == 1)
-                  KV_LOAD4(sR(r) + h * L::kSub, &tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv);
+                  KV_LOAD4(sR(r) + h * L::kSub, tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv);
                 else
-                  KV_LOAD3(sR(r) + h * L::kSub, kv ? &tm_v : &tm_k, bRf(r), h * 64, it.j, row0);
+                  KV_LOAD3(sR(r) + h * L::kSub, kv ? tm_v : tm_k, bRf(r), h * 64, it.j, row0);
               }
             }
           }
@@ -809,10 +816,9 @@ static bool pair_enabled(int phase) {
 }
 
 template <int D, bool PAIR>
-static apb_status launch_impl(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                              const CUtensorMap& tg, cudaStream_t stream) {
+static apb_status launch_impl(const AttnLaunch& La, cudaStream_t stream) {
   using L = Layout<D>;
-  const int grid = p.n_local_items + p.n_anchor_items;
+  const int grid = La.item_begin[La.n];
   if (grid == 0) return APB_OK;
   static std::atomic<uint64_t> smem_set{0};
   if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(apb_attention_kernel<D, PAIR>), L::kAlloc, smem_set))
@@ -831,9 +837,9 @@ static apb_status launch_impl(const AttnParams& p, const CUtensorMap& tq, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, apb_attention_kernel<D, PAIR>, tq, tk, tv, tg, p);
+    e = cudaLaunchKernelEx(&cfg, apb_attention_kernel<D, PAIR>, La);
   } else {
-    apb_attention_kernel<D, PAIR><<<grid, kThreads, L::kAlloc, stream>>>(tq, tk, tv, tg, p);
+    apb_attention_kernel<D, PAIR><<<grid, kThreads, L::kAlloc, stream>>>(La);
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
@@ -856,17 +862,38 @@ extern "C" int apb_debug_cta_times(unsigned long long* out, int n_ctas) {
 }
 #endif
 
+apb_status launch_attention_hosts(int D, const AttnLaunch& La, int phase, cudaStream_t stream) {
+  if (La.n < 1 || La.n > kAttnMaxHosts) return fail(APB_ERR_CONFIG, "1..8 hosts per attention launch");
+#ifndef APB_PSMEM
+  // clusters pair items 2c and 2c+1: both must belong to the same host and (segment, KV head), i.e.
+  // every host's segments hold an even number of items per KV head (decode_item: per_head =
+  // ceil(units / 2)) — then every host's item range starts at an even index
+  bool even_heads = true;
+  for (int i = 0; i < La.n; ++i) {
+    const AttnParams& p = La.p[i];
+    even_heads = even_heads && (p.n_local_items / p.hk) % 2 == 0 && (p.n_anchor_items / p.hk) % 2 == 0;
+  }
+  if (D == 128 && even_heads && attn::pair_enabled(phase))
+    return attn::launch_impl<128, true>(La, stream);
+#endif
+  if (D == 128) return attn::launch_impl<128, false>(La, stream);
+  if (D == 64) return attn::launch_impl<64, false>(La, stream);
+  return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+}
+
 apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream) {
-#ifndef APB_PSMEM
-  // clusters pair items 2c and 2c+1: both must belong to the same (segment, KV head), i.e. every
-  // segment holds an even number of items per KV head (decode_item: per_head = ceil(units / 2))
-  const bool even_heads = (p.n_local_items / p.hk) % 2 == 0 && (p.n_anchor_items / p.hk) % 2 == 0;
-  if (D == 128 && even_heads && attn::pair_enabled(p.phase)) return attn::launch_impl<128, true>(p, tq, tk, tv, tg, stream);
-#endif
-  if (D == 128) return attn::launch_impl<128, false>(p, tq, tk, tv, tg, stream);
-  if (D == 64) return attn::launch_impl<64, false>(p, tq, tk, tv, tg, stream);
-  return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  static_assert(sizeof(AttnLaunch) <= 32764, "kernel parameter space");
+  AttnLaunch La{};
+  La.n = 1;
+  La.tq[0] = tq;
+  La.tk[0] = tk;
+  La.tv[0] = tv;
+  La.tg = tg;
+  La.p[0] = p;
+  La.item_begin[0] = 0;
+  La.item_begin[1] = p.n_local_items + p.n_anchor_items;
+  return launch_attention_hosts(D, La, p.phase, stream);
 }
 
 }  // namespace apb

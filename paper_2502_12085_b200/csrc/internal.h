@@ -46,6 +46,20 @@ struct AttnParams {
 };
 apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream);
+// Several hosts' attention in ONE launch (the hosts a rank owns, same phase): per-host tensor maps
+// and parameters in the kernel's parameter space (~4.4 KB, CUDA >= 12.1 large kernel parameters);
+// the grid is the concatenation of the hosts' work items, host i's items at
+// [item_begin[i], item_begin[i+1]) in that host's own order.
+constexpr int kAttnMaxHosts = 8;
+struct AttnLaunch {
+  CUtensorMap tq[kAttnMaxHosts], tk[kAttnMaxHosts], tv[kAttnMaxHosts];
+  CUtensorMap tg;  // the gathered passing slots (shared by every host of the launch)
+  AttnParams p[kAttnMaxHosts];
+  int item_begin[kAttnMaxHosts + 1];
+  int n;
+};
+// phase: the launch's phase for the pairing policy (a host without passing keys runs LOCAL as ALL)
+apb_status launch_attention_hosts(int D, const AttnLaunch& L, int phase, cudaStream_t stream);
 
 // ---------------------------------------------------------------- retaining-head scoring
 struct ScoreParams {

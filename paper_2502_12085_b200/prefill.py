@@ -41,7 +41,8 @@ class PrefillRank:
     def __init__(self, base: apb.Dims, hosts: list[int], comm: apb.Comm | None = None,
                  device: torch.device | str = "cuda", skip_unused_last: bool = False,
                  split_phases: bool | None = None, compressor: str = "retain", shared_set: bool = False,
-                 seed: int = 0, same_device: bool = False, peers: "apb.Peers | None" = None):
+                 seed: int = 0, same_device: bool = False, peers: "apb.Peers | None" = None,
+                 batched: bool = False):
         """base: problem dims (its `host` field is ignored); hosts: host indices this rank owns
         (contiguous, in order).  skip_unused_last: do not score/select host H-1 — its
         compressed block is ignored by every host, so outputs are unchanged.
@@ -56,7 +57,12 @@ class PrefillRank:
         peers: an opened apb.Peers — the exchange over peer memory (CUDA IPC) instead of NCCL: the
         compaction pushes every selected row into every rank's buffer (apb_select_topk_peers), the
         PASSING launch waits for its slots on the device, then releases the buffer (two buffers
-        alternate by layer).  Implies the LOCAL / PASSING split."""
+        alternate by layer).  Implies the LOCAL / PASSING split.
+        batched: every attention phase of the owned hosts is ONE launch (apb_attention_fwd_hosts,
+        heaviest host first) instead of one launch per host.  The single-rank schedule then
+        compresses every host first (scoring + selection on the main stream) and runs the whole
+        layer's attention as one launch with the GPU to itself; the split schedule runs one LOCAL
+        and one PASSING launch."""
         if compressor not in ("retain", "random"):
             raise ValueError(f"compressor must be 'retain' or 'random', not {compressor!r}")
         self.compressor, self.shared_set, self.seed = compressor, shared_set, seed
@@ -79,6 +85,7 @@ class PrefillRank:
             raise ValueError(f"hosts {self.hosts} are a strict subset of range(H={base.H}) but there is no "
                              "multi-rank communicator to fill the other hosts' passing slots")
         self.same_device = same_device
+        self.batched = batched
         self.cyclic = nr > 1 and nr < base.H and self.hosts == list(range(self.hosts[0], base.H, nr))
         if nr > 1 and not self.cyclic and self.hosts != list(range(self.hosts[0], self.hosts[0] + len(self.hosts))):
             raise ValueError("owned hosts must be a contiguous block or the cyclic set r, r+N, ...")
@@ -160,6 +167,14 @@ class PrefillRank:
 
     def attention(self, io: dict[int, HostIO], phase: int, stream=None) -> None:
         name = {apb.PHASE_ALL: "attn_all", apb.PHASE_LOCAL: "attn_local", apb.PHASE_PASSING: "attn_passing"}[phase]
+        if self.batched:
+            for c in range(0, len(self.hosts), 8):  # at most 8 hosts per launch
+                hs = self.hosts[c:c + 8]
+                self._op(name, -1, stream, lambda: apb.attention_fwd_hosts(
+                    [self.dims(h) for h in hs], [io[h].q for h in hs], [io[h].k for h in hs], [io[h].v for h in hs],
+                    self.gathered, [io[h].out for h in hs], [io[h].lse for h in hs], phase=phase,
+                    ws=[self.ws[h] for h in hs], stream=stream))
+            return
         for h in self.hosts:
             x = io[h]
             self._op(name, h, stream, lambda: apb.attention_fwd(self.dims(h), x.q, x.k, x.v, self.gathered, x.out,
@@ -181,7 +196,7 @@ class PrefillRank:
             b.record(main)
             events.append((a, b))
 
-        if not overlap:
+        if not overlap or (self.batched and not self.split_phases):
             self.compress(io, weights, main, layer_idx)
             self.exchange(main)
             timed(lambda: self.attention(io, apb.PHASE_ALL, main))

@@ -235,3 +235,33 @@ def test_peers_contract_errors(lib):
     assert lib.apb_peers_wait(None, 1, 1, None) == apb.ERR_CONTRACT
     assert lib.apb_peers_release(None, 1, None) == apb.ERR_CONTRACT
     assert lib.apb_peers_destroy(None) == apb.OK
+
+
+def test_attention_hosts_contract_errors_before_any_gpu_work(lib):
+    """apb_attention_fwd_hosts validates every host before launching (no GPU needed): a repeated
+    host and hosts whose dims differ beyond `host` are APB_ERR_CONFIG, a bad per-host pointer is
+    APB_ERR_CONTRACT, n outside [1, 8] is rejected by the binding."""
+    def qkvo(host, base=0x100000):
+        d = _dims(host=host)
+        r = d.rows
+        return (d, _FakeT(base, (r, 4, 64)), _FakeT(base + 0x10000, (r, 2, 64)), _FakeT(base + 0x20000, (r, 2, 64)),
+                _FakeT(base + 0x30000, (r, 4, 64)))
+    a, b = qkvo(1), qkvo(2, 0x200000)
+    g = _FakeT(0x300000, (4, 2, 2, 64, 64))
+    with pytest.raises(apb.ApbError) as e:   # host 1 twice
+        apb.attention_fwd_hosts([a[0], a[0]], [a[1], a[1]], [a[2], a[2]], [a[3], a[3]], g, [a[4], a[4]], stream=0)
+    assert e.value.status == apb.ERR_CONFIG
+    import dataclasses
+    d2 = dataclasses.replace(b[0], l_a=b[0].l_a + 64)   # anchor length differs
+    r2 = d2.rows
+    with pytest.raises(apb.ApbError) as e:
+        apb.attention_fwd_hosts([a[0], d2], [a[1], _FakeT(0x200000, (r2, 4, 64))],
+                                [a[2], _FakeT(0x210000, (r2, 2, 64))], [a[3], _FakeT(0x220000, (r2, 2, 64))], g,
+                                [a[4], _FakeT(0x230000, (r2, 4, 64))], stream=0)
+    assert e.value.status == apb.ERR_CONFIG
+    with pytest.raises(apb.ApbError) as e:   # host 2's q misaligned
+        apb.attention_fwd_hosts([a[0], b[0]], [a[1], _FakeT(0x200002, b[1].shape)], [a[2], b[2]], [a[3], b[3]], g,
+                                [a[4], b[4]], stream=0)
+    assert e.value.status == apb.ERR_CONTRACT
+    with pytest.raises(apb.ApbError):
+        apb.attention_fwd_hosts([], [], [], [], g, [], stream=0)

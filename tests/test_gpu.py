@@ -267,7 +267,7 @@ def _index_sets_ok(idx_gpu, s_or, lp):
 
 
 @pytest.mark.parametrize("name", ["toy", "d128-sink"])
-@pytest.mark.parametrize("mode", ["ordered", "split", "serial"])
+@pytest.mark.parametrize("mode", ["ordered", "split", "serial", "batched", "split-batched"])
 def test_prefill_layer_end_to_end(name, mode):
     """All four steps through PrefillRank, every host of the layer emulated on one GPU, in the
     three schedules: ordered one-pass (single rank), LOCAL/PASSING split around the exchange
@@ -277,7 +277,8 @@ def test_prefill_layer_end_to_end(name, mode):
     cfg = CASES[name].replace(d_hidden=1024)
     hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
     w = synth.retain_weights(cfg, 0)
-    rank = PrefillRank(dims_of(cfg, 0), list(range(cfg.H)), split_phases=(mode == "split"))
+    rank = PrefillRank(dims_of(cfg, 0), list(range(cfg.H)), split_phases=mode.startswith("split"),
+                       batched=mode.endswith("batched"))
     io = {}
     for h in range(cfg.H):
         q = dev(hosts[h]["q"])
@@ -328,6 +329,65 @@ def test_attention_paired_matches_single_cta(name, phase, monkeypatch):
         monkeypatch.setenv("APB_ATTN_PAIR", "0")
         b = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
         assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True), f"host {h}"
+
+
+def run_attention_hosts(cfg, hs, xs, gathered_bits, phase):
+    """apb_attention_fwd_hosts over hosts hs (one launch per phase); returns {h: (O, lse)}."""
+    from paper_2502_12085_b200 import apb
+    ds = [dims_of(cfg, h) for h in hs]
+    q = [dev(xs[h]["q"]) for h in hs]
+    k = [dev(xs[h]["k"]) for h in hs]
+    v = [dev(xs[h]["v"]) for h in hs]
+    out = [torch.full_like(x, float("nan")) for x in q]
+    lse = [torch.full((cfg.hq, d.rows), float("nan"), device="cuda") for d in ds]
+    ws = [torch.empty(max(apb.workspace_size(d, apb.WS_ATTENTION), 16), dtype=torch.uint8, device="cuda") for d in ds]
+    g = dev(gathered_bits) if gathered_bits is not None else None
+    if phase == "split":
+        apb.attention_fwd_hosts(ds, q, k, v, None, out, lse, phase=apb.PHASE_LOCAL, ws=ws)
+        apb.attention_fwd_hosts(ds, q, k, v, g, out, lse, phase=apb.PHASE_PASSING, ws=ws)
+    else:
+        apb.attention_fwd_hosts(ds, q, k, v, g, out, lse, phase=apb.PHASE_ALL, ws=ws)
+    torch.cuda.synchronize()
+    return {h: (out[i].float().cpu().double().numpy(), lse[i].cpu().double().numpy().T) for i, h in enumerate(hs)}
+
+
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa8-d128", "mha", "d128-sink", "lq"])
+@pytest.mark.parametrize("phase", ["all", "split"])
+@pytest.mark.parametrize("pair", ["", "0"])
+def test_attention_hosts_equals_per_host(name, phase, pair, monkeypatch):
+    """apb_attention_fwd_hosts (one launch over several hosts' items, heaviest host first) is
+    bit-identical to one apb_attention_fwd call per host — every host, a strict subset in a
+    scrambled order (a rank owning cyclic hosts), with and without the paired kernel."""
+    monkeypatch.setenv("APB_ATTN_PAIR", pair)
+    cfg = CASES[name]
+    hosts, ref = oracle_layer(cfg)
+    subsets = [list(range(cfg.H)), list(range(cfg.H - 1, -1, -2))]
+    for hs in subsets:
+        got = run_attention_hosts(cfg, hs, hosts, ref["gathered"], phase)
+        for h in hs:
+            a = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
+            b = got[h]
+            assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True), (hs, h)
+
+
+def test_attention_hosts_contract():
+    """Mismatched dims across the hosts of one launch and a repeated host are APB_ERR_CONFIG."""
+    from paper_2502_12085_b200 import apb
+    cfg = CASES["toy"]
+    hosts, ref = oracle_layer(cfg)
+    ds = [dims_of(cfg, 1), dims_of(cfg, 1)]
+    q = [dev(hosts[1]["q"])] * 2
+    k = [dev(hosts[1]["k"])] * 2
+    v = [dev(hosts[1]["v"])] * 2
+    out = [torch.empty_like(q[0])] * 2
+    with pytest.raises(apb.ApbError) as e:
+        apb.attention_fwd_hosts(ds, q, k, v, dev(ref["gathered"]), out)
+    assert e.value.status == apb.ERR_CONFIG
+    import dataclasses
+    ds = [dims_of(cfg, 1), dataclasses.replace(dims_of(cfg, 2), l_p=cfg.l_p + 1)]
+    with pytest.raises(apb.ApbError) as e:
+        apb.attention_fwd_hosts(ds, q, k, v, dev(ref["gathered"]), out)
+    assert e.value.status == apb.ERR_CONFIG
 
 
 # ----------------------------------------------------------------------------- full size

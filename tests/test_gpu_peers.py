@@ -44,7 +44,7 @@ def _dev(bits):
     return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
 
 
-def _worker(rank, world, port, layout, q):
+def _worker(rank, world, port, layout, q, batched=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -59,7 +59,7 @@ def _worker(rank, world, port, layout, q):
     dist.all_gather_object(handles, peers.handle)
     peers.open(handles)
     mine = hosts_of_rank(cfg.H, world, rank, layout)
-    pr = PrefillRank(base, mine, peers=peers)
+    pr = PrefillRank(base, mine, peers=peers, batched=batched)
     results = []
     for layer in range(LAYERS):
         io = {}
@@ -83,15 +83,15 @@ def _worker(rank, world, port, layout, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", ["block", "cyclic"])
-def test_peer_exchange_two_ranks_one_gpu(layout):
+@pytest.mark.parametrize("layout,batched", [("block", False), ("cyclic", False), ("cyclic", True)])
+def test_peer_exchange_two_ranks_one_gpu(layout, batched):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, q, batched)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(world))
