@@ -517,14 +517,15 @@ def op_breakdown(pr, step, cfg, H, hosts, layers, world, peaks, barrier):
         e = out.setdefault(name, {"ms_per_step": 0.0, "launches": 0, "lower_bound_ms": 0.0})
         e["ms_per_step"] += a.elapsed_time(b)
         e["launches"] += 1
+        hs = h if isinstance(h, list) else [h]  # a list: one batched launch over those hosts
         if name == "score":
-            e["lower_bound_ms"] += score_flops / tf * 1e3
+            e["lower_bound_ms"] += len(hs) * score_flops / tf * 1e3
         elif name == "select_compact":
-            e["lower_bound_ms"] += sel_bytes / hbm * 1e3
+            e["lower_bound_ms"] += len(hs) * sel_bytes / hbm * 1e3
         elif name == "exchange":
             e["lower_bound_ms"] += recv / (NVLINK_GBS * 1e9) * 1e3
-        else:  # one host, or (h = -1) one batched launch over every owned host
-            for hh in (hosts if h < 0 else [h]):
+        else:
+            for hh in hs:
                 f_all = workload.attention_flops(cfg.n, H, hh, cfg.l_a, cfg.l_p, cfg.hq, cfg.d, cfg.l_q)
                 f_pass = 4 * cfg.d * cfg.hq * l_b * hh * lpp
                 f = {"attn_all": f_all, "attn_local": f_all - f_pass, "attn_passing": f_pass}[name]

@@ -114,6 +114,16 @@ apb_status apb_retain_score(const apb_dims* dims, const apb_retain_weights* w,
                             int64_t q_row_stride, int64_t kv_row_stride,
                             float* scores, void* ws, size_t ws_bytes, apb_stream_t stream);
 apb_status apb_retain_workspace_size(const apb_dims* dims, const apb_retain_weights* w, size_t* bytes);
+/* The scoring of n (1..8) hosts of one rank in ONE GEMM launch (plus one finalize launch) — the
+ * same scores, bit for bit, as n apb_retain_score calls with the CTA-pair GEMM (Alg. apb_prefill
+ * line "retain", runs on every host; a rank owning several hosts runs them all).
+ *  dims[i]  host i's dims (every field equal across entries except `host`, else APB_ERR_CONFIG)
+ *  q/k/v/scores: HOST arrays of n per-host device pointers as in apb_retain_score; strides shared
+ *  ws       n x apb_retain_workspace_size() bytes (host i's partials at i x that size), required */
+apb_status apb_retain_score_hosts(int32_t n, const apb_dims* dims, const apb_retain_weights* w,
+                                  const void* const* q, const void* const* k, const void* const* v,
+                                  int64_t q_row_stride, int64_t kv_row_stride, float* const* scores,
+                                  void* ws, size_t ws_bytes, apb_stream_t stream);
 
 /* ---------------------------------------------------------------- step 2: select + compact
  * For each KV head j: idx[j] = the l_p' block indices with the largest scores[j][.]
@@ -125,6 +135,13 @@ apb_status apb_select_topk(const apb_dims* dims, const float* scores,
                            const void* k, const void* v, int64_t kv_row_stride,
                            int32_t* indices, void* send, void* ws, size_t ws_bytes,
                            apb_stream_t stream);
+/* The selection + compaction of n (1..8) hosts of one rank in one select launch and one gather
+ * launch (l_b <= 32K; above, one launch per host) — bit-identical to n apb_select_topk calls.
+ *  dims[i]  host i's dims (every field equal across entries except `host`, else APB_ERR_CONFIG)
+ *  scores/k/v/indices/send: HOST arrays of n per-host device pointers as in apb_select_topk */
+apb_status apb_select_topk_hosts(int32_t n, const apb_dims* dims, const float* const* scores,
+                                 const void* const* k, const void* const* v, int64_t kv_row_stride,
+                                 int32_t* const* indices, void* const* send, apb_stream_t stream);
 
 /* ---------------------------------------------------------------- method variants (NEXT #3)
  * Compressor and selection variants of the ablation lattice (Table 4).

@@ -35,7 +35,8 @@ EXPORTED = ("apb_retain_score", "apb_select_topk", "apb_exchange_passing", "apb_
             "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check", "apb_comm_abort",
             "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size",
             "apb_peers_create", "apb_peers_open", "apb_peers_gathered", "apb_select_topk_peers", "apb_peers_wait",
-            "apb_peers_release", "apb_peers_destroy", "apb_attention_fwd_hosts")
+            "apb_peers_release", "apb_peers_destroy", "apb_attention_fwd_hosts", "apb_retain_score_hosts",
+            "apb_select_topk_hosts")
 
 
 class ApbError(RuntimeError):
@@ -85,6 +86,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     dp = ctypes.POINTER(_Dims)
     lib.apb_retain_score.argtypes = [dp, ctypes.POINTER(_Weights), vp, vp, vp, i64, i64, vp, vp, sz, vp]
     lib.apb_select_topk.argtypes = [dp, vp, vp, vp, i64, vp, vp, vp, sz, vp]
+    lib.apb_retain_score_hosts.argtypes = [i32, dp, ctypes.POINTER(_Weights), vp, vp, vp, i64, i64, vp, vp, sz, vp]
+    lib.apb_select_topk_hosts.argtypes = [i32, dp, vp, vp, vp, i64, vp, vp, vp]
     lib.apb_exchange_passing.argtypes = [vp, dp, vp, vp]
     lib.apb_exchange_passing_cyclic.argtypes = [vp, dp, vp, vp]
     lib.apb_attention_fwd.argtypes = [dp, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.c_int, vp, sz, vp]
@@ -129,7 +132,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
               "apb_exchange_passing_cyclic", "apb_decode_step_hosts", "apb_exchange_plan", "apb_comm_check",
               "apb_comm_abort", "apb_exchange_partials_cyclic", "apb_gemm", "apb_retain_workspace_size",
               "apb_peers_create", "apb_peers_open", "apb_peers_gathered", "apb_select_topk_peers", "apb_peers_wait",
-              "apb_peers_release", "apb_peers_destroy", "apb_attention_fwd_hosts"):
+              "apb_peers_release", "apb_peers_destroy", "apb_attention_fwd_hosts", "apb_retain_score_hosts",
+            "apb_select_topk_hosts"):
         getattr(lib, f).restype = ctypes.c_int
     lib.apb_status_string.argtypes = [ctypes.c_int]
     lib.apb_status_string.restype = ctypes.c_char_p
@@ -328,6 +332,64 @@ def select_topk(dims: Dims, scores, k, v, indices, send, stream=None) -> None:
     _check(load().apb_select_topk(ctypes.byref(d), scores.data_ptr(), k.data_ptr(), v.data_ptr(),
                                   _rowstride(k, "k"), indices.data_ptr(), send.data_ptr(), None, 0,
                                   _stream(stream)), "apb_select_topk")
+
+
+def _ptrs(xs):
+    return (ctypes.c_void_p * len(xs))(*[_ptr(x) for x in xs])
+
+
+def _same_problem(dims: list[Dims]) -> None:
+    if not 1 <= len(dims) <= 8:
+        raise ApbError(ERR_CONTRACT, "hosts", "1..8 hosts per launch")
+
+
+def retain_score_hosts(dims: list[Dims], w: RetainWeights, q: list, k: list, v: list, scores: list, ws,
+                       stream=None) -> None:
+    """apb_retain_score_hosts: the scoring of several hosts (dims[i].host) in one GEMM launch;
+    ws: len(dims) x retain_workspace_size bytes."""
+    _same_problem(dims)
+    n = len(dims)
+    if not len(q) == len(k) == len(v) == len(scores) == n:
+        raise ApbError(ERR_CONTRACT, "hosts", "one q/k/v/scores per host")
+    for i in range(n):
+        _check_qkv(dims[i], q[i], k[i], v[i])
+        _need_numel(scores[i], "scores", torch.float32, dims[i].n_kv_heads * dims[i].l_b)
+        if _rowstride(q[i], "q") != _rowstride(q[0], "q") or _rowstride(k[i], "k") != _rowstride(k[0], "k"):
+            raise ApbError(ERR_CONTRACT, "hosts", "the hosts' q / kv row strides must be equal")
+    _need(w.w1, "w1", torch.bfloat16, dense=True)
+    _need(w.w2, "w2", torch.float32, dense=True)
+    for b, nm in ((w.b1, "b1"), (w.b2, "b2")):
+        if b is not None:
+            _need(b, nm, torch.float32, dense=True)
+    if w.w2.dim() != 2 or w.w2.shape[1] != w.w1.shape[0]:
+        raise ApbError(ERR_CONTRACT, "w2", "must be [n_out][d_hidden]")
+    _need(ws, "ws", ws.dtype, dense=True)
+    cd = (_Dims * n)(*[d.c() for d in dims])
+    wc = w.c()
+    _check(load().apb_retain_score_hosts(n, cd, ctypes.byref(wc), _ptrs(q), _ptrs(k), _ptrs(v), _rowstride(q[0], "q"),
+                                         _rowstride(k[0], "k"), _ptrs(scores), _ptr(ws), ws.numel() * ws.element_size(),
+                                         _stream(stream)), "apb_retain_score_hosts")
+
+
+def select_topk_hosts(dims: list[Dims], scores: list, k: list, v: list, indices: list, send: list,
+                      stream=None) -> None:
+    """apb_select_topk_hosts: several hosts' selection + compaction in one launch pair."""
+    _same_problem(dims)
+    n = len(dims)
+    if not len(scores) == len(k) == len(v) == len(indices) == len(send) == n:
+        raise ApbError(ERR_CONTRACT, "hosts", "one scores/k/v/indices/send per host")
+    for i, d in enumerate(dims):
+        _need_numel(scores[i], "scores", torch.float32, d.n_kv_heads * d.l_b)
+        if d.l_pp > 0:
+            _need(k[i], "k", torch.bfloat16, d.rows, d.n_kv_heads * d.head_dim)
+            _need(v[i], "v", torch.bfloat16, d.rows, d.n_kv_heads * d.head_dim)
+            if _rowstride(k[i], "k") != _rowstride(v[i], "v") or _rowstride(k[i], "k") != _rowstride(k[0], "k"):
+                raise ApbError(ERR_CONTRACT, "k/v", "K and V of every host must share one row stride")
+            _need_numel(indices[i], "indices", torch.int32, d.n_kv_heads * d.l_pp)
+            _need_numel(send[i], "send", torch.bfloat16, 2 * d.n_kv_heads * d.l_pp * d.head_dim)
+    cd = (_Dims * n)(*[d.c() for d in dims])
+    _check(load().apb_select_topk_hosts(n, cd, _ptrs(scores), _ptrs(k), _ptrs(v), _rowstride(k[0], "k"),
+                                        _ptrs(indices), _ptrs(send), _stream(stream)), "apb_select_topk_hosts")
 
 
 def random_scores(dims: Dims, seed: int, layer: int, scores, stream=None) -> None:

@@ -410,6 +410,69 @@ extern "C" apb_status apb_retain_score(const apb_dims* d, const apb_retain_weigh
   return launch_retain_score(p, tq, tk, tv, tw, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" apb_status apb_retain_score_hosts(int32_t n, const apb_dims* dims, const apb_retain_weights* w,
+                                             const void* const* q, const void* const* k, const void* const* v,
+                                             int64_t q_row_stride, int64_t kv_row_stride, float* const* scores,
+                                             void* ws, size_t ws_bytes, apb_stream_t stream) {
+  if (n < 1 || n > 8) return fail(APB_ERR_CONFIG, "n must be in [1, 8]");
+  if (!dims || !q || !k || !v || !scores) return fail(APB_ERR_CONTRACT, "dims/q/k/v/scores array is NULL");
+  apb_status st;
+  for (int i = 0; i < n; ++i) {
+    const apb_dims& a = dims[i];
+    const apb_dims& b = dims[0];
+    if ((st = check_dims(&a))) return st;
+    if (a.n != b.n || a.H != b.H || a.l_q != b.l_q || a.l_a != b.l_a || a.l_p != b.l_p || a.n_heads != b.n_heads ||
+        a.n_kv_heads != b.n_kv_heads || a.head_dim != b.head_dim)
+      return fail(APB_ERR_CONFIG, "the hosts of one launch must share every dimension but `host`");
+  }
+  const apb_dims* d = &dims[0];
+  if ((st = check_retain_weights(d, w))) return st;
+  const int D = d->head_dim, hq = d->n_heads, hk = d->n_kv_heads;
+  if (!w->w1 || !aligned16(w->w1) || !w->w2) return fail(APB_ERR_CONTRACT, "w1/w2 NULL or misaligned");
+  const size_t per = retain_ws_bytes(d, w);
+  if (!ws || ws_bytes < per * (size_t)n || !aligned16(ws))
+    return fail(APB_ERR_CONTRACT, "workspace missing, misaligned or smaller than n x apb_retain_workspace_size");
+  CUtensorMap tq[8], tk[8], tv[8];
+  int L_A[8];
+  uint32_t box[2] = {64, 128};
+  for (int i = 0; i < n; ++i) {
+    if ((st = check_rows(q[i], q_row_stride, (int64_t)hq * D, "q"))) return st;
+    if ((st = check_rows(k[i], kv_row_stride, (int64_t)hk * D, "k"))) return st;
+    if ((st = check_rows(v[i], kv_row_stride, (int64_t)hk * D, "v"))) return st;
+    if (!scores[i] || (reinterpret_cast<uintptr_t>(scores[i]) & 15))
+      return fail(APB_ERR_CONTRACT, "scores NULL or misaligned");
+    L_A[i] = (int)L_A_of(&dims[i]);
+    const int64_t rows = L_A[i] + d->l_b;
+    uint64_t qd[2] = {(uint64_t)hq * D, (uint64_t)rows}, qs[1] = {(uint64_t)q_row_stride * 2};
+    uint64_t kd[2] = {(uint64_t)hk * D, (uint64_t)rows}, ks[1] = {(uint64_t)kv_row_stride * 2};
+    if (!make_tmap_bf16(&tq[i], q[i], 2, qd, qs, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&tk[i], k[i], 2, kd, ks, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&tv[i], v[i], 2, kd, ks, box)) return APB_ERR_CUDA;
+  }
+  if ((st = check_device())) return st;
+  ScoreParams p{};
+  p.l_b = d->l_b;
+  p.hq = hq;
+  p.hk = hk;
+  p.D = D;
+  p.d_in = w->d_in;
+  p.d_hidden = w->d_hidden;
+  p.n_out = w->n_out;
+  p.kq = hq * D / 64;
+  p.kk = hk * D / 64;
+  p.b1 = w->b1;
+  p.w2 = w->w2;
+  p.b2 = w->b2;
+  CUtensorMap tw, twh;
+  uint64_t wd[2] = {(uint64_t)w->d_in, (uint64_t)w->d_hidden};
+  uint64_t ws_[1] = {(uint64_t)w->d_in * 2};
+  uint32_t wbox[2] = {64, (uint32_t)score_tile_n() / 2}, whbox[2] = {64, (uint32_t)score_tile_n() / 4};
+  if (!make_tmap_bf16(&tw, w->w1, 2, wd, ws_, wbox)) return APB_ERR_CUDA;
+  if (!make_tmap_bf16(&twh, w->w1, 2, wd, ws_, whbox)) return APB_ERR_CUDA;
+  return launch_score_gemm_hosts(p, n, tq, tk, tv, L_A, scores, tw, twh, static_cast<float*>(ws),
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
 // ---------------------------------------------------------------- step 2: select + compact
 extern "C" apb_status apb_select_topk(const apb_dims* d, const float* scores, const void* k, const void* v,
                                       int64_t kv_row_stride, int32_t* indices, void* send, void* ws, size_t ws_bytes,
@@ -428,6 +491,40 @@ extern "C" apb_status apb_select_topk(const apb_dims* d, const float* scores, co
   if ((st = check_device())) return st;
   return launch_select_compact(d->l_b, (int)lpp, hk, D, (int)L_A_of(d), scores, k, v, kv_row_stride, indices, send,
                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+
+extern "C" apb_status apb_select_topk_hosts(int32_t n, const apb_dims* dims, const float* const* scores,
+                                            const void* const* k, const void* const* v, int64_t kv_row_stride,
+                                            int32_t* const* indices, void* const* send, apb_stream_t stream) {
+  if (n < 1 || n > kSelMaxHosts) return fail(APB_ERR_CONFIG, "n must be in [1, 8]");
+  if (!dims || !scores || !k || !v || !indices || !send) return fail(APB_ERR_CONTRACT, "an array argument is NULL");
+  apb_status st;
+  const apb_dims* d = &dims[0];
+  const int D = d->head_dim, hk = d->n_kv_heads;
+  SelHosts sh{};
+  sh.n = n;
+  for (int i = 0; i < n; ++i) {
+    const apb_dims& a = dims[i];
+    if ((st = check_dims(&a))) return st;
+    if (a.n != d->n || a.H != d->H || a.l_q != d->l_q || a.l_a != d->l_a || a.l_p != d->l_p ||
+        a.n_heads != d->n_heads || a.n_kv_heads != hk || a.head_dim != D)
+      return fail(APB_ERR_CONFIG, "the hosts of one launch must share every dimension but `host`");
+    if (!scores[i] || !indices[i]) return fail(APB_ERR_CONTRACT, "scores/indices NULL");
+    if ((st = check_rows(k[i], kv_row_stride, (int64_t)hk * D, "k"))) return st;
+    if ((st = check_rows(v[i], kv_row_stride, (int64_t)hk * D, "v"))) return st;
+    if (!send[i] || !aligned16(send[i])) return fail(APB_ERR_CONTRACT, "send NULL or misaligned");
+    sh.scores[i] = scores[i];
+    sh.indices[i] = indices[i];
+    sh.k[i] = static_cast<const uint16_t*>(k[i]);
+    sh.v[i] = static_cast<const uint16_t*>(v[i]);
+    sh.send[i] = static_cast<uint16_t*>(send[i]);
+    sh.L_A[i] = (int)L_A_of(&a);
+  }
+  const int64_t lpp = lpp_of(d);
+  if (lpp == 0) return APB_OK;
+  if ((st = check_device())) return st;
+  return launch_select_compact_hosts(d->l_b, (int)lpp, hk, D, sh, kv_row_stride, reinterpret_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------- method variants (NEXT #3)

@@ -62,6 +62,14 @@ struct Cfg {
 };
 constexpr double kL2Budget = 48.0 * (1 << 20);  // bytes of a raster group's resident operand rows
 constexpr int kEpiScore = 100;                  // internal epilogue: retaining-head partial scores
+constexpr int kGemmMaxHosts = 8;
+
+// Tensor maps of one launch (kernel parameter space): A per host as up to three maps, W, C and
+// the quarter-tile W map of the half-tile tail.
+struct Maps {
+  CUtensorMap a[kGemmMaxHosts][3];
+  CUtensorMap w, c, wh;
+};
 
 struct Params {
   int64_t M;
@@ -79,8 +87,13 @@ struct Params {
   int hint_w, hint_c;   // L2 policies: W loads evict_last, C stores evict_first (APB_GEMM_HINTS)
   int raster_n, group;  // raster: groups of `group` M-tiles (N fastest... see tile_coords) or N-tiles
   // A from up to three row-aligned maps ([Q | K | V] for the retaining head): K blocks [0, kq) from
-  // map 0, [kq, kqk) from map 1, the rest from map 2; A's row coordinate is a_row0 + row
-  int kq, kqk, a_row0;
+  // map 0, [kq, kqk) from map 1, the rest from map 2; A's row coordinate is a_row0[host] + row.
+  // n_hosts > 1 (scoring only): the same M x N problem for several hosts in one launch, tile
+  // T -> host T / tiles_per_host (its own A maps, a_row0 and partial slots part + host * part_stride)
+  int kq, kqk;
+  int n_hosts, tiles_per_host;
+  int a_row0[kGemmMaxHosts];
+  int64_t part_stride;
   // SCORE: partial[nb][row][n_out] = W2[:, nb*256 .. +256] SiLU(acc + b1[...])  (fp32)
   const float* b1;
   const float* w2;
@@ -106,15 +119,18 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int
 // Work item -> tile (+ half: -1 = the whole BN-wide tile, 0 / 1 = its left / right BN/2 columns).
 // The tiles of a final partial wave are split in two halves (launch_params), so that wave is
 // half as long: 256 scoring tiles on 74 pairs run in 3.5 instead of 4 tile-times.
-__device__ __forceinline__ void item_coords(const Params& p, int item, int& mb, int& nb, int& half) {
+__device__ __forceinline__ void item_coords(const Params& p, int item, int& host, int& mb, int& nb, int& half) {
+  int T;
   if (item < p.n_full) {
-    tile_coords(p, item, mb, nb);
+    T = item;
     half = -1;
   } else {
     const int r = item - p.n_full;
-    tile_coords(p, p.n_full + r / 2, mb, nb);
+    T = p.n_full + r / 2;
     half = r & 1;
   }
+  host = T / p.tiles_per_host;
+  tile_coords(p, T - host * p.tiles_per_host, mb, nb);
 }
 
 __device__ __forceinline__ float bf16_round(float x) {
@@ -138,10 +154,10 @@ __device__ __forceinline__ void load32(const uint16_t* src, float (&v)[32], int 
 
 template <int BN_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a1,
-                const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_w,
-                const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_wh,
-                const Params p) {
+    gemm_kernel(const __grid_constant__ Maps tm, const Params p) {
+  const CUtensorMap* tm_w = &tm.w;
+  const CUtensorMap* tm_c = &tm.c;
+  const CUtensorMap* tm_wh = &tm.wh;
   using C = Cfg<BN_>;
   constexpr int BN = C::BN, STAGES = C::STAGES, kBBytes = C::kBBytes, kStageBytes = C::kStageBytes;
   constexpr int kOffBar = C::kOffBar, kOffTmem = C::kOffTmem, kOffInv = C::kOffInv, kOffStage = C::kOffStage;
@@ -186,9 +202,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint64_t pol_last = policy_evict_last();
     int it = 0;
     for (int t = pair; t < p.n_items; t += npairs) {
-      int mb, nb, half;
-      item_coords(p, t, mb, nb, half);
-      const int arow = p.a_row0 + mb * 2 * BM + rank * BM;
+      int host, mb, nb, half;
+      item_coords(p, t, host, mb, nb, half);
+      const int arow = p.a_row0[host] + mb * 2 * BM + rank * BM;
+      const CUtensorMap* tma = tm.a[host];
       const int wrow = half < 0 ? nb * BN + rank * (BN / 2) : nb * BN + half * (BN / 2) + rank * (BN / 4);
       const uint32_t stage_tx = half < 0 ? 2 * kStageBytes : 2 * (kABytes + kBBytes / 2);
       for (int kb = 0; kb < p.nkb; ++kb, ++it) {
@@ -198,17 +215,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (rank == 0) mbar_arrive_expect_tx(bFull(s), stage_tx);
           const uint32_t st = sbase + s * kStageBytes;
           if (kb < p.kq)
-            tma_load_2d_pair(st, &tm_a, full_leader0 + 8u * s, kb * BK, arow);
+            tma_load_2d_pair(st, &tma[0], full_leader0 + 8u * s, kb * BK, arow);
           else if (kb < p.kqk)
-            tma_load_2d_pair(st, &tm_a1, full_leader0 + 8u * s, (kb - p.kq) * BK, arow);
+            tma_load_2d_pair(st, &tma[1], full_leader0 + 8u * s, (kb - p.kq) * BK, arow);
           else
-            tma_load_2d_pair(st, &tm_a2, full_leader0 + 8u * s, (kb - p.kqk) * BK, arow);
+            tma_load_2d_pair(st, &tma[2], full_leader0 + 8u * s, (kb - p.kqk) * BK, arow);
           if (half >= 0)  // this CTA's quarter of the W tile (BN/4 rows) for a half-tile item
-            tma_load_2d_pair(st + kABytes, &tm_wh, full_leader0 + 8u * s, kb * BK, wrow);
+            tma_load_2d_pair(st + kABytes, tm_wh, full_leader0 + 8u * s, kb * BK, wrow);
           else if (p.hint_w)  // the operand the raster keeps resident in L2 for the whole group
-            tma_load_2d_pair_hint(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow, pol_last);
+            tma_load_2d_pair_hint(st + kABytes, tm_w, full_leader0 + 8u * s, kb * BK, wrow, pol_last);
           else
-            tma_load_2d_pair(st + kABytes, &tm_w, full_leader0 + 8u * s, kb * BK, wrow);
+            tma_load_2d_pair(st + kABytes, tm_w, full_leader0 + 8u * s, kb * BK, wrow);
         }
         __syncwarp();
       }
@@ -269,16 +286,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (r == 0) {
         // output lines are not re-read by this kernel: first candidates for eviction, so the
         // operand rows the raster keeps resident stay in L2
-        if (p.hint_c) tma_store_2d_hint(&tm_c, sstage + buf * kStageOut, col, row0, pol_first);
-        else tma_store_2d(&tm_c, sstage + buf * kStageOut, col, row0);
+        if (p.hint_c) tma_store_2d_hint(tm_c, sstage + buf * kStageOut, col, row0, pol_first);
+        else tma_store_2d(tm_c, sstage + buf * kStageOut, col, row0);
         bulk_commit_group();
       }
       ++chunk_ctr;
     };
     int tl = 0;
     for (int t = pair; t < p.n_items; t += npairs, ++tl) {
-      int mb, nb, half;
-      item_coords(p, t, mb, nb, half);
+      int host, mb, nb, half;
+      item_coords(p, t, host, mb, nb, half);
       const int b = tl & 1;
       const int64_t row = (int64_t)mb * 2 * BM + rank * BM + r;
       const bool row_ok = row < p.M;
@@ -345,8 +362,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
           if (row_ok) {
-            float* dst = p.part + ((int64_t)slot * p.M + row) * p.n_out + og;
-            float* dst2 = p.part + ((int64_t)(slot + 1) * p.M + row) * p.n_out + og;
+            float* part = p.part + host * p.part_stride;
+            float* dst = part + ((int64_t)slot * p.M + row) * p.n_out + og;
+            float* dst2 = part + ((int64_t)(slot + 1) * p.M + row) * p.n_out + og;
 #pragma unroll
             for (int oc = 0; oc < 32; ++oc)
               if (oc < no) {
@@ -442,14 +460,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 template <int BN>
-static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtensorMap& ta1, const CUtensorMap& ta2,
-                                const CUtensorMap& tw, const CUtensorMap& tc, const CUtensorMap* twh, bool score,
-                                cudaStream_t stream) {
+static apb_status launch_params(Params& p, Maps& m, bool halves, bool score, cudaStream_t stream) {
   using C = Cfg<BN>;
   const int smem = score ? C::kSmemScore : C::kSmem;
+  if (p.n_hosts < 1) p.n_hosts = 1;
   p.num_m = (int)((p.M + 2 * BM - 1) / (2 * BM));
   p.num_n = (p.N + BN - 1) / BN;
-  p.num_tiles = p.num_m * p.num_n;
+  p.tiles_per_host = p.num_m * p.num_n;
+  p.num_tiles = p.tiles_per_host * p.n_hosts;
   p.nkb = (p.K + BK - 1) / BK;
   {
     // estimated DRAM bytes: row groups read A once and W once per group; column groups the reverse
@@ -482,13 +500,14 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
   p.n_items = p.n_full = p.num_tiles;
   const int tail = p.num_tiles % npairs;
   const char* split_env = std::getenv("APB_GEMM_TAIL_SPLIT");  // timing experiments: "0" disables
-  if (twh && tail > 0 && 2 * tail <= npairs && p.num_tiles > npairs && !(split_env && split_env[0] == '0')) {
+  if (halves && tail > 0 && 2 * tail <= npairs && p.num_tiles > npairs && !(split_env && split_env[0] == '0')) {
     // a partial last wave: its tiles run as half tiles (twice as many, half as long)
     p.n_full = p.num_tiles - tail;
     p.n_items = p.n_full + 2 * tail;
   }
   const int pairs = std::min(p.n_items, npairs);
-  gemm_kernel<BN><<<2 * pairs, kThreads, smem, stream>>>(ta0, ta1, ta2, tw, tc, twh ? *twh : tw, p);
+  if (!halves) m.wh = m.w;  // never dereferenced
+  gemm_kernel<BN><<<2 * pairs, kThreads, smem, stream>>>(m, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   count_launch();
@@ -498,11 +517,16 @@ static apb_status launch_params(Params& p, const CUtensorMap& ta0, const CUtenso
 // score_finalize_kernel: o[oc] = b2[oc] + sum_nb part[nb][t][oc] (nb order), s[j][t] = max over the
 // r = n_out / hk outputs of KV head j (reading G4).  One thread per block token; a token's n_out
 // partials are contiguous, read as float4 when n_out % 4 == 0 (every paper config).
-__global__ void __launch_bounds__(128) score_finalize_kernel(const float* __restrict__ part, int l_b, int n_parts,
-                                                             int n_out, int hk, const float* __restrict__ b2,
-                                                             float* __restrict__ scores) {
+struct ScoreOut {
+  float* s[kGemmMaxHosts];  // per host: [hk][l_b]
+};
+__global__ void __launch_bounds__(128) score_finalize_kernel(const float* __restrict__ part_all, int64_t part_stride,
+                                                             int l_b, int n_parts, int n_out, int hk,
+                                                             const float* __restrict__ b2, const __grid_constant__ ScoreOut so) {
   const int t = blockIdx.x * 128 + threadIdx.x;
   if (t >= l_b) return;
+  const float* part = part_all + blockIdx.y * part_stride;  // grid.y = host of the launch
+  float* scores = so.s[blockIdx.y];
   const int rr = n_out / hk;
   float m = -INFINITY;
   auto emit = [&](int oc, float o) {  // outputs arrive in oc order
@@ -540,18 +564,19 @@ __global__ void __launch_bounds__(128) score_finalize_kernel(const float* __rest
 
 apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   using namespace gemm;
-  CUtensorMap ta, tw;
+  Maps m;
   {
     uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.M};
     uint64_t str[1] = {(uint64_t)g.lda * 2};
     uint32_t box[2] = {BK, BM};
-    if (!make_tmap_bf16(&ta, g.a, 2, dims, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&m.a[0][0], g.a, 2, dims, str, box)) return APB_ERR_CUDA;
+    m.a[0][1] = m.a[0][2] = m.a[0][0];
   }
   {
     uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.N};
     uint64_t str[1] = {(uint64_t)g.ldw * 2};
     uint32_t box[2] = {BK, 128};  // this CTA's half of a 256-column W tile
-    if (!make_tmap_bf16(&tw, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&m.w, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
   }
   Params p{};
   p.M = g.M;
@@ -569,23 +594,22 @@ apb_status launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   p.kq = p.kqk = (g.K + BK - 1) / BK;
   // STORE / RESIDUAL can run the tiles of a partial last wave as half tiles (SWIGLU's tile holds
   // gate and up halves, ROPE's whole heads: they keep whole tiles)
-  CUtensorMap twh;
   const bool halves = g.epi == APB_EPI_STORE || g.epi == APB_EPI_RESIDUAL;
   if (halves) {
     uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.N};
     uint64_t str[1] = {(uint64_t)g.ldw * 2};
     uint32_t box[2] = {BK, 64};
-    if (!make_tmap_bf16(&twh, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&m.wh, g.w, 2, dims, str, box)) return APB_ERR_CUDA;
   }
-  CUtensorMap tc;
   {
     const uint64_t ncols = g.epi == APB_EPI_SWIGLU ? (uint64_t)g.N / 2 : (uint64_t)g.N;
     uint64_t dims[2] = {ncols, (uint64_t)g.M};
     uint64_t str[1] = {(uint64_t)g.ldc * 2};
     uint32_t box[2] = {32, BM};
-    if (!make_tmap_bf16(&tc, g.c, 2, dims, str, box, 64)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&m.c, g.c, 2, dims, str, box, 64)) return APB_ERR_CUDA;
   }
-  return launch_params<256>(p, ta, ta, ta, tw, tc, halves ? &twh : nullptr, false, stream);
+  p.n_hosts = 1;
+  return launch_params<256>(p, m, halves, false, stream);
 }
 
 // Hidden-unit tile of the scoring GEMM: 256 (default) or 128 (APB_SCORE_BN=128).  Measured on the
@@ -599,10 +623,11 @@ int score_tile_n() {
   return bn;
 }
 
-apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, const CUtensorMap& tw1, const CUtensorMap& tw1h, float* part,
-                             cudaStream_t stream) {
+apb_status launch_score_gemm_hosts(const ScoreParams& sp, int n, const CUtensorMap* tq, const CUtensorMap* tk,
+                                   const CUtensorMap* tv, const int* L_A, float* const* scores, const CUtensorMap& tw1,
+                                   const CUtensorMap& tw1h, float* part, cudaStream_t stream) {
   using namespace gemm;
+  if (n < 1 || n > kGemmMaxHosts) return fail(APB_ERR_CONFIG, "1..8 hosts per scoring launch");
   Params p{};
   p.M = sp.l_b;
   p.N = sp.d_hidden;
@@ -610,23 +635,43 @@ apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const
   p.epi = kEpiScore;
   p.kq = sp.kq;
   p.kqk = sp.kq + sp.kk;
-  p.a_row0 = sp.L_A;
+  p.n_hosts = n;
+  Maps m;
+  for (int i = 0; i < n; ++i) {
+    p.a_row0[i] = L_A[i];
+    m.a[i][0] = tq[i];
+    m.a[i][1] = tk[i];
+    m.a[i][2] = tv[i];
+  }
+  m.w = tw1;
+  m.c = tw1;  // no tile stores
+  m.wh = tw1h;
   p.b1 = sp.b1;
   p.w2 = sp.w2;
   p.n_out = sp.n_out;
   p.d_hidden = sp.d_hidden;
   p.part = part;
   const int bn = score_tile_n();
-  apb_status st = bn == 128 ? launch_params<128>(p, tq, tk, tv, tw1, tw1 /* no tile stores */, &tw1h, true, stream)
-                            : launch_params<256>(p, tq, tk, tv, tw1, tw1, &tw1h, true, stream);
-  if (st) return st;
   const int n_parts = (sp.d_hidden + bn / 2 - 1) / (bn / 2);  // one partial slot per bn/2 hidden units
-  score_finalize_kernel<<<(sp.l_b + 127) / 128, 128, 0, stream>>>(part, sp.l_b, n_parts, sp.n_out, sp.hk, sp.b2,
-                                                                   sp.scores);
+  p.part_stride = (int64_t)n_parts * sp.l_b * sp.n_out;       // one host's partial slots
+  apb_status st = bn == 128 ? launch_params<128>(p, m, true, true, stream) : launch_params<256>(p, m, true, true, stream);
+  if (st) return st;
+  ScoreOut so{};
+  for (int i = 0; i < n; ++i) so.s[i] = scores[i];
+  score_finalize_kernel<<<dim3((sp.l_b + 127) / 128, n), 128, 0, stream>>>(part, p.part_stride, sp.l_b, n_parts,
+                                                                          sp.n_out, sp.hk, sp.b2, so);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("score_finalize launch: ") + cudaGetErrorString(e));
   count_launch();
   return APB_OK;
+}
+
+apb_status launch_score_gemm(const ScoreParams& sp, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const CUtensorMap& tw1, const CUtensorMap& tw1h, float* part,
+                             cudaStream_t stream) {
+  float* scores[1] = {sp.scores};
+  const int L_A[1] = {sp.L_A};
+  return launch_score_gemm_hosts(sp, 1, &tq, &tk, &tv, L_A, scores, tw1, tw1h, part, stream);
 }
 
 }  // namespace apb

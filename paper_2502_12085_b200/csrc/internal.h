@@ -79,6 +79,12 @@ int score_tile_n();  // hidden units per scoring GEMM tile (128 or 256)
 apb_status launch_score_gemm(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, const CUtensorMap& tw1, const CUtensorMap& tw1h, float* part,
                              cudaStream_t stream);
+// n (1..8) hosts' scoring in one GEMM launch + one finalize launch: host i's [Q|K|V] maps tq/tk/tv[i],
+// anchor rows L_A[i], scores[i]; `part` holds n consecutive per-host partial areas (the retain
+// workspace of one host, n times).  p's L_A and scores fields are ignored.
+apb_status launch_score_gemm_hosts(const ScoreParams& p, int n, const CUtensorMap* tq, const CUtensorMap* tk,
+                                   const CUtensorMap* tv, const int* L_A, float* const* scores, const CUtensorMap& tw1,
+                                   const CUtensorMap& tw1h, float* part, cudaStream_t stream);
 
 // ---------------------------------------------------------------- selection + compaction
 apb_status launch_rmsnorm(int64_t rows, int dim, const void* x, int64_t xs, const void* w, float eps, void* y,
@@ -116,6 +122,20 @@ struct GatherDst {
   uint32_t* counter;          // CTA-completion counter (this rank's device memory)
   int32_t epoch;
 };
+// Several hosts' selection + compaction in one select launch and one gather launch (same l_b, l_p,
+// hk; per-host pointers and anchor lengths).  l_b > 32K: one launch pair per host.
+constexpr int kSelMaxHosts = 8;
+struct SelHosts {
+  int n;
+  const float* scores[kSelMaxHosts];
+  int32_t* indices[kSelMaxHosts];
+  const uint16_t* k[kSelMaxHosts];
+  const uint16_t* v[kSelMaxHosts];
+  uint16_t* send[kSelMaxHosts];
+  int L_A[kSelMaxHosts];
+};
+apb_status launch_select_compact_hosts(int l_b, int lp, int hk, int D, const SelHosts& sh, int64_t kv_row_stride,
+                                       cudaStream_t stream);
 apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const float* scores,
                                  const void* k, const void* v, int64_t kv_row_stride, int32_t* indices,
                                  void* send, cudaStream_t stream, const GatherDst* push = nullptr);

@@ -348,8 +348,9 @@ constexpr int kCandReg = 4096;  // candidate list capacity (else digits 2-3 scan
 constexpr int kOutStage = 4096; // staged output indices (else written straight to global)
 
 template <int KPT>
-__global__ void __launch_bounds__(kFT) select_reg_kernel(const float* __restrict__ scores, int l_b, int lp,
-                                                         int32_t* __restrict__ indices) {
+__global__ void __launch_bounds__(kFT) select_reg_kernel(const __grid_constant__ SelHosts sh, int l_b, int lp) {
+  const float* __restrict__ scores = sh.scores[blockIdx.y];  // grid.y = host of the launch
+  int32_t* __restrict__ indices = sh.indices[blockIdx.y];
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t wtot[64];
   __shared__ uint32_t cand[kCandReg];  // candidate keys; reused as the staged output indices
@@ -457,14 +458,18 @@ __global__ void __launch_bounds__(kFT) select_reg_kernel(const float* __restrict
 // compaction — and the launch's last CTA then publishes `epoch` in every rank's flag word for this
 // slot (release at system scope, after every CTA's stores were fenced at system scope).
 template <int D>
-__global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ k,
-                                                     const uint16_t* __restrict__ v, int64_t kv_row_stride, int L_A,
-                                                     int lp, int hk, const GatherDst dst) {
+__global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ SelHosts sh, int64_t kv_row_stride,
+                                                     int lp, int hk, const __grid_constant__ GatherDst dst) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the select grid's indices are visible
+  const int host = blockIdx.z >> 1;                   // grid.z = 2 x hosts of the launch
+  const int32_t* __restrict__ idx = sh.indices[host];
+  const uint16_t* __restrict__ k = sh.k[host];
+  const uint16_t* __restrict__ v = sh.v[host];
+  const int L_A = sh.L_A[host];
   constexpr int kVec = D / 8;                         // 16-byte vectors per row
   constexpr int kBatch = 8;
   constexpr int kRows = 256 * kBatch / kVec;          // rows per CTA
-  const int j = blockIdx.y, kv = blockIdx.z;
+  const int j = blockIdx.y, kv = blockIdx.z & 1;
   const int r0 = blockIdx.x * kRows;
   const uint16_t* src = (kv ? v : k) + (int64_t)j * D;
   const int64_t off = (((int64_t)kv * hk + j) * lp) * D;  // elements into a slot
@@ -478,8 +483,10 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
     if (r < lp)
       buf[q] = __ldg(reinterpret_cast<const uint4*>(src + (L_A + (int64_t)__ldg(idx + (int64_t)j * lp + r)) * kv_row_stride) + c);
   }
-  for (int d = 0; d < dst.n; ++d) {
-    uint4* out = reinterpret_cast<uint4*>(dst.send[d] + off);
+  // destinations: the push list (one host, peer exchange) or this host's own slot
+  const int nd = dst.n > 0 ? dst.n : 1;
+  for (int d = 0; d < nd; ++d) {
+    uint4* out = reinterpret_cast<uint4*>((dst.n > 0 ? dst.send[d] : sh.send[host]) + off);
 #pragma unroll
     for (int q = 0; q < kBatch; ++q)
       if (rr[q] >= 0) out[(int64_t)rr[q] * kVec + (q * 256 + threadIdx.x) % kVec] = buf[q];
@@ -760,11 +767,11 @@ static apb_status launch_fast(const float* scores, int l_b, int lp, int hk, int3
 }
 
 template <int D>
-static cudaError_t launch_gather(const int32_t* idx, const void* k, const void* v, int64_t kv_row_stride, int L_A,
-                                 int lp, int hk, const GatherDst& dst, cudaStream_t stream) {
+static cudaError_t launch_gather(const SelHosts& sh, int64_t kv_row_stride, int lp, int hk, const GatherDst& dst,
+                                 cudaStream_t stream) {
   constexpr int kRows = 256 * 8 / (D / 8);
   cudaLaunchConfig_t c = {};
-  c.gridDim = dim3((lp + kRows - 1) / kRows, hk, 2);
+  c.gridDim = dim3((lp + kRows - 1) / kRows, hk, 2 * sh.n);
   c.blockDim = dim3(256);
   c.stream = stream;
   cudaLaunchAttribute attr;
@@ -772,8 +779,7 @@ static cudaError_t launch_gather(const int32_t* idx, const void* k, const void* 
   attr.val.programmaticStreamSerializationAllowed = 1;
   c.attrs = &attr;
   c.numAttrs = 1;
-  return cudaLaunchKernelEx(&c, gather_kernel<D>, idx, static_cast<const uint16_t*>(k),
-                            static_cast<const uint16_t*>(v), kv_row_stride, L_A, lp, hk, dst);
+  return cudaLaunchKernelEx(&c, gather_kernel<D>, sh, kv_row_stride, lp, hk, dst);
 }
 
 }  // namespace sel
@@ -805,10 +811,18 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
   }
   if (push || !(env && env[0] == 'l')) {
     apb_status st = APB_OK;
+    SelHosts sh{};
+    sh.n = 1;
+    sh.scores[0] = scores;
+    sh.indices[0] = indices;
+    sh.k[0] = static_cast<const uint16_t*>(k);
+    sh.v[0] = static_cast<const uint16_t*>(v);
+    sh.send[0] = static_cast<uint16_t*>(send);
+    sh.L_A[0] = L_A;
     if (l_b <= 16 * sel::kFT)
-      sel::select_reg_kernel<16><<<hk, sel::kFT, 0, stream>>>(scores, l_b, lp, indices);
+      sel::select_reg_kernel<16><<<hk, sel::kFT, 0, stream>>>(sh, l_b, lp);
     else if (l_b <= 32 * sel::kFT)
-      sel::select_reg_kernel<32><<<hk, sel::kFT, 0, stream>>>(scores, l_b, lp, indices);
+      sel::select_reg_kernel<32><<<hk, sel::kFT, 0, stream>>>(sh, l_b, lp);
     else
       st = l_b <= sel::kMaxSmemKeys ? sel::launch_fast<true>(scores, l_b, lp, hk, indices, stream)
                                     : sel::launch_fast<false>(scores, l_b, lp, hk, indices, stream);
@@ -820,8 +834,10 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
       count_launch(1);
       return APB_OK;
     }
-    e = D == 128 ? sel::launch_gather<128>(indices, k, v, kv_row_stride, L_A, lp, hk, dst, stream)
-                 : sel::launch_gather<64>(indices, k, v, kv_row_stride, L_A, lp, hk, dst, stream);
+    const GatherDst none{};  // n = 0: each host's own slot sh.send[host]
+    const GatherDst& gd = push ? *push : none;
+    e = D == 128 ? sel::launch_gather<128>(sh, kv_row_stride, lp, hk, gd, stream)
+                 : sel::launch_gather<64>(sh, kv_row_stride, lp, hk, gd, stream);
     if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gather launch: ") + cudaGetErrorString(e));
     count_launch(2);
     return APB_OK;
@@ -843,6 +859,33 @@ apb_status launch_select_compact(int l_b, int lp, int hk, int D, int L_A, const 
                                                        static_cast<uint16_t*>(send));
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("compact launch: ") + cudaGetErrorString(e));
+  count_launch(2);
+  return APB_OK;
+}
+
+apb_status launch_select_compact_hosts(int l_b, int lp, int hk, int D, const SelHosts& sh, int64_t kv_row_stride,
+                                       cudaStream_t stream) {
+  const char* env = std::getenv("APB_SELECT");
+  if (sh.n < 1 || sh.n > kSelMaxHosts) return fail(APB_ERR_CONFIG, "1..8 hosts per select launch");
+  if (l_b > 32 * sel::kFT || (env && env[0] == 'l') || (D != 128 && D != 64)) {
+    for (int i = 0; i < sh.n; ++i) {  // one launch (pair) per host
+      apb_status st = launch_select_compact(l_b, lp, hk, D, sh.L_A[i], sh.scores[i], sh.k[i], sh.v[i], kv_row_stride,
+                                            sh.indices[i], sh.send[i], stream);
+      if (st) return st;
+    }
+    return APB_OK;
+  }
+  // every host's KV heads in one select launch (grid hk x n) and one PDL gather launch
+  if (l_b <= 16 * sel::kFT)
+    sel::select_reg_kernel<16><<<dim3(hk, sh.n), sel::kFT, 0, stream>>>(sh, l_b, lp);
+  else
+    sel::select_reg_kernel<32><<<dim3(hk, sh.n), sel::kFT, 0, stream>>>(sh, l_b, lp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("select launch: ") + cudaGetErrorString(e));
+  const GatherDst none{};
+  e = D == 128 ? sel::launch_gather<128>(sh, kv_row_stride, lp, hk, none, stream)
+               : sel::launch_gather<64>(sh, kv_row_stride, lp, hk, none, stream);
+  if (e != cudaSuccess) return fail(APB_ERR_CUDA, std::string("gather launch: ") + cudaGetErrorString(e));
   count_launch(2);
   return APB_OK;
 }

@@ -59,7 +59,8 @@ class PrefillRank:
         PASSING launch waits for its slots on the device, then releases the buffer (two buffers
         alternate by layer).  Implies the LOCAL / PASSING split.
         batched: every attention phase of the owned hosts is ONE launch (apb_attention_fwd_hosts,
-        heaviest host first) instead of one launch per host.  The single-rank schedule then
+        heaviest host first) instead of one launch per host, and so are their scoring
+        (apb_retain_score_hosts) and selection (apb_select_topk_hosts).  The single-rank schedule then
         compresses every host first (scoring + selection on the main stream) and runs the whole
         layer's attention as one launch with the GPU to itself; the split schedule runs one LOCAL
         and one PASSING launch."""
@@ -115,7 +116,8 @@ class PrefillRank:
     def dims(self, h: int) -> apb.Dims:
         return self.base.with_host(h)
 
-    def _op(self, name: str, h: int, stream, fn) -> None:
+    def _op(self, name: str, h, stream, fn) -> None:
+        """h: the host of the op, a list of hosts (one batched launch) or -1 (all / none)."""
         if self.trace is None:
             return fn()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -152,10 +154,25 @@ class PrefillRank:
 
     def compress(self, io: dict[int, HostIO], weights: apb.RetainWeights | None, stream=None,
                  layer_idx: int = 0) -> None:
-        """Steps 1-2 for every owned host."""
-        for h in self.hosts:
-            if self._compresses(h):
+        """Steps 1-2 for every owned host (batched: one scoring launch and one select launch pair
+        for up to 8 hosts at a time)."""
+        hs_all = [h for h in self.hosts if self._compresses(h)]
+        if not self.batched or self.peers is not None or self.compressor != "retain" or self.shared_set:
+            for h in hs_all:
                 self._compress_host(h, io, weights, layer_idx, stream)
+            return
+        for c in range(0, len(hs_all), 8):
+            hs = hs_all[c:c + 8]
+            ds = [self.dims(h) for h in hs]
+            n = apb.retain_workspace_size(ds[0], weights) * len(hs)
+            if self.score_ws.get("batch") is None or self.score_ws["batch"].numel() < n:
+                self.score_ws["batch"] = torch.empty(max(n, 16), dtype=torch.uint8, device=self.device)
+            self._op("score", hs, stream, lambda: apb.retain_score_hosts(
+                ds, weights, [io[h].q for h in hs], [io[h].k for h in hs], [io[h].v for h in hs],
+                [self.scores[h] for h in hs], self.score_ws["batch"], stream=stream))
+            self._op("select_compact", hs, stream, lambda: apb.select_topk_hosts(
+                ds, [self.scores[h] for h in hs], [io[h].k for h in hs], [io[h].v for h in hs],
+                [self.indices[h] for h in hs], [self.gathered[h] for h in hs], stream=stream))
 
     def exchange(self, stream=None) -> None:
         """Step 3: in-place AllGather(s) of the packed [2][hk][l_p'][d] slots (with peers the
@@ -170,7 +187,7 @@ class PrefillRank:
         if self.batched:
             for c in range(0, len(self.hosts), 8):  # at most 8 hosts per launch
                 hs = self.hosts[c:c + 8]
-                self._op(name, -1, stream, lambda: apb.attention_fwd_hosts(
+                self._op(name, hs, stream, lambda: apb.attention_fwd_hosts(
                     [self.dims(h) for h in hs], [io[h].q for h in hs], [io[h].k for h in hs], [io[h].v for h in hs],
                     self.gathered, [io[h].out for h in hs], [io[h].lse for h in hs], phase=phase,
                     ws=[self.ws[h] for h in hs], stream=stream))

@@ -265,3 +265,34 @@ def test_attention_hosts_contract_errors_before_any_gpu_work(lib):
     assert e.value.status == apb.ERR_CONTRACT
     with pytest.raises(apb.ApbError):
         apb.attention_fwd_hosts([], [], [], [], g, [], stream=0)
+
+
+def test_compress_hosts_contract_errors_before_any_gpu_work(lib):
+    """apb_retain_score_hosts / apb_select_topk_hosts: hosts with different dims, a workspace
+    smaller than n x apb_retain_workspace_size, and NULL arrays are rejected without a GPU."""
+    import dataclasses
+    d1, d2 = _dims(host=1), _dims(host=2)
+    r = d1.rows
+    q = [_FakeT(0x100000, (r, 4, 64)), _FakeT(0x200000, (r, 4, 64))]
+    k = [_FakeT(0x110000, (r, 2, 64)), _FakeT(0x210000, (r, 2, 64))]
+    v = [_FakeT(0x120000, (r, 2, 64)), _FakeT(0x220000, (r, 2, 64))]
+    sc = [_FakeT(0x130000, (2, d1.l_b), 4), _FakeT(0x230000, (2, d1.l_b), 4)]
+    w = apb.RetainWeights(w1=_FakeT(0x50000, (256, 8 * 64)), w2=_FakeT(0x60000, (4, 256), 4))
+    per = apb.retain_workspace_size(d1, w)
+    small = _FakeT(0x400000, (per,), 1, dtype=torch.uint8)
+    with pytest.raises(apb.ApbError) as e:   # workspace for one host only
+        apb.retain_score_hosts([d1, d2], w, q, k, v, sc, small, stream=0)
+    assert e.value.status == apb.ERR_CONTRACT
+    big = _FakeT(0x400000, (2 * per,), 1, dtype=torch.uint8)
+    d2x = dataclasses.replace(d2, l_p=d2.l_p + 8)
+    with pytest.raises(apb.ApbError) as e:
+        apb.retain_score_hosts([d1, d2x], w, q, k, v, sc, big, stream=0)
+    assert e.value.status == apb.ERR_CONFIG
+    idx = [_FakeT(0x500000, (2, d1.l_pp), 4, dtype=torch.int32), _FakeT(0x510000, (2, d1.l_pp), 4, dtype=torch.int32)]
+    send = [_FakeT(0x600000, (2, 2, d1.l_pp, 64)), _FakeT(0x700000, (2, 2, d1.l_pp, 64))]
+    with pytest.raises(apb.ApbError) as e:   # n_heads differs (nothing the binding sizes by)
+        apb.select_topk_hosts([d1, dataclasses.replace(d2, n_heads=6)], sc, k, v, idx, send, stream=0)
+    assert e.value.status == apb.ERR_CONFIG
+    with pytest.raises(apb.ApbError) as e:   # host 2's send misaligned
+        apb.select_topk_hosts([d1, d2], sc, k, v, idx, [send[0], _FakeT(0x700008, (2, 2, d1.l_pp, 64))], stream=0)
+    assert e.value.status == apb.ERR_CONTRACT

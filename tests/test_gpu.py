@@ -196,6 +196,57 @@ def test_retain_score_plans_bit_identical(plan, monkeypatch):
     assert np.array_equal(out[0], out[1])
 
 
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3", "yi-heads"])
+@pytest.mark.parametrize("tail", ["", "0"])
+def test_retain_score_hosts_equals_per_host(name, tail, monkeypatch):
+    """apb_retain_score_hosts (every host's tiles in one CTA-pair GEMM launch: tile T of host
+    T / tiles_per_host, the partial last wave split into half tiles across hosts; one finalize
+    launch) gives the per-host apb_retain_score scores bit for bit — each tile and each partial
+    slot is computed in the same fixed order whichever launch it belongs to."""
+    from paper_2502_12085_b200 import apb
+    monkeypatch.setenv("APB_GEMM_TAIL_SPLIT", tail)
+    cfg = (CASES[name] if name in CASES else
+           synth.Config("yi-heads", 20, n=1400, H=2, l_a=64, l_p=100, hq=56, hk=8, d=64)).replace(d_hidden=1024)
+    w = weights_dev(synth.retain_weights(cfg, 0, n_out=cfg.hq))
+    xs = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    for hs in (list(range(cfg.H)), list(range(cfg.H - 1, -1, -2))):
+        ds = [dims_of(cfg, h) for h in hs]
+        q = [dev(xs[h]["q"]) for h in hs]
+        k = [dev(xs[h]["k"]) for h in hs]
+        v = [dev(xs[h]["v"]) for h in hs]
+        sc = [torch.full((cfg.hk, cfg.l_b), float("nan"), device="cuda") for _ in hs]
+        ws = torch.empty(apb.retain_workspace_size(ds[0], w) * len(hs), dtype=torch.uint8, device="cuda")
+        apb.retain_score_hosts(ds, w, q, k, v, sc, ws)
+        for i, h in enumerate(hs):
+            ref = torch.empty((cfg.hk, cfg.l_b), device="cuda")
+            apb.retain_score(ds[i], w, q[i], k[i], v[i], ref)
+            torch.cuda.synchronize()
+            assert torch.equal(sc[i], ref), (hs, h)
+
+
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3"])
+def test_select_topk_hosts_equals_per_host(name):
+    """apb_select_topk_hosts (one select launch over every host's KV heads, one gather launch)
+    gives the per-host indices and send slots bit for bit."""
+    from paper_2502_12085_b200 import apb
+    cfg = CASES[name]
+    xs = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    sc = [torch.from_numpy(np.ascontiguousarray(synth.random_scores(cfg, 0, h, ties=True), dtype=np.float32)).cuda()
+          for h in range(cfg.H)]
+    hs = list(range(cfg.H))
+    ds = [dims_of(cfg, h) for h in hs]
+    k = [dev(xs[h]["k"]) for h in hs]
+    v = [dev(xs[h]["v"]) for h in hs]
+    idx = [torch.full((cfg.hk, cfg.l_pp), -1, dtype=torch.int32, device="cuda") for _ in hs]
+    send = [torch.zeros((2, cfg.hk, cfg.l_pp, cfg.d), dtype=torch.bfloat16, device="cuda") for _ in hs]
+    apb.select_topk_hosts(ds, sc, k, v, idx, send)
+    torch.cuda.synchronize()
+    for h in hs:
+        idx_or = oracle.select_all_heads(sc[h].cpu().double().numpy(), cfg.l_p)
+        assert np.array_equal(idx[h].cpu().numpy(), idx_or), h
+        assert np.array_equal(to_bits(send[h]), oracle.compact(xs[h]["k"], xs[h]["v"], xs[h]["L_A"], idx_or)), h
+
+
 def _select_gpu(cfg, h, x, scores_np):
     from paper_2502_12085_b200 import apb
     s = torch.from_numpy(np.ascontiguousarray(scores_np, dtype=np.float32)).cuda()
