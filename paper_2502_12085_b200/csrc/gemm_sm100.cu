@@ -85,6 +85,7 @@ struct Params {
   int num_m, num_n, num_tiles, nkb;
   int n_items, n_full;  // work items; items >= n_full are half tiles (BN/2 columns, the tail wave)
   int hint_w, hint_c;   // L2 policies: W loads evict_last, C stores evict_first (APB_GEMM_HINTS)
+  int dbg;              // timing experiments only (APB_SCORE_DBG): 1 = SCORE epilogue skips the W2 products
   int raster_n, group;  // raster: groups of `group` M-tiles (N fastest... see tile_coords) or N-tiles
   // A from up to three row-aligned maps ([Q | K | V] for the retaining head): K blocks [0, kq) from
   // map 0, [kq, kqk) from map 1, the rest from map 2; A's row coordinate is a_row0[host] + row.
@@ -332,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int oc = 0; oc < 32; ++oc) o[oc] = 0.f;
 #pragma unroll 1
-          for (int c = 0; c < bne; c += 32) {
+          for (int c = 0; c < (p.dbg == 1 ? 0 : bne); c += 32) {
             uint32_t zr[32];
             tmem_ld32(tacc + c, zr);
             tmem_wait_ld();
@@ -490,6 +491,7 @@ static apb_status launch_params(Params& p, Maps& m, bool halves, bool score, cud
     p.hint_w = hs.find('w') != std::string::npos;
     p.hint_c = hs.find('c') != std::string::npos;
   }
+  if (const char* dbg = std::getenv("APB_SCORE_DBG")) p.dbg = std::atoi(dbg);
   static std::atomic<uint64_t> smem_set{0};
   if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(gemm_kernel<BN>), C::kSmemScore, smem_set))
     return st;
