@@ -167,8 +167,10 @@ extern "C" apb_status apb_workspace_size(const apb_dims* d, apb_ws_kind which, s
 // apb_attention_fwd_hosts).  *skip: nothing to compute (PASSING without passing keys).
 static apb_status attention_setup(const apb_dims* d, const void* q, const void* k, const void* v, int64_t q_row_stride,
                                   int64_t kv_row_stride, const void* gathered, void* out, int64_t out_row_stride,
-                                  float* lse, apb_phase phase, void* ws, size_t ws_bytes, AttnParams& p,
-                                  CUtensorMap& tq, CUtensorMap& tk, CUtensorMap& tv, CUtensorMap& tg, bool* skip) {
+                                  float* lse, apb_phase phase, void* ws, size_t ws_bytes, AttnLaunch& La, int slot,
+                                  CUtensorMap& tg, bool* skip) {
+  AttnParams& p = La.p[slot];
+  CUtensorMap &tq = La.tq[slot], &tk = La.tk[slot], &tv = La.tv[slot];
   *skip = false;
   apb_status st = check_dims(d);
   if (st) return st;
@@ -243,6 +245,16 @@ static apb_status attention_setup(const apb_dims* d, const void* q, const void* 
     if (!make_tmap_bf16(&tk, k, 3, dims, str, box)) return APB_ERR_CUDA;
     if (!make_tmap_bf16(&tv, v, 3, dims, str, box)) return APB_ERR_CUDA;
   }
+  {
+    // the bf16 output, anchor rows and block rows as separate maps (TMA stores clip at each end)
+    uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)out_row_stride * 2};
+    uint32_t box[3] = {64, 1, 128};
+    uint64_t da[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)(L_A > 0 ? L_A : 1)};
+    uint64_t db[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)d->l_b};
+    if (!make_tmap_bf16(&La.to_a[slot], out, 3, da, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&La.to_b[slot], static_cast<char*>(out) + L_A * out_row_stride * 2, 3, db, str, box))
+      return APB_ERR_CUDA;
+  }
   if (p.n_slots > 0 && phase != APB_PHASE_LOCAL) {
     uint64_t dims[4] = {(uint64_t)D, (uint64_t)lpp, (uint64_t)hk, (uint64_t)2 * d->H};
     uint64_t str[3] = {(uint64_t)D * 2, (uint64_t)lpp * D * 2, (uint64_t)hk * lpp * D * 2};
@@ -258,15 +270,17 @@ extern "C" apb_status apb_attention_fwd(const apb_dims* d, const void* q, const 
                                         int64_t q_row_stride, int64_t kv_row_stride, const void* gathered, void* out,
                                         int64_t out_row_stride, float* lse, apb_phase phase, void* ws, size_t ws_bytes,
                                         apb_stream_t stream) {
-  AttnParams p;
-  CUtensorMap tq, tk, tv, tg;
+  AttnLaunch La{};
   bool skip = false;
   apb_status st = attention_setup(d, q, k, v, q_row_stride, kv_row_stride, gathered, out, out_row_stride, lse, phase,
-                                  ws, ws_bytes, p, tq, tk, tv, tg, &skip);
+                                  ws, ws_bytes, La, 0, La.tg, &skip);
   if (st) return st;
   if ((st = check_device())) return st;
   if (skip) return APB_OK;
-  return launch_attention(d->head_dim, p, tq, tk, tv, tg, reinterpret_cast<cudaStream_t>(stream));
+  La.n = 1;
+  La.item_begin[0] = 0;
+  La.item_begin[1] = La.p[0].n_local_items + La.p[0].n_anchor_items;
+  return launch_attention_hosts(d->head_dim, La, (int)phase, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" apb_status apb_attention_fwd_hosts(int32_t n, const apb_dims* dims, const void* const* q,
@@ -300,8 +314,7 @@ extern "C" apb_status apb_attention_fwd_hosts(int32_t n, const apb_dims* dims, c
     bool skip = false;
     apb_status st = attention_setup(&dims[i], q[i], k[i], v[i], q_row_stride, kv_row_stride, gathered, out[i],
                                     out_row_stride, lse ? lse[i] : nullptr, phase, ws ? ws[i] : nullptr,
-                                    ws_bytes ? ws_bytes[i] : 0, La.p[La.n], La.tq[La.n], La.tk[La.n], La.tv[La.n], tg,
-                                    &skip);
+                                    ws_bytes ? ws_bytes[i] : 0, La, La.n, tg, &skip);
     if (st) return st;
     if (skip) continue;
     if (La.p[La.n].n_slots > 0 && phase != APB_PHASE_LOCAL) {

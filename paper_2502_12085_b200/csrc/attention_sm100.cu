@@ -90,8 +90,9 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
 __device__ unsigned long long g_trace[64 * 32];
 __device__ int g_trace_block = 0;
 #define TRACE(slot, i) do { if (blockIdx.x == g_trace_block && (i) < 64) g_trace[(i) * 32 + (slot)] = clock64(); } while (0)
-// per-CTA timeline of the last launch: [start globaltimer ns, end ns, smid] for blockIdx < 65536
-__device__ unsigned long long g_cta_time[3 * 65536];
+// per-CTA timeline of the last launch: [start globaltimer ns, end ns, smid, first S MMA issued ns,
+// O final (last PV complete) ns] for blockIdx < 65536
+__device__ unsigned long long g_cta_time[5 * 65536];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -99,9 +100,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define CTA_TIME(k) do { if (threadIdx.x == 0 && blockIdx.x < 65536) { \
     unsigned int sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); \
-    g_cta_time[3 * blockIdx.x + (k)] = gtimer(); g_cta_time[3 * blockIdx.x + 2] = sm; } } while (0)
+    g_cta_time[5 * blockIdx.x + (k)] = gtimer(); g_cta_time[5 * blockIdx.x + 2] = sm; } } while (0)
+#define CTA_STAMP(k) do { if (blockIdx.x < 65536) g_cta_time[5 * blockIdx.x + (k)] = gtimer(); } while (0)
 #else
 #define CTA_TIME(k) do {} while (0)
+#define CTA_STAMP(k) do {} while (0)
 #define TRACE(slot, i) do {} while (0)
 #endif
 
@@ -493,6 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i == 0) {
           mbar_wait_sleep(bRf(nK % NR), (nK / NR) & 1);
           tc_fence_after();
+          if (elect_one()) CTA_STAMP(3);
+          __syncwarp();
           for (int t = 0; t < it.ntiles; ++t) {
             TRACE(t, 0);
             issue_S(t, nK % NR);
@@ -750,9 +755,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bO(t), 0);
 #endif
       tc_fence_after();
+      if (tid == 0 && t == 0) CTA_STAMP(4);
       const float inv_l = 1.f / l_run;
       const bool to_ws = (it.seg == 1) && p.local_to_ws;
       const int64_t grow_idx = (it.seg == 0 ? 0 : p.L_A) + row;  // row of q/out on this host
+#ifndef APB_PSMEM
+      if (!to_ws) {
+        // bf16 O tile -> shared memory (SW128, the Q tile layout) -> TMA store(s) by one thread.
+        // The staging slot (2 nkv + t) mod kRing of the K/V ring is idle: its last load is at least
+        // kRing - 2 loads older than the final V, so every MMA reading it has completed (the tile's
+        // last PV did), and the peer of a pair no longer multicasts into it.  Rows past the
+        // segment's end are clipped by the output map (anchor and block rows are separate maps).
+        const uint32_t stg = sR((2 * it.nkv + t) % NR);
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int e = q4 * 8, chunk = (c & 1) * 4 + q4;
+            const uint32_t a = stg + (c >> 1) * L::kSub + tid * 128 + ((chunk ^ (tid & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                         "r"(pack_bf16x2(__uint_as_float(r[e]) * inv_l, __uint_as_float(r[e + 1]) * inv_l)),
+                         "r"(pack_bf16x2(__uint_as_float(r[e + 2]) * inv_l, __uint_as_float(r[e + 3]) * inv_l)),
+                         "r"(pack_bf16x2(__uint_as_float(r[e + 4]) * inv_l, __uint_as_float(r[e + 5]) * inv_l)),
+                         "r"(pack_bf16x2(__uint_as_float(r[e + 6]) * inv_l, __uint_as_float(r[e + 7]) * inv_l))
+                         : "memory");
+          }
+        }
+        fence_proxy_async_smem();  // the generic-proxy writes are visible to the TMA engine
+        named_bar_sync(3 + t, 128);
+        if (tid == 0) {
+          const CUtensorMap* to = it.seg == 0 ? &La.to_a[hh] : &La.to_b[hh];
+#pragma unroll
+          for (int h = 0; h < L::kHalves; ++h) tma_store_3d(to, stg + h * L::kSub, h * 64, qh, it.rtt[t] * BM);
+          bulk_commit_group();
+          bulk_wait_group_read<0>();  // shared memory may be released (the CTA exits after this)
+        }
+      } else
+#endif
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t r[32];
@@ -857,12 +899,13 @@ extern "C" int apb_debug_trace(unsigned long long* out, int n, int block) {
   return cudaMemcpyFromSymbol(out, attn::g_trace, sizeof(unsigned long long) * (n < 2048 ? n : 2048)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int apb_debug_cta_times(unsigned long long* out, int n_ctas) {
-  const int n = 3 * (n_ctas < 65536 ? n_ctas : 65536);
+  const int n = 5 * (n_ctas < 65536 ? n_ctas : 65536);
   return cudaMemcpyFromSymbol(out, attn::g_cta_time, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
 }
 #endif
 
 apb_status launch_attention_hosts(int D, const AttnLaunch& La, int phase, cudaStream_t stream) {
+  static_assert(sizeof(AttnLaunch) <= 32764, "kernel parameter space");
   if (La.n < 1 || La.n > kAttnMaxHosts) return fail(APB_ERR_CONFIG, "1..8 hosts per attention launch");
 #ifndef APB_PSMEM
   // clusters pair items 2c and 2c+1: both must belong to the same host and (segment, KV head), i.e.
@@ -879,21 +922,6 @@ apb_status launch_attention_hosts(int D, const AttnLaunch& La, int phase, cudaSt
   if (D == 128) return attn::launch_impl<128, false>(La, stream);
   if (D == 64) return attn::launch_impl<64, false>(La, stream);
   return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
-}
-
-apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                            const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream) {
-  static_assert(sizeof(AttnLaunch) <= 32764, "kernel parameter space");
-  AttnLaunch La{};
-  La.n = 1;
-  La.tq[0] = tq;
-  La.tk[0] = tk;
-  La.tv[0] = tv;
-  La.tg = tg;
-  La.p[0] = p;
-  La.item_begin[0] = 0;
-  La.item_begin[1] = p.n_local_items + p.n_anchor_items;
-  return launch_attention_hosts(D, La, p.phase, stream);
 }
 
 }  // namespace apb

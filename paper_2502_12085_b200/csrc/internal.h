@@ -44,8 +44,6 @@ struct AttnParams {
   float* ws_lse;              // [hq][l_b] fp32, log2 domain
   int dbg_skip;               // debug-only (env APB_DEBUG_SKIP): bit0 skip K loads, bit1 skip V loads, bit2 skip softmax (timing experiments)
 };
-apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                            const CUtensorMap& tv, const CUtensorMap& tg, cudaStream_t stream);
 // Several hosts' attention in ONE launch (the hosts a rank owns, same phase): per-host tensor maps
 // and parameters in the kernel's parameter space (~4.4 KB, CUDA >= 12.1 large kernel parameters);
 // the grid is the concatenation of the hosts' work items, host i's items at
@@ -53,6 +51,9 @@ apb_status launch_attention(int D, const AttnParams& p, const CUtensorMap& tq, c
 constexpr int kAttnMaxHosts = 8;
 struct AttnLaunch {
   CUtensorMap tq[kAttnMaxHosts], tk[kAttnMaxHosts], tv[kAttnMaxHosts];
+  // bf16 output of the anchor rows [0, L_A) and of the block rows [L_A, L_A + l_b) as two maps
+  // (d, heads, rows), so a TMA store of a ragged last tile is clipped at its own segment's end
+  CUtensorMap to_a[kAttnMaxHosts], to_b[kAttnMaxHosts];
   CUtensorMap tg;  // the gathered passing slots (shared by every host of the launch)
   AttnParams p[kAttnMaxHosts];
   int item_begin[kAttnMaxHosts + 1];

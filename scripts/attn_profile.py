@@ -126,10 +126,16 @@ def main():
         n_loc = (nB * g_ + 1) // 2 * cfg.hk
         n_anc = 0 if a.phase == "passing" else (nA * g_ + 1) // 2 * cfg.hk
         n = n_loc + n_anc
-        buf = (ctypes.c_ulonglong * (3 * n))()
+        buf = (ctypes.c_ulonglong * (5 * n))()
         lib.apb_debug_cta_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.apb_debug_cta_times(buf, n)
-        t = np.array(list(buf), dtype=np.int64).reshape(n, 3)
+        t = np.array(list(buf), dtype=np.int64).reshape(n, 5)
+        pro = (t[:, 3] - t[:, 0]).astype(np.float64)
+        epi = (t[:, 1] - t[:, 4]).astype(np.float64)
+        tot = (t[:, 1] - t[:, 0]).astype(np.float64)
+        print(f"per CTA: prologue (start -> first S issued) mean {pro.mean():.0f} ns, epilogue (O final -> end) "
+              f"mean {epi.mean():.0f} ns, CTA mean {tot.mean():.0f} ns; (prologue + epilogue) / CTA time "
+              f"{(pro.sum() + epi.sum()) / tot.sum():.4f}")
         t0 = t[:, 0].min()
         st, en, sm = t[:, 0] - t0, t[:, 1] - t0, t[:, 2]
         span = en.max()
