@@ -431,12 +431,11 @@ def main():
         traffic = json.load(open(tpath)).get(args.config, {}).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
-                "kernel": "apb_attention_kernel<128" + (", paired: 2-CTA clusters multicasting K/V"
-                                                         if cfg.d == 128
-                                                         and os.environ.get("APB_ATTN_PAIR", "")[:1] != "0"
-                                                         and (not pr.split_phases
-                                                              or os.environ.get("APB_ATTN_PAIR", "")[:1] == "1")
-                                                         else "") + "> ("
+                "kernel": "apb_attention_kernel<128" + (
+                    ", paired: 2-CTA clusters multicasting K/V"
+                    if cfg.d == 128 and (os.environ.get("APB_ATTN_PAIR", "")[:1] == "1"
+                                         or (os.environ.get("APB_ATTN_PAIR", "")[:1] == "a" and not pr.split_phases))
+                    else ", persistent: CTAs steal pending items (clusterlaunchcontrol)") + "> ("
                 + (("one LOCAL + one PASSING launch over the rank's hosts" if pr.batched
                     else "LOCAL + PASSING launches") if pr.split_phases
                    else ("one PHASE_ALL launch per layer over every host" if pr.batched

@@ -231,7 +231,6 @@ static apb_status attention_setup(const apb_dims* d, const void* q, const void* 
     p.ws_lse = reinterpret_cast<float*>(static_cast<char*>(ws) + o);
   }
 
-  if (const char* dbg = std::getenv("APB_DEBUG_SKIP")) p.dbg_skip = std::atoi(dbg);  // timing experiments only
   {
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)hq, (uint64_t)rows};
     uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)q_row_stride * 2};

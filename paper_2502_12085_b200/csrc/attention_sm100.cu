@@ -36,18 +36,11 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 // K and V tiles share one ring, loaded in consumption order K(0), V(0), K(1), V(1), ...;
 // K(i) is released after S_1(i), V(i) after PV_1(i) — also in sequence order — so a slot is
-// reused exactly kRing loads later.  Load n (= 2i for K(i), 2i+1 for V(i)) uses slot n % kRing.
-#ifndef APB_RING
-#define APB_RING 5
-#endif
-#ifdef APB_PSMEM
-// P lives in shared memory (64 KB for the two tiles), which leaves room for 3 K/V tiles at d = 128
+// reused exactly kRing loads later.  Load n (= 2i for K(i), 2i+1 for V(i), counted across all the
+// items a CTA runs) uses slot n % kRing.  3 slots at d = 128 leave room for the O staging tiles
+// (ring depths 2..5 measured equal in round 1: the loads are not on the critical path).
 template <int D>
 constexpr int ring_slots() { return D == 128 ? 3 : 6; }
-#else
-template <int D>
-constexpr int ring_slots() { return D == 128 ? APB_RING : 2 * APB_RING; }
-#endif
 constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, {TMA, MMA, 2 idle}
 constexpr int kLoadWarp = 10;  // SMSP 2 (warps 0/4 on SMSP 0 would otherwise share with it)
 constexpr int kMmaWarp = 9;
@@ -115,21 +108,17 @@ struct Layout {
   static constexpr int kTile = kHalves * kSub;     // bytes of a 128 x D bf16 tile
   static constexpr int kRing = ring_slots<D>();
   static constexpr int kQ = 0;
-  static constexpr int kR = kQ + 2 * kTile;  // the K/V ring
-#ifdef APB_PSMEM
-  static constexpr int kP = kR + kRing * kTile;    // P_t: [128 rows][128 keys] bf16, two SW128 sub-tiles
-  static constexpr int kBar = kP + 2 * 2 * kSub;
-  // barriers: Qfull, full[kRing], empty[kRing], Sfull[2], Sfree[2], Pfull[2][2 halves], PVdone[2]
-  static constexpr int kNumBars = 1 + 2 * kRing + 10;
-#else
-  static constexpr int kBar = kR + kRing * kTile;
-  // barriers: Qfull, full[kRing], empty[kRing], Sfull[2], Pfull[2][2 halves], Odone[2]
-  static constexpr int kNumBars = 1 + 2 * kRing + 8;
-#endif
-  static constexpr int kTmemPtr = kBar + kNumBars * 8;
+  static constexpr int kR = kQ + 2 * kTile;        // the K/V ring
+  static constexpr int kO = kR + kRing * kTile;    // bf16 O staging of the two tiles (TMA stores)
+  static constexpr int kBar = kO + 2 * kTile;
+  // barriers: Qfull, Qfree, full[kRing], empty[kRing], Sfull[2], Pfull[2][2 halves], Ofull[2],
+  // Ofree[2], work[2] (next-item response landed), workfree[2] (response read by every role)
+  static constexpr int kNumBars = 2 + 2 * kRing + 12;
+  static constexpr int kWork = (kBar + kNumBars * 8 + 15) / 16 * 16;  // 2 x 16-byte CLC responses
+  static constexpr int kTmemPtr = kWork + 32;
   static constexpr int kUsed = kTmemPtr + 16;
-  // keep one CTA per SM (each CTA allocates all 512 TMEM columns)
-  static constexpr int kAlloc = (kUsed + 1024) > 120 * 1024 ? (kUsed + 1024) : 120 * 1024;
+  static constexpr int kAlloc = kUsed + 1024;      // + alignment slack; one CTA per SM (512 TMEM columns)
+  static_assert(kAlloc <= 232448, "shared memory");
 };
 
 struct Item {
@@ -230,19 +219,21 @@ __device__ __forceinline__ int visible_cols(const AttnParams& p, const Item& it,
 // tile and multicasts it to both, so the tile crosses L2 -> SM once per pair; a ring slot is
 // refilled only after both CTAs' MMAs released it (empty barriers count 2, released by multicast
 // commits).  Tiles past the prefix are loaded whole by the CTA that needs them and released by two
-// local commits.
+// local commits.  A pair runs one item each (no work stealing).
+//
+// Persistent (single CTA): a CTA starts on item blockIdx.x, and when its TMA warp has issued the
+// last load of an item it asks the hardware for more work (clusterlaunchcontrol.try_cancel): a
+// CTA of this grid that has not launched yet is cancelled and its item runs here next.  Every role
+// reads the response at the end of its current item, so the next item's Q / K / V loads and first
+// S MMAs overlap the current item's last steps and epilogue, and no CTA launch, barrier set-up,
+// TMEM allocation or Q-load latency sits between items.  Items keep the launch order (heaviest
+// first): the stealing is dynamic, the last items go to whichever SMs free up first.
+// Cross-item hazards: the Q tiles are reloaded after the previous item's last S MMA (Qfree), O_t
+// is overwritten by the next item's first PV_t only after the softmax warps have read it (Ofree),
+// the staging tile of O_t is rewritten only after its previous TMA store has read it.
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     apb_attention_kernel(const __grid_constant__ AttnLaunch La) {
-  // this CTA's host (launch-uniform tables in the parameter space) and its item within the host
-  int hh = 0;
-  while (hh + 1 < La.n && static_cast<int>(blockIdx.x) >= La.item_begin[hh + 1]) ++hh;
-  const AttnParams& p = La.p[hh];
-  const int w_item = static_cast<int>(blockIdx.x) - La.item_begin[hh];
-  const CUtensorMap* tm_q = &La.tq[hh];
-  const CUtensorMap* tm_k = &La.tk[hh];
-  const CUtensorMap* tm_v = &La.tv[hh];
-  const CUtensorMap* tm_g = &La.tg;
   using L = Layout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
@@ -250,28 +241,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NR = L::kRing;
   const uint32_t sQ = sbase + L::kQ;
   const uint32_t bar0 = sbase + L::kBar;
-  const uint32_t bQ = bar0;
+  const uint32_t bQ = bar0, bQf = bar0 + 8u;
   auto sR = [&](int slot) { return sbase + L::kR + slot * L::kTile; };
-  auto bRf = [&](int slot) { return bar0 + 8u * (1 + slot); };
-  auto bRe = [&](int slot) { return bar0 + 8u * (1 + NR + slot); };
-  auto bS = [&](int t) { return bar0 + 8u * (1 + 2 * NR + t); };
-  auto bP = [&](int t, int half) { return bar0 + 8u * (3 + 2 * NR + 2 * t + half); };
-  auto bO = [&](int t) { return bar0 + 8u * (7 + 2 * NR + t); };
-#ifdef APB_PSMEM
-  // bO(t) doubles as PVdone(t) (one commit per PV_t(i)); Sfree(t): the softmax has S_t in registers
-  auto bSf = [&](int t) { return bar0 + 8u * (9 + 2 * NR + t); };
-  auto sP = [&](int t) { return sbase + L::kP + t * 2 * L::kSub; };
-#endif
+  auto sO = [&](int t) { return sbase + L::kO + t * L::kTile; };
+  auto bRf = [&](int slot) { return bar0 + 8u * (2 + slot); };
+  auto bRe = [&](int slot) { return bar0 + 8u * (2 + NR + slot); };
+  auto bS = [&](int t) { return bar0 + 8u * (2 + 2 * NR + t); };
+  auto bP = [&](int t, int half) { return bar0 + 8u * (4 + 2 * NR + 2 * t + half); };
+  auto bO = [&](int t) { return bar0 + 8u * (8 + 2 * NR + t); };
+  auto bOf = [&](int t) { return bar0 + 8u * (10 + 2 * NR + t); };
+  auto bW = [&](int b) { return bar0 + 8u * (12 + 2 * NR + b); };
+  auto bWf = [&](int b) { return bar0 + 8u * (14 + 2 * NR + b); };
+  auto sW = [&](int b) { return sbase + L::kWork + 16u * b; };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtr);
+  constexpr int kWorkReaders = 9;  // the MMA warp and the 8 softmax warps read every response
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
-  const Item it = decode_item(p, w_item);
-  // K/V tiles shared with the partner CTA (PAIR): the common prefix of the two walks
-  const int n_shared = PAIR ? min(it.nkv, decode_item(p, w_item ^ 1).nkv) : 0;  // item_begin[] even
   CTA_TIME(0);
 
   if (threadIdx.x == 0) {
     mbar_init(bQ, 1);
+    mbar_init(bQf, 1);
     for (int r = 0; r < NR; ++r) {
       mbar_init(bRf(r), 1);
       mbar_init(bRe(r), PAIR ? 2 : 1);
@@ -281,20 +271,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bP(t, 0), BM);
       mbar_init(bP(t, 1), BM);
       mbar_init(bO(t), 1);
-#ifdef APB_PSMEM
-      mbar_init(bSf(t), BM);
-#endif
+      mbar_init(bOf(t), BM);
+      mbar_init(bW(t), 1);
+      mbar_init(bWf(t), kWorkReaders);
     }
     fence_mbar_init();
   }
   if (warp == kLoadWarp) {
     tmem_alloc<512>(smem_u32(tmem_ptr));
-    if (elect_one()) {
-      tma_prefetch_desc(tm_q);
-      tma_prefetch_desc(tm_k);
-      tma_prefetch_desc(tm_v);
-      tma_prefetch_desc(tm_g);
-    }
     __syncwarp();
   }
   tc_fence_before();
@@ -304,81 +288,129 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMEM base broadcast from lane 0: provably warp-uniform, so every TMEM address and UMMA
   // operand below lives in uniform registers (no per-instruction waterfall loops).
   const uint32_t tmem = warp_uniform(*tmem_ptr);
+
+  // ---- the work list: item k of this CTA is launch item `gid`; host hh, item w within the host
+  struct Work {
+    int hh, w;
+    const AttnParams* p;
+    Item it;
+    int n_shared;
+  };
+  auto resolve = [&](int gid) {
+    Work c;
+    int hh = 0;
+    while (hh + 1 < La.n && gid >= La.item_begin[hh + 1]) ++hh;
+    c.hh = hh;
+    c.w = gid - La.item_begin[hh];
+    c.p = &La.p[hh];
+    c.it = decode_item(*c.p, c.w);
+    // K/V tiles shared with the partner CTA (PAIR): the common prefix of the two walks
+    c.n_shared = PAIR ? min(c.it.nkv, decode_item(*c.p, c.w ^ 1).nkv) : 0;  // item_begin[] even
+    return c;
+  };
+  // next item: wait for the response of the k-th request (buffer k & 1), read it, -1 if none
+  auto next_gid = [&](int k, bool reader) -> int {
+    const int b = k & 1;
+    mbar_wait_sleep(bW(b), (k >> 1) & 1);
+    uint32_t ok, x;
+    asm volatile(
+        "{\n\t.reg .b128 h;\n\t.reg .pred p;\n\t"
+        "ld.shared.b128 h, [%2];\n\t"
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, h;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, h;\n\t}"
+        : "=r"(ok), "=r"(x)
+        : "r"(sW(b))
+        : "memory");
+    __syncwarp();
+    if (reader && (threadIdx.x & 31) == 0) mbar_arrive(bWf(b));
+    return ok ? static_cast<int>(x) : -1;
+  };
+
   // Register split: the softmax warpgroups hold a 128-wide S row per thread; the producer / MMA
   // warpgroup needs few registers.  (per SMSP: 2 x 200 + 1 x 104 regs x 32 lanes <= 16384)
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
     if (warp == kLoadWarp) {
       // ============================================================== TMA producer (warp-converged)
-      const int qbase = it.seg == 0 ? 0 : p.L_A;
-#ifndef APB_NO_L2_HINTS
       const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-#define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d_hint(dst, map, bar, a, b, c, pol_kv)
-#define KV_LOAD4(dst, map, bar, a, b, c, d) tma_load_4d_hint(dst, map, bar, a, b, c, d, pol_kv)
-#else
-      const uint64_t pol_kv = policy_evict_last();  // PAIR's multicast loads keep the hint
-#define KV_LOAD3(dst, map, bar, a, b, c) tma_load_3d(dst, map, bar, a, b, c)
-#define KV_LOAD4(dst, map, bar, a, b, c, d) tma_load_4d(dst, map, bar, a, b, c, d)
-#endif
-      if (elect_one()) {
-        mbar_arrive_expect_tx(bQ, it.ntiles * L::kTile);
-        for (int t = 0; t < it.ntiles; ++t)
-          for (int h = 0; h < L::kHalves; ++h)
-#ifndef APB_NO_L2_HINTS
-            tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM, pol_q);
-#else
-            tma_load_3d(sQ + t * L::kTile + h * L::kSub, tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM);
-#endif
-      }
-      __syncwarp();
-#ifdef APB_PSMEM
-      // loads in the MMA warp's consumption order: K(0), then per step i: K(i+1), V(i)
-      for (int n = 0; n < 2 * it.nkv; ++n) {
-        int kv, i;
-        if (n == 0) { kv = 0; i = 0; }
-        else if (n - 1 == 2 * (it.nkv - 1)) { kv = 1; i = it.nkv - 1; }
-        else if (((n - 1) & 1) == 0) { kv = 0; i = (n - 1) / 2 + 1; }
-        else { kv = 1; i = (n - 2) / 2; }
-        const KvTile kt = kv_tile(p, it, i);
-        const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
-        {
-          const int r = n % NR;
-#else
-      for (int i = 0; i < it.nkv; ++i) {
-        const KvTile kt = kv_tile(p, it, i);
-        const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
+      int n0 = 0;  // ring sequence number of this item's first load
+      int gid = static_cast<int>(blockIdx.x);
+      for (int k = 0;; ++k) {
+        const Work c = resolve(gid);
+        const Item& it = c.it;
+        const AttnParams& p = *c.p;
+        const CUtensorMap* tm_q = &La.tq[c.hh];
+        const CUtensorMap* tm_k = &La.tk[c.hh];
+        const CUtensorMap* tm_v = &La.tv[c.hh];
+        const CUtensorMap* tm_g = &La.tg;
+        if (k == 0 && elect_one()) {
+          tma_prefetch_desc(tm_q);
+          tma_prefetch_desc(tm_k);
+          tma_prefetch_desc(tm_v);
+          tma_prefetch_desc(tm_g);
+        }
+        const int qbase = it.seg == 0 ? 0 : p.L_A;
+        if (k > 0) mbar_wait_sleep(bQf, (k - 1) & 1);  // the previous item's last S MMA read Q
+        if (elect_one()) {
+          mbar_arrive_expect_tx(bQ, it.ntiles * L::kTile);
+          for (int t = 0; t < it.ntiles; ++t)
+            for (int h = 0; h < L::kHalves; ++h)
+              tma_load_3d_hint(sQ + t * L::kTile + h * L::kSub, tm_q, bQ, h * 64, it.qht[t], qbase + it.rtt[t] * BM,
+                               pol_q);
+        }
+        __syncwarp();
+        for (int i = 0; i < it.nkv; ++i) {
+          const KvTile kt = kv_tile(p, it, i);
+          const int row0 = (kt.kind == 2 ? p.L_A : 0) + kt.c * BN;
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {
-          const int n = 2 * i + kv, r = n % NR;
-#endif
-          mbar_wait_sleep(bRe(r), ((n / NR) & 1) ^ 1);
-          if (elect_one()) {
-            if (!PAIR && (p.dbg_skip & (1 << kv)) && i >= NR) {
-              mbar_arrive(bRf(r));
-            } else if (PAIR && i < n_shared) {
-              // this CTA's half of the tile, into the same slot of both CTAs of the pair
-              const int h = static_cast<int>(cluster_ctarank());
-              mbar_arrive_expect_tx(bRf(r), L::kTile);
-              if (kt.kind == 1)
-                tma_load_4d_mc_hint(sR(r) + h * L::kSub, tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv, 0x3, pol_kv);
-              else
-                tma_load_3d_mc_hint(sR(r) + h * L::kSub, kv ? tm_v : tm_k, bRf(r), h * 64, it.j, row0, 0x3, pol_kv);
-            } else {
-              mbar_arrive_expect_tx(bRf(r), L::kTile);
-              for (int h = 0; h < L::kHalves; ++h) {
+          for (int kv = 0; kv < 2; ++kv) {
+            const int n = n0 + 2 * i + kv, r = n % NR;
+            mbar_wait_sleep(bRe(r), ((n / NR) & 1) ^ 1);
+            if (elect_one()) {
+              if (PAIR && i < c.n_shared) {
+                // this CTA's half of the tile, into the same slot of both CTAs of the pair
+                const int h = static_cast<int>(cluster_ctarank());
+                mbar_arrive_expect_tx(bRf(r), L::kTile);
                 if (kt.kind == 1)
-                  KV_LOAD4(sR(r) + h * L::kSub, tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv);
+                  tma_load_4d_mc_hint(sR(r) + h * L::kSub, tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv, 0x3,
+                                      pol_kv);
                 else
-                  KV_LOAD3(sR(r) + h * L::kSub, kv ? tm_v : tm_k, bRf(r), h * 64, it.j, row0);
+                  tma_load_3d_mc_hint(sR(r) + h * L::kSub, kv ? tm_v : tm_k, bRf(r), h * 64, it.j, row0, 0x3, pol_kv);
+              } else {
+                mbar_arrive_expect_tx(bRf(r), L::kTile);
+                for (int h = 0; h < L::kHalves; ++h) {
+                  if (kt.kind == 1)
+                    tma_load_4d_hint(sR(r) + h * L::kSub, tm_g, bRf(r), h * 64, kt.c * BN, it.j, kt.slot * 2 + kv,
+                                     pol_kv);
+                  else
+                    tma_load_3d_hint(sR(r) + h * L::kSub, kv ? tm_v : tm_k, bRf(r), h * 64, it.j, row0, pol_kv);
+                }
               }
             }
+            __syncwarp();
           }
-          __syncwarp();
         }
+        n0 += 2 * it.nkv;
+        if constexpr (PAIR) break;  // a pair runs one item each
+        // every load of this item is issued: ask for the next item (response buffer k & 1, free
+        // once the readers of request k - 2 have read it)
+        mbar_wait_sleep(bWf(k & 1), ((k >> 1) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(bW(k & 1), 16);
+          asm volatile(
+              "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+                  sW(k & 1)),
+              "r"(bW(k & 1))
+              : "memory");
+        }
+        __syncwarp();
+        gid = next_gid(k, false);
+        if (gid < 0) break;
       }
       if constexpr (PAIR) {
         // drain: every release of this CTA's slots (by both MMA warps) has landed before exit
-        const int ntot = 2 * it.nkv;
+        const int ntot = n0;
         for (int r = 0; r < NR && r < ntot; ++r) {
           const int n_last = r + ((ntot - 1 - r) / NR) * NR;
           mbar_wait_sleep(bRe(r), (n_last / NR) & 1);
@@ -405,432 +437,323 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) mma_commit(bar);
         __syncwarp();
       };
-      // release of a ring slot: in PAIR mode on both CTAs' empty barriers
-      // (tile i of the walk; past the shared prefix both arrivals are local)
-      auto release = [&](int slot, int i) {
-        if (elect_one()) {
-          if (PAIR && i < n_shared) {
-            mma_commit_mc(bRe(slot), 0x3);
-          } else {
-            mma_commit(bRe(slot));
-            if (PAIR) mma_commit(bRe(slot));
-          }
-        }
-        __syncwarp();
-      };
-      int trace_i = 0;
-      (void)trace_i;
-      // O_t += P_t V in two K halves: keys [0,64) as soon as the softmax publishes the first half
-      // of P_t, keys [64,128) after the second half.
-      auto issue_PV = [&](int t, int s, bool acc, uint32_t parity) {
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-#ifdef APB_MMA_SPIN
-          mbar_wait(bP(t, half), parity);
-#else
-          mbar_wait_sleep(bP(t, half), parity);
-#endif
-          TRACE(2 + 2 * t + half, trace_i);
-          tc_fence_after();
+      int n0 = 0, gid = static_cast<int>(blockIdx.x);
+      int pseq[2] = {0, 0};  // P_t steps so far (bP(t, *) phases)
+      int oseq[2] = {0, 0};  // items tile t took part in so far (bO(t) / bOf(t) phases)
+      for (int k = 0;; ++k) {
+        const Work c = resolve(gid);
+        const Item& it = c.it;
+        const AttnParams& p = *c.p;
+        // release of a ring slot: in PAIR mode on both CTAs' empty barriers
+        // (tile i of the walk; past the shared prefix both arrivals are local)
+        auto release = [&](int slot, int i) {
           if (elect_one()) {
-#pragma unroll
-            for (int k = half * (BN / 32); k < (half + 1) * (BN / 32); ++k) {
-              mma_ts(tmem + 256 + t * D, tmem + t * 128 + k * 8,
-                     sdesc_sw128(sR(s) + k * 2048, L::kSub, 1024), idPV, (acc || k > 0) ? 1u : 0u);
+            if (PAIR && i < c.n_shared) {
+              mma_commit_mc(bRe(slot), 0x3);
+            } else {
+              mma_commit(bRe(slot));
+              if (PAIR) mma_commit(bRe(slot));
             }
           }
           __syncwarp();
-        }
-      };
-      const bool carry = (p.phase == APB_PHASE_PASSING);
-      mbar_wait_sleep(bQ, 0);
-      tc_fence_after();
-#ifdef APB_PSMEM
-      // S_t(i+1) is issued as soon as the softmax holds S_t(i) in registers (Sfree), so it runs
-      // under softmax_t(i); PV_t(i) (SS: A = P_t from shared memory) when P_t(i) is published.
-      // Ring sequence numbers follow the producer's order K(0), K(1), V(0), K(2), V(1), ...
-      auto nK = [&](int i) { return i == 0 ? 0 : 2 * i - 1; };
-      auto nV = [&](int i) { return i == it.nkv - 1 ? 2 * it.nkv - 1 : 2 * i + 2; };
-      if (it.nkv > 0) {
-        mbar_wait_sleep(bRf(0), 0);
-        tc_fence_after();
-        for (int t = 0; t < it.ntiles; ++t) issue_S(t, 0);
-        release(0, 0);
-      }
-      for (int i = 0; i < it.nkv; ++i) {
-        if (i + 1 < it.nkv) {
-          const int n = nK(i + 1);
-          for (int t = 0; t < it.ntiles; ++t) {
-            mbar_wait_sleep(bSf(t), i & 1);
-            if (t == 0) mbar_wait_sleep(bRf(n % NR), (n / NR) & 1);
-            tc_fence_after();
-            issue_S(t, n % NR);
-          }
-          release(n % NR, i + 1);
-        }
-        const int n = nV(i), sv = n % NR;
-        mbar_wait_sleep(bRf(sv), (n / NR) & 1);
-        tc_fence_after();
-        for (int t = 0; t < it.ntiles; ++t) {
+        };
+        // O_t += P_t V in two K halves: keys [0,64) as soon as the softmax publishes the first half
+        // of P_t, keys [64,128) after the second half.  The first PV_t of an item overwrites O_t:
+        // the softmax warps must have read the previous item's O_t (Ofree).
+        auto issue_PV = [&](int t, int s, bool acc, int step) {
+          if (step == 0 && oseq[t] > 0) mbar_wait_sleep(bOf(t), (oseq[t] - 1) & 1);
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            mbar_wait_sleep(bP(t, half), i & 1);
+            mbar_wait_sleep(bP(t, half), (pseq[t] + step) & 1);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
-              for (int k = half * (BN / 32); k < (half + 1) * (BN / 32); ++k)
-                mma_ss(tmem + 256 + t * D, sdesc_sw128(sP(t) + (k / 4) * L::kSub + (k % 4) * 32, 16, 1024),
-                       sdesc_sw128(sR(sv) + k * 2048, L::kSub, 1024), idPV, (carry || i > 0 || k > 0) ? 1u : 0u);
+              for (int kk = half * (BN / 32); kk < (half + 1) * (BN / 32); ++kk) {
+                mma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, sdesc_sw128(sR(s) + kk * 2048, L::kSub, 1024), idPV,
+                       (acc || kk > 0) ? 1u : 0u);
+              }
             }
             __syncwarp();
           }
-          commit(bO(t));  // PVdone(t): P_t is free and O_t stable
-        }
-        release(sv, i);
-      }
-      (void)issue_PV;
-#else
-      for (int i = 0; i < it.nkv; ++i) {
-        trace_i = i;
-        const int nK = 2 * i, nV = 2 * i + 1, nK1 = 2 * i + 2;  // ring sequence numbers
-        if (i == 0) {
-          mbar_wait_sleep(bRf(nK % NR), (nK / NR) & 1);
-          tc_fence_after();
-          if (elect_one()) CTA_STAMP(3);
-          __syncwarp();
-          for (int t = 0; t < it.ntiles; ++t) {
-            TRACE(t, 0);
-            issue_S(t, nK % NR);
-          }
-          release(nK % NR, 0);
-        }
-        mbar_wait_sleep(bRf(nV % NR), (nV / NR) & 1);
-        TRACE(12, i);
+        };
+        const bool carry = (p.phase == APB_PHASE_PASSING);
+        mbar_wait_sleep(bQ, k & 1);
         tc_fence_after();
-        for (int t = 0; t < it.ntiles; ++t) {
-          issue_PV(t, nV % NR, carry || i > 0, i & 1);
-          if (t == it.ntiles - 1) release(nV % NR, i);
-          if (i + 1 < it.nkv) {
-            if (t == 0) {
-              mbar_wait_sleep(bRf(nK1 % NR), (nK1 / NR) & 1);
-              TRACE(13, i + 1);
-              tc_fence_after();
+        for (int i = 0; i < it.nkv; ++i) {
+          const int nK = n0 + 2 * i, nV = nK + 1, nK1 = nK + 2;  // ring sequence numbers
+          if (i == 0) {
+            mbar_wait_sleep(bRf(nK % NR), (nK / NR) & 1);
+            tc_fence_after();
+            if (elect_one()) CTA_STAMP(3);
+            __syncwarp();
+            for (int t = 0; t < it.ntiles; ++t) {
+              TRACE(t, 0);
+              issue_S(t, nK % NR);
             }
-            TRACE(t, i + 1);
-            issue_S(t, nK1 % NR);
-            if (t == it.ntiles - 1) release(nK1 % NR, i + 1);
-          } else {
-            commit(bO(t));
+            release(nK % NR, 0);
+            if (it.nkv == 1) commit(bQf);  // the item's last S MMAs are issued: Q may be reloaded
+          }
+          mbar_wait_sleep(bRf(nV % NR), (nV / NR) & 1);
+          TRACE(12, i);
+          tc_fence_after();
+          for (int t = 0; t < it.ntiles; ++t) {
+            issue_PV(t, nV % NR, carry || i > 0, i);
+            if (t == it.ntiles - 1) release(nV % NR, i);
+            if (i + 1 < it.nkv) {
+              if (t == 0) {
+                mbar_wait_sleep(bRf(nK1 % NR), (nK1 / NR) & 1);
+                TRACE(13, i + 1);
+                tc_fence_after();
+              }
+              TRACE(t, i + 1);
+              issue_S(t, nK1 % NR);
+              if (t == it.ntiles - 1) {
+                release(nK1 % NR, i + 1);
+                if (i + 2 == it.nkv) commit(bQf);  // the item's last S MMAs are issued
+              }
+            } else {
+              commit(bO(t));
+            }
           }
         }
+        for (int t = 0; t < it.ntiles; ++t) {
+          pseq[t] += it.nkv;
+          ++oseq[t];
+        }
+        n0 += 2 * it.nkv;
+        if constexpr (PAIR) break;
+        gid = next_gid(k, true);
+        if (gid < 0) break;
       }
-#endif
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
     // ================================================================ softmax warpgroups
     const int t = warp / 4;
-    if (t < it.ntiles) {
-      const int tid = threadIdx.x % 128;
-      const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t tS = tmem + lane_base + t * 128;
-      const uint32_t tO = tmem + lane_base + 256 + t * D;
-      const int qh = it.qht[t];
-      const int row = it.rtt[t] * BM + tid;  // row index inside the query segment
-      const bool row_valid = it.seg == 0 ? row < p.L_A : row < p.l_b;
-      const float sl2 = p.scale_log2;
-      float m_run = -INFINITY, l_run = 0.f;
-      bool o_valid = false;
+    const int tid = threadIdx.x % 128;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + t * 128;
+    const uint32_t tO = tmem + lane_base + 256 + t * D;
+    const float* no_p = nullptr;
+    (void)no_p;
+    int sseq = 0;  // S_t steps so far (bS(t) phases)
+    int oseq = 0;  // items this tile took part in (bO(t) phases)
+    int gid = static_cast<int>(blockIdx.x);
+    for (int k = 0;; ++k) {
+      const Work c = resolve(gid);
+      const Item& it = c.it;
+      const AttnParams& p = *c.p;
+      if (t < it.ntiles) {
+        const int qh = it.qht[t];
+        const int row = it.rtt[t] * BM + tid;  // row index inside the query segment
+        const bool row_valid = it.seg == 0 ? row < p.L_A : row < p.l_b;
+        const float sl2 = p.scale_log2;
+        float m_run = -INFINITY, l_run = 0.f;
+        bool o_valid = false;
 
-      if (p.phase == APB_PHASE_PASSING) {
-        // LSE carry-in: the LOCAL phase's normalised partial (O, m + log2 l) becomes the
-        // initial online-softmax state (m = lse2, l = 1, O = O_partial) — an exact merge.
-        const float* src = p.ws_o + ((int64_t)(row_valid ? row : 0) * p.hq + qh) * D;
-        m_run = row_valid ? p.ws_lse[(int64_t)qh * p.l_b + row] : 0.f;
-        l_run = 1.f;
+        if (p.phase == APB_PHASE_PASSING) {
+          // LSE carry-in: the LOCAL phase's normalised partial (O, m + log2 l) becomes the
+          // initial online-softmax state (m = lse2, l = 1, O = O_partial) — an exact merge.
+          // (O_t of this tile's previous item was read by these threads' epilogue.)
+          const float* src = p.ws_o + ((int64_t)(row_valid ? row : 0) * p.hq + qh) * D;
+          m_run = row_valid ? p.ws_lse[(int64_t)qh * p.l_b + row] : 0.f;
+          l_run = 1.f;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t r[32];
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            float4 f = row_valid ? *reinterpret_cast<const float4*>(src + c * 32 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-            r[e] = __float_as_uint(f.x);
-            r[e + 1] = __float_as_uint(f.y);
-            r[e + 2] = __float_as_uint(f.z);
-            r[e + 3] = __float_as_uint(f.w);
+            for (int e = 0; e < 32; e += 4) {
+              float4 f = row_valid ? *reinterpret_cast<const float4*>(src + cc * 32 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+              r[e] = __float_as_uint(f.x);
+              r[e + 1] = __float_as_uint(f.y);
+              r[e + 2] = __float_as_uint(f.z);
+              r[e + 3] = __float_as_uint(f.w);
+            }
+            tmem_st32(tO + cc * 32, r);
           }
-          tmem_st32(tO + c * 32, r);
+          tmem_wait_st();
+          o_valid = true;
         }
-        tmem_wait_st();
-        o_valid = true;
-      }
 
-#ifdef APB_PINGPONG
-      const bool pingpong = (it.ntiles == 2);
-      if (pingpong && t == 1) named_bar_arrive(1, 256);  // tile 0 goes first
-#endif
-      for (int i = 0; i < it.nkv; ++i) {
-        const KvTile kt = kv_tile(p, it, i);
-        const int nv = visible_cols(p, it, kt, row);
-#ifdef APB_SOFTMAX_SLEEP
-        mbar_wait_sleep(bS(t), i & 1);
-#else
-        mbar_wait(bS(t), i & 1);
-#endif
-        if (tid == 0) TRACE(6 + t, i);
-        tc_fence_after();
-        if (p.dbg_skip & 4) {  // timing experiment only: no softmax work, publish stale P
+        for (int i = 0; i < it.nkv; ++i) {
+          const KvTile kt = kv_tile(p, it, i);
+          const int nv = visible_cols(p, it, kt, row);
+          mbar_wait(bS(t), (sseq + i) & 1);
+          if (tid == 0) TRACE(6 + t, i);
+          tc_fence_after();
+          uint32_t sr[128];
+          tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+          tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+          tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
+          tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+          tmem_wait_ld();
+          float* s = reinterpret_cast<float*>(sr);
+          if (tid == 0) TRACE(16 + t * 4, i);
+          if (nv < BN) {
+#pragma unroll
+            for (int cc = 0; cc < BN; ++cc)
+              if (cc >= nv) s[cc] = -INFINITY;
+          }
+          // 2^(s*scale*log2e - m) for the 64 columns of one half; packed FFMA2 for the argument;
+          // kPolyPairs of every 16 column pairs on the FMA pipe (Cody-Waite + degree-3 polynomial,
+          // rel. error 7.5e-5 << bf16's 3.9e-3), the rest on MUFU.EX2.
+          auto exp_half = [&](int half, float m_use, uint32_t (&pk)[32], uint64_t (&acc2)[4]) {
+            const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_use, -m_use);
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) {
+              const int col = half * 64 + 2 * cc;
+              const uint64_t x2 = ffma2(f2_pack(s[col], s[col + 1]), sc2, nm2);
+              float p0, p1;
+              if ((cc % 16) < kPolyPairs) {
+                const uint64_t p2 = exp2_poly2(x2);
+                f2_unpack(p2, p0, p1);
+              } else {
+                float x0, x1;
+                f2_unpack(x2, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              pk[cc] = pack_bf16x2(p0, p1);
+              // the row sum adds the bf16 weights the PV MMA actually uses, so the normalisation
+              // matches them (with the lazy rescale the row max's weight is 2^delta, not 1, and
+              // bf16-rounding it alone would bias O by up to 2^-9 relative; reading G21)
+              acc2[cc & 3] = f2_add_bf16x2(acc2[cc & 3], pk[cc]);
+            }
+          };
+          // Speculation: the running max m_run only moves when a row max grows by more than the
+          // threshold, so the first half's exponentials are computed against m_run on the
+          // MUFU/FMA pipes while the ALU pipe reduces the new row max; the (rare) rows whose max
+          // grew redo the half with the new max.
+          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+          uint32_t pk[32];
+          const bool have_m = (m_run != -INFINITY);
+          const float m_spec = have_m ? m_run : 0.f;
+          exp_half(0, m_spec, pk, acc2);
+          float mx8[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) mx8[q] = fmax3(s[2 * q], s[2 * q + 1], s[16 + 2 * q]);
+#pragma unroll
+          for (int cc = 32; cc < BN; cc += 16) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mx8[q] = fmax3(mx8[q], s[cc + 2 * q], s[cc + 2 * q + 1]);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], s[16 + 2 * q + 1]);
+          const float mx = sl2 * fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+          const bool grow = !have_m || (mx > m_run + kRescaleThreshold);
+          float alpha = 1.f;
+          if (tid == 0) TRACE(17 + t * 4, i);
+          if (__any_sync(0xffffffffu, grow)) {
+            if (grow) {
+              const float m_new = fmaxf(m_run, mx);
+              alpha = have_m ? ex2(m_run - m_new) : 0.f;
+              m_run = m_new;
+              const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+              acc2[0] = acc2[1] = acc2[2] = acc2[3] = 0ull;
+              exp_half(0, m_use, pk, acc2);
+            }
+            // rescale the running O_t before any PV_t(i) MMA (PV_t(i-1) is complete: S_t(i) was
+            // issued after it)
+            if (__any_sync(0xffffffffu, grow && o_valid && alpha != 1.f)) {
+              const float a = (grow && o_valid) ? alpha : 1.f;
+#pragma unroll
+              for (int cc = 0; cc < D / 16; ++cc) {
+                uint32_t r[16];
+                tmem_ld16(tO + cc * 16, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * a);
+                tmem_st16(tO + cc * 16, r);
+              }
+            }
+          }
+          const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+          if (tid == 0) TRACE(18 + t * 4, i);
+          tmem_st32(tS, pk);
+          tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bP(t, 0));
+          if (tid == 0) TRACE(8 + 2 * t, i);
+          exp_half(1, m_use, pk, acc2);
+          tmem_st32(tS + 32, pk);
+          tmem_wait_st();
+          tc_fence_before();
           mbar_arrive(bP(t, 1));
+          if (tid == 0) TRACE(9 + 2 * t, i);
+          if ((tid & 31) == 0) TRACE(24 + t * 4 + (tid >> 5), i);
+          float r0, r1, r2, r3;
+          f2_unpack(fadd2(acc2[0], acc2[1]), r0, r1);
+          f2_unpack(fadd2(acc2[2], acc2[3]), r2, r3);
+          l_run = l_run * alpha + ((r0 + r1) + (r2 + r3));
           o_valid = true;
-          continue;
         }
-        uint32_t sr[128];
-        tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
-        tmem_wait_ld();
-#ifdef APB_PSMEM
-        tc_fence_before();
-        mbar_arrive(bSf(t));  // S_t(i) is in registers: the MMA warp may compute S_t(i+1) now
-#endif
-        float* s = reinterpret_cast<float*>(sr);
-        if (tid == 0) TRACE(16 + t * 4, i);
-        if (nv < BN) {
-#pragma unroll
-          for (int c = 0; c < BN; ++c)
-            if (c >= nv) s[c] = -INFINITY;
-        }
-        // 2^(s*scale*log2e - m) for the 64 columns of one half; packed FFMA2 for the argument;
-        // kPolyPairs of every 16 column pairs on the FMA pipe (Cody-Waite + degree-3 polynomial,
-        // rel. error 7.5e-5 << bf16's 3.9e-3), the rest on MUFU.EX2 — balancing the two pipes.
-        auto exp_half = [&](int half, float m_use, uint32_t (&pk)[32], uint64_t (&acc2)[4]) {
-          const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_use, -m_use);
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int col = half * 64 + 2 * c;
-            const uint64_t x2 = ffma2(f2_pack(s[col], s[col + 1]), sc2, nm2);
-            float p0, p1;
-            uint64_t p2;
-            if ((c % 16) < kPolyPairs) {
-              p2 = exp2_poly2(x2);
-              f2_unpack(p2, p0, p1);
-            } else {
-              float x0, x1;
-              f2_unpack(x2, x0, x1);
-#ifdef APB_DEBUG_NO_MUFU
-              p0 = x0 * 1e-30f;  // timing experiment only: no MUFU
-              p1 = x1 * 1e-30f;
-#else
-              p0 = ex2(x0);
-              p1 = ex2(x1);
-#endif
-              p2 = f2_pack(p0, p1);
-            }
-            pk[c] = pack_bf16x2(p0, p1);
-#ifdef APB_ROWSUM_FP32
-            acc2[c & 3] = fadd2(acc2[c & 3], p2);
-#else
-            // the row sum adds the bf16 weights the PV MMA actually uses, so the normalisation
-            // matches them (with the lazy rescale the row max's weight is 2^delta, not 1, and
-            // bf16-rounding it alone would bias O by up to 2^-9 relative)
-            (void)p2;
-            acc2[c & 3] = f2_add_bf16x2(acc2[c & 3], pk[c]);
-#endif
-          }
-        };
-        // Speculation: the running max m_run only moves when a row max grows by more than the
-        // threshold, so the first half's exponentials are computed against m_run on the
-        // MUFU/FMA pipes while the ALU pipe reduces the new row max; the (rare) rows whose max
-        // grew redo the half with the new max.
-        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-        uint32_t pk[32];
-        const bool have_m = (m_run != -INFINITY);
-        const float m_spec = have_m ? m_run : 0.f;
-#ifdef APB_PINGPONG
-        // Optional ping-pong (-DAPB_PINGPONG): the two softmax warpgroups take turns for their
-        // MUFU-heavy phase (named barriers 1 + t, 256 threads).  Measured 3% slower than letting
-        // them overlap freely, so it is off by default.
-        if (pingpong) named_bar_sync(1 + t, 256);
-#endif
-        exp_half(0, m_spec, pk, acc2);
-        float mx8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmax3(s[2 * q], s[2 * q + 1], s[16 + 2 * q]);
-#pragma unroll
-        for (int c = 32; c < BN; c += 16) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) mx8[q] = fmax3(mx8[q], s[c + 2 * q], s[c + 2 * q + 1]);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], s[16 + 2 * q + 1]);
-        const float mx = sl2 * fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        const bool grow = !have_m || (mx > m_run + kRescaleThreshold);
-        float alpha = 1.f;
-        if (tid == 0) TRACE(17 + t * 4, i);
-#ifdef APB_PSMEM
-        if (i > 0) {  // PV_t(i-1) complete: O_t may be rescaled and P_t overwritten
-          mbar_wait(bO(t), (i - 1) & 1);
-          tc_fence_after();
-        }
-#endif
-        if (__any_sync(0xffffffffu, grow)) {
-          if (grow) {
-            const float m_new = fmaxf(m_run, mx);
-            alpha = have_m ? ex2(m_run - m_new) : 0.f;
-            m_run = m_new;
-            const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-            acc2[0] = acc2[1] = acc2[2] = acc2[3] = 0ull;
-            exp_half(0, m_use, pk, acc2);
-          }
-          // rescale the running O_t before any PV_t(i) MMA (PV_t(i-1) is complete: S_t(i) was
-          // issued after it)
-          if (__any_sync(0xffffffffu, grow && o_valid && alpha != 1.f)) {
-            const float a = (grow && o_valid) ? alpha : 1.f;
-#pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
-              uint32_t r[16];
-              tmem_ld16(tO + c * 16, r);
-              tmem_wait_ld();
-#pragma unroll
-              for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * a);
-              tmem_st16(tO + c * 16, r);
-            }
-          }
-        }
-        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        if (tid == 0) TRACE(18 + t * 4, i);
-#ifdef APB_PSMEM
-        auto store_P = [&](int half) {  // row tid of the SW128 K-major sub-tile `half` of P_t
-          const uint32_t base = sP(t) + half * L::kSub + tid * 128;
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + ((q ^ (tid & 7)) << 4)),
-                         "r"(pk[4 * q]), "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3]) : "memory");
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
-        };
-        store_P(0);
-        tmem_wait_st();  // an O rescale above
-        tc_fence_before();
-        mbar_arrive(bP(t, 0));
-#else
-        tmem_st32(tS, pk);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(bP(t, 0));
-#endif
-        if (tid == 0) TRACE(8 + 2 * t, i);
-        exp_half(1, m_use, pk, acc2);
-#ifdef APB_PSMEM
-        store_P(1);
-        tc_fence_before();
-        mbar_arrive(bP(t, 1));
-#else
-        tmem_st32(tS + 32, pk);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(bP(t, 1));
-#endif
-        if (tid == 0) TRACE(9 + 2 * t, i);
-        if ((tid & 31) == 0) TRACE(24 + t * 4 + (tid >> 5), i);
-#ifdef APB_PINGPONG
-        if (pingpong) named_bar_arrive(2 - t, 256);  // hand the turn to the other tile
-#endif
-        float r0, r1, r2, r3;
-        f2_unpack(fadd2(acc2[0], acc2[1]), r0, r1);
-        f2_unpack(fadd2(acc2[2], acc2[3]), r2, r3);
-        l_run = l_run * alpha + ((r0 + r1) + (r2 + r3));
-        o_valid = true;
-      }
+        sseq += it.nkv;
 
-#ifdef APB_PINGPONG
-      if (pingpong && t == 0) named_bar_sync(1, 256);  // consume tile 1's last hand-off
-#endif
-      // ============================================================== epilogue
-#ifdef APB_PSMEM
-      mbar_wait(bO(t), (it.nkv - 1) & 1);  // PV_t of the last step
-#else
-      mbar_wait(bO(t), 0);
-#endif
-      tc_fence_after();
-      if (tid == 0 && t == 0) CTA_STAMP(4);
-      const float inv_l = 1.f / l_run;
-      const bool to_ws = (it.seg == 1) && p.local_to_ws;
-      const int64_t grow_idx = (it.seg == 0 ? 0 : p.L_A) + row;  // row of q/out on this host
-#ifndef APB_PSMEM
-      if (!to_ws) {
-        // bf16 O tile -> shared memory (SW128, the Q tile layout) -> TMA store(s) by one thread.
-        // The staging slot (2 nkv + t) mod kRing of the K/V ring is idle: its last load is at least
-        // kRing - 2 loads older than the final V, so every MMA reading it has completed (the tile's
-        // last PV did), and the peer of a pair no longer multicasts into it.  Rows past the
-        // segment's end are clipped by the output map (anchor and block rows are separate maps).
-        const uint32_t stg = sR((2 * it.nkv + t) % NR);
+        // ============================================================== epilogue
+        mbar_wait(bO(t), oseq & 1);
+        ++oseq;
+        tc_fence_after();
+        if (tid == 0 && t == 0) CTA_STAMP(4);
+        const float inv_l = 1.f / l_run;
+        const bool to_ws = (it.seg == 1) && p.local_to_ws;
+        const int64_t grow_idx = (it.seg == 0 ? 0 : p.L_A) + row;  // row of q/out on this host
+        uint32_t o[D];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const int e = q4 * 8, chunk = (c & 1) * 4 + q4;
-            const uint32_t a = stg + (c >> 1) * L::kSub + tid * 128 + ((chunk ^ (tid & 7)) << 4);
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                         "r"(pack_bf16x2(__uint_as_float(r[e]) * inv_l, __uint_as_float(r[e + 1]) * inv_l)),
-                         "r"(pack_bf16x2(__uint_as_float(r[e + 2]) * inv_l, __uint_as_float(r[e + 3]) * inv_l)),
-                         "r"(pack_bf16x2(__uint_as_float(r[e + 4]) * inv_l, __uint_as_float(r[e + 5]) * inv_l)),
-                         "r"(pack_bf16x2(__uint_as_float(r[e + 6]) * inv_l, __uint_as_float(r[e + 7]) * inv_l))
-                         : "memory");
-          }
-        }
-        fence_proxy_async_smem();  // the generic-proxy writes are visible to the TMA engine
-        named_bar_sync(3 + t, 128);
-        if (tid == 0) {
-          const CUtensorMap* to = it.seg == 0 ? &La.to_a[hh] : &La.to_b[hh];
-#pragma unroll
-          for (int h = 0; h < L::kHalves; ++h) tma_store_3d(to, stg + h * L::kSub, h * 64, qh, it.rtt[t] * BM);
-          bulk_commit_group();
-          bulk_wait_group_read<0>();  // shared memory may be released (the CTA exits after this)
-        }
-      } else
-#endif
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tO + c * 32, r);
+        for (int cc = 0; cc < D / 32; ++cc) tmem_ld32(tO + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[cc * 32]));
         tmem_wait_ld();
-        if (row_valid) {
-          if (to_ws) {
-            float* dst = p.ws_o + ((int64_t)row * p.hq + qh) * D + c * 32;
+        tc_fence_before();
+        mbar_arrive(bOf(t));  // O_t is in registers: the next item's first PV_t may overwrite it
+        if (!to_ws) {
+          // bf16 O tile -> shared memory (SW128, the Q tile layout) -> TMA store(s) by one thread.
+          // Rows past the segment's end are clipped by the output map (anchor and block rows are
+          // separate maps).  The staging tile is rewritten only after its previous store read it.
+          const uint32_t stg = sO(t);
+          if (tid == 0) bulk_wait_group_read<0>();
+          named_bar_sync(3 + t, 128);
 #pragma unroll
-            for (int e = 0; e < 32; e += 4)
-              *reinterpret_cast<float4*>(dst + e) =
-                  make_float4(__uint_as_float(r[e]) * inv_l, __uint_as_float(r[e + 1]) * inv_l,
-                              __uint_as_float(r[e + 2]) * inv_l, __uint_as_float(r[e + 3]) * inv_l);
-          } else {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + grow_idx * p.out_row_stride + (int64_t)qh * D + c * 32;
+          for (int cc = 0; cc < D / 32; ++cc) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 8) {
-              uint4 v;
-              v.x = pack_bf16x2(__uint_as_float(r[e]) * inv_l, __uint_as_float(r[e + 1]) * inv_l);
-              v.y = pack_bf16x2(__uint_as_float(r[e + 2]) * inv_l, __uint_as_float(r[e + 3]) * inv_l);
-              v.z = pack_bf16x2(__uint_as_float(r[e + 4]) * inv_l, __uint_as_float(r[e + 5]) * inv_l);
-              v.w = pack_bf16x2(__uint_as_float(r[e + 6]) * inv_l, __uint_as_float(r[e + 7]) * inv_l);
-              *reinterpret_cast<uint4*>(dst + e) = v;
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int e = cc * 32 + q4 * 8, chunk = (cc & 1) * 4 + q4;
+              const uint32_t a = stg + (cc >> 1) * L::kSub + tid * 128 + ((chunk ^ (tid & 7)) << 4);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                           "r"(pack_bf16x2(__uint_as_float(o[e]) * inv_l, __uint_as_float(o[e + 1]) * inv_l)),
+                           "r"(pack_bf16x2(__uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l)),
+                           "r"(pack_bf16x2(__uint_as_float(o[e + 4]) * inv_l, __uint_as_float(o[e + 5]) * inv_l)),
+                           "r"(pack_bf16x2(__uint_as_float(o[e + 6]) * inv_l, __uint_as_float(o[e + 7]) * inv_l))
+                           : "memory");
             }
           }
+          fence_proxy_async_smem();  // the generic-proxy writes are visible to the TMA engine
+          named_bar_sync(3 + t, 128);
+          if (tid == 0) {
+            const CUtensorMap* to = it.seg == 0 ? &La.to_a[c.hh] : &La.to_b[c.hh];
+#pragma unroll
+            for (int h = 0; h < L::kHalves; ++h) tma_store_3d(to, stg + h * L::kSub, h * 64, qh, it.rtt[t] * BM);
+            bulk_commit_group();
+          }
+        } else if (row_valid) {
+          float* dst = p.ws_o + ((int64_t)row * p.hq + qh) * D;
+#pragma unroll
+          for (int e = 0; e < D; e += 4)
+            *reinterpret_cast<float4*>(dst + e) =
+                make_float4(__uint_as_float(o[e]) * inv_l, __uint_as_float(o[e + 1]) * inv_l,
+                            __uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l);
+        }
+        if (row_valid) {
+          const float lse2 = m_run + __log2f(l_run);
+          if (to_ws) {
+            p.ws_lse[(int64_t)qh * p.l_b + row] = lse2;
+          } else if (p.lse) {
+            p.lse[(int64_t)qh * p.lse_ld + grow_idx] = lse2 * 0.69314718055994530942f;
+          }
         }
       }
-      if (row_valid) {
-        const float lse2 = m_run + __log2f(l_run);
-        if (to_ws) {
-          p.ws_lse[(int64_t)qh * p.l_b + row] = lse2;
-        } else if (p.lse) {
-          p.lse[(int64_t)qh * p.lse_ld + grow_idx] = lse2 * 0.69314718055994530942f;
-        }
-      }
+      if constexpr (PAIR) break;
+      gid = next_gid(k, true);
+      if (gid < 0) break;
     }
+    if (tid == 0) bulk_wait_group_read<0>();  // the last TMA store has read its staging tile
   }
 
   tc_fence_before();
@@ -843,18 +766,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Paired (2-CTA cluster, multicast K/V) launch: on by default where it applies (D = 128, g % 4 == 0);
-// APB_ATTN_PAIR=0 in the environment selects the single-CTA kernel (A/B timing).
-// Read per launch (a getenv per multi-ms launch) so a test can compare both kernels in one process.
-// Paired 2-CTA clusters: by default for the one-pass PHASE_ALL launch (the N = 1 schedule: 0.6 %
-// faster and ~50 W lower on the L8 critical host); the LOCAL / PASSING launches of the N > 1
-// schedule run unpaired (L8 critical host, queued: LOCAL 2.86 vs 2.93 ms, PASSING 3.34 vs 3.35 ms).
-// APB_ATTN_PAIR=0: never; APB_ATTN_PAIR=1: every phase.
+// Launch policy.  Default: the persistent single-CTA kernel for every phase (CTAs steal pending
+// items with clusterlaunchcontrol.try_cancel, so no launch / set-up / Q-load gap sits between
+// items): L8 bench 112.6-112.8 K tokens/s vs 111.1 K for round 2's per-item paired kernel on the
+// same box, 32K 383 K vs 364 K, Qwen-14B 60.1 K vs 59.1 K (scripts/gpu/r2s2_persist2.sh).  The
+// paired 2-CTA kernel (multicast K/V, ~50 W less, one item per cluster) stays available:
+// APB_ATTN_PAIR=1 (every phase where it applies), APB_ATTN_PAIR=all (PHASE_ALL only, round 2's
+// default).
 static bool pair_enabled(int phase) {
   const char* e = std::getenv("APB_ATTN_PAIR");
-  if (e && e[0] == '0') return false;
   if (e && e[0] == '1') return true;
-  return phase == APB_PHASE_ALL;
+  if (e && e[0] == 'a') return phase == APB_PHASE_ALL;
+  return false;
 }
 
 template <int D, bool PAIR>

@@ -312,8 +312,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // retaining head (reading G2): a = SiLU(z + b1) for this item's hidden units
         // (BN, or BN/2 for a half-tile item), partial o[oc] = sum_h W2[oc][h] a_h in fp32 (fixed
         // order: chunks of 32 in column order, packed FFMA2 pairs) -> part[slot][row][oc] with one
-        // slot per BN/2 hidden units (a whole tile writes its sum to its first slot and zeros to the
-        // second); score_finalize_kernel sums the slots in order.  32 outputs per pass over TMEM.
+        // slot per BN/2 hidden units (a whole tile writes each half's sum to that half's slot, so
+        // the slots do not depend on the tiling); score_finalize_kernel sums the slots in order.
+        // 32 outputs per pass over TMEM.
         float* w2s = reinterpret_cast<float*>(smem + kOffW2);
         float* b1s = reinterpret_cast<float*>(smem + kOffB1);
         named_bar_sync(1, 128);  // the previous tile's readers of w2s / b1s are done
@@ -332,8 +333,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           float o[32];
 #pragma unroll
           for (int oc = 0; oc < 32; ++oc) o[oc] = 0.f;
+          float* part = p.part + host * p.part_stride;
 #pragma unroll 1
           for (int c = 0; c < (p.dbg == 1 ? 0 : bne); c += 32) {
+            if (c == BN / 2) {
+              // a whole tile writes its first BN/2 hidden units' sum to their own slot, as the half
+              // tile covering them would: the partial slots (and so the scores) do not depend on
+              // which tiles of a launch run as half tiles (per-host and multi-host launches agree)
+              if (row_ok) {
+                float* dst = part + ((int64_t)slot * p.M + row) * p.n_out + og;
+#pragma unroll
+                for (int oc = 0; oc < 32; ++oc)
+                  if (oc < no) dst[oc] = o[oc];
+              }
+#pragma unroll
+              for (int oc = 0; oc < 32; ++oc) o[oc] = 0.f;
+            }
             uint32_t zr[32];
             tmem_ld32(tacc + c, zr);
             tmem_wait_ld();
@@ -362,16 +377,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
-          if (row_ok) {
-            float* part = p.part + host * p.part_stride;
-            float* dst = part + ((int64_t)slot * p.M + row) * p.n_out + og;
-            float* dst2 = part + ((int64_t)(slot + 1) * p.M + row) * p.n_out + og;
+          if (row_ok) {  // the (second, for a whole tile) BN/2 hidden units' slot
+            float* dst = part + ((int64_t)(half < 0 ? slot + 1 : slot) * p.M + row) * p.n_out + og;
 #pragma unroll
             for (int oc = 0; oc < 32; ++oc)
-              if (oc < no) {
-                dst[oc] = o[oc];
-                if (half < 0) dst2[oc] = 0.f;
-              }
+              if (oc < no) dst[oc] = o[oc];
           }
         }
       } else if (p.epi == APB_EPI_SWIGLU) {

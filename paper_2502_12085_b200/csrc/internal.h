@@ -42,7 +42,7 @@ struct AttnParams {
   int64_t lse_ld;
   float* ws_o;                // [l_b][hq][D] fp32
   float* ws_lse;              // [hq][l_b] fp32, log2 domain
-  int dbg_skip;               // debug-only (env APB_DEBUG_SKIP): bit0 skip K loads, bit1 skip V loads, bit2 skip softmax (timing experiments)
+  int dbg_skip;               // unused (round-1 timing experiments; kept for the struct layout)
 };
 // Several hosts' attention in ONE launch (the hosts a rank owns, same phase): per-host tensor maps
 // and parameters in the kernel's parameter space (~4.4 KB, CUDA >= 12.1 large kernel parameters);

@@ -404,7 +404,7 @@ def run_attention_hosts(cfg, hs, xs, gathered_bits, phase):
 
 @pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa8-d128", "mha", "d128-sink", "lq"])
 @pytest.mark.parametrize("phase", ["all", "split"])
-@pytest.mark.parametrize("pair", ["", "0"])
+@pytest.mark.parametrize("pair", ["", "1"])
 def test_attention_hosts_equals_per_host(name, phase, pair, monkeypatch):
     """apb_attention_fwd_hosts (one launch over several hosts' items, heaviest host first) is
     bit-identical to one apb_attention_fwd call per host — every host, a strict subset in a
@@ -439,6 +439,56 @@ def test_attention_hosts_contract():
     with pytest.raises(apb.ApbError) as e:
         apb.attention_fwd_hosts(ds, q, k, v, dev(ref["gathered"]), out)
     assert e.value.status == apb.ERR_CONFIG
+
+
+@pytest.mark.parametrize("phase", ["all", "split"])
+def test_attention_persistent_steals_matches_paired(phase, monkeypatch):
+    """More work items than resident CTAs (host 1: 544 items, host 3: 576 over 148 SMs), so the
+    persistent kernel's CTAs take pending items from the launch (clusterlaunchcontrol) and run
+    several items each, with Q reloads, O hand-offs and barrier phases carried across items.  The
+    paired kernel runs one item per cluster; both feed the same tiles to the same MMAs in the same
+    order per item: bit-identical O and lse, in one launch per host and in one launch over hosts."""
+    cfg = synth.Config("steal", 21, n=4 * 8192, H=4, l_a=512, l_p=256, hq=16, hk=4, d=128, d_hidden=256)
+    hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)).astype(np.float32)
+    gathered = synth.f32_to_bf16_bits(g)
+    monkeypatch.setenv("APB_ATTN_PAIR", "1")
+    ref = {h: run_attention(cfg, h, hosts[h], gathered, phase) for h in (1, 3)}
+    monkeypatch.setenv("APB_ATTN_PAIR", "")
+    for h in (1, 3):
+        a = run_attention(cfg, h, hosts[h], gathered, phase)
+        assert np.array_equal(a[0], ref[h][0], equal_nan=True) and np.array_equal(a[1], ref[h][1], equal_nan=True), h
+    got = run_attention_hosts(cfg, [0, 1, 2, 3], hosts, gathered, phase)
+    for h in (1, 3):
+        assert np.array_equal(got[h][0], ref[h][0], equal_nan=True) and np.array_equal(got[h][1], ref[h][1],
+                                                                                         equal_nan=True), h
+    assert np.isfinite(got[0][0]).all() and np.isfinite(got[2][0]).all()
+
+
+@pytest.mark.parametrize("phase", ["all", "split"])
+def test_attention_persistent_d64_steals_vs_oracle(phase):
+    """d = 64 (never paired) with more items than resident CTAs (host 2: 272 items): the
+    persistent kernel against the fp64 oracle on 640 sampled rows (every 128-row tile boundary of
+    both segments +-1 included), per-host launch and one launch over every host."""
+    cfg = synth.Config("steal64", 22, n=4 * 4096, H=4, l_a=500, l_p=300, hq=16, hk=4, d=64, d_hidden=256)
+    hosts = [synth.host_qkv(cfg, 0, hh) for hh in range(cfg.H)]
+    g = np.random.default_rng(6).standard_normal((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)).astype(np.float32)
+    ref = {"gathered": synth.f32_to_bf16_bits(g)}
+    h = 2
+    x = hosts[h]
+    rng = np.random.default_rng(9)
+    rows = set()
+    for seg0, n in ((0, x["L_A"]), (x["L_A"], cfg.l_b)):
+        for b in range(0, n, 128):
+            rows.update(r for r in (seg0 + b - 1, seg0 + b, seg0 + b + 127) if seg0 <= r < seg0 + n)
+    rows = np.array(sorted(rows | set(rng.integers(0, x["L_A"] + cfg.l_b, 640 - len(rows)).tolist())))
+    pk, pv = oracle.passing(ref["gathered"], h)
+    O_or, lse_or = oracle.attention_blas(x["q"], x["k"], x["v"], x["L_A"], pk, pv, rows)
+    a = run_attention(cfg, h, x, ref["gathered"], phase)
+    b = run_attention_hosts(cfg, list(range(cfg.H)), hosts, ref["gathered"], phase)[h]
+    assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True)
+    check_attention(a[0][rows], a[1][rows], O_or, lse_or, f"steal64 host {h} {phase}")
 
 
 # ----------------------------------------------------------------------------- full size

@@ -74,14 +74,15 @@ def sample_rows(L_A, l_b, n_target, rng, tile_every=128):
     return np.array(sorted(r for r in rows if 0 <= r < n))
 
 
-def run_layer(cfg, hosts, w, split):
-    """One layer of the hot path for every host through PrefillRank, the bench's launch
-    configuration (ordered one-pass at N = 1, or the LOCAL / PASSING split)."""
+def run_layer(cfg, hosts, w, split, batched=False):
+    """One layer of the hot path for every host through PrefillRank: the bench's launch
+    configuration at N = 1 (batched: every host compressed, then one persistent attention launch
+    over all hosts' items), the round-2 ordered one-pass schedule, or the LOCAL / PASSING split."""
     from paper_2502_12085_b200 import apb
     from paper_2502_12085_b200.prefill import HostIO, PrefillRank
     base = apb.Dims(n=cfg.n, H=cfg.H, host=0, l_a=cfg.l_a, l_p=cfg.l_p, n_heads=cfg.hq, n_kv_heads=cfg.hk,
                     head_dim=cfg.d, l_q=cfg.l_q)
-    rank = PrefillRank(base, list(range(cfg.H)), split_phases=split)
+    rank = PrefillRank(base, list(range(cfg.H)), split_phases=split, batched=batched)
     io = {}
     for h in range(cfg.H):
         q = dev(hosts[h]["q"])
@@ -139,13 +140,13 @@ def check_attention_rows(cfg, hosts, gathered, outs, n_crit, n_other, rng, label
             assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN and lerr.max() <= LSE_TOL, msg
 
 
-def _full_protocol(cfg, n_crit, n_other, schedules=("ordered", "split")):
+def _full_protocol(cfg, n_crit, n_other, schedules=("batched", "ordered", "split")):
     hosts = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
     w = synth.retain_weights(cfg, 0)
     runs = []
     ref = None
     for sch in schedules:
-        rank, io = run_layer(cfg, hosts, w, split=(sch == "split"))
+        rank, io = run_layer(cfg, hosts, w, split=(sch == "split"), batched=(sch == "batched"))
         g = to_bits(rank.gathered)
         if ref is None:
             ref = (rank, g)
@@ -161,7 +162,7 @@ def _full_protocol(cfg, n_crit, n_other, schedules=("ordered", "split")):
 
 
 def test_llama8b_128k_full_protocol():
-    """The headline config, both schedules: every score, rules (i)/(ii) on every host, the
+    """The headline config in the bench's schedule and the two others: every score, rules (i)/(ii) on every host, the
     gathered buffer, 4096+ critical-host rows (all 160 tile boundaries +-1) and 1024+ rows of
     every other host."""
     _full_protocol(synth.CONFIGS["llama8b-128k"], n_crit=4096, n_other=1024)
@@ -169,13 +170,13 @@ def test_llama8b_128k_full_protocol():
 
 def test_llama8b_128k_d3_sink_needles():
     """The same layer under D3 (sink key + 16 needles x3 per block + shared query direction):
-    peaked scores and softmax rows at full size, ordered schedule."""
+    peaked scores and softmax rows at full size, the bench's (batched) schedule."""
     _full_protocol(synth.CONFIGS["llama8b-128k"].replace(dist="D3"), n_crit=1536, n_other=384,
-                   schedules=("ordered",))
+                   schedules=("batched",))
 
 
 def test_llama8b_32k_all_rows():
-    """BASELINE's 32K row (l_a = 1K, l_p = 512): EVERY query row of every host, both schedules."""
+    """BASELINE's 32K row (l_a = 1K, l_p = 512): EVERY query row of every host, all three schedules."""
     _full_protocol(synth.CONFIGS["llama8b-32k"], n_crit=1 << 30, n_other=1 << 30)
 
 
@@ -186,4 +187,4 @@ def test_other_configs_full_protocol(name, n_crit, n_other):
     d_in = 9216): every score of every host, selection rules (i) and (ii), the gathered buffer,
     and sampled attention rows (every 128-row tile boundary of the critical host included).  The
     512K / 1M rows' attention is checked by test_gpu.py::test_full_size_max_sampled."""
-    _full_protocol(synth.CONFIGS[name], n_crit=n_crit, n_other=n_other, schedules=("ordered",))
+    _full_protocol(synth.CONFIGS[name], n_crit=n_crit, n_other=n_other, schedules=("batched",))
