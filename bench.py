@@ -435,7 +435,7 @@ def main():
                     ", paired: 2-CTA clusters multicasting K/V"
                     if cfg.d == 128 and (os.environ.get("APB_ATTN_PAIR", "")[:1] == "1"
                                          or (os.environ.get("APB_ATTN_PAIR", "")[:1] == "a" and not pr.split_phases))
-                    else ", persistent: CTAs steal pending items (clusterlaunchcontrol)") + "> ("
+                    else ", persistent: one CTA per SM taking items from a work counter") + "> ("
                 + (("one LOCAL + one PASSING launch over the rank's hosts" if pr.batched
                     else "LOCAL + PASSING launches") if pr.split_phases
                    else ("one PHASE_ALL launch per layer over every host" if pr.batched

@@ -101,6 +101,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TRACE(slot, i) do {} while (0)
 #endif
 
+// Work counters of the persistent launches: slot [next item, CTAs done]; each launch takes the
+// next slot of the ring (host side), so launches in flight on different streams never share one,
+// and the launch's last CTA resets its slot for the launch that reuses it.
+constexpr int kCtrSlots = 64;
+__device__ unsigned int g_attn_ctr[kCtrSlots][2];
+
 template <int D>
 struct Layout {
   static constexpr int kHalves = D / 64;           // 64-element (128 B) swizzle atoms per row
@@ -221,13 +227,14 @@ __device__ __forceinline__ int visible_cols(const AttnParams& p, const Item& it,
 // commits).  Tiles past the prefix are loaded whole by the CTA that needs them and released by two
 // local commits.  A pair runs one item each (no work stealing).
 //
-// Persistent (single CTA): a CTA starts on item blockIdx.x, and when its TMA warp has issued the
-// last load of an item it asks the hardware for more work (clusterlaunchcontrol.try_cancel): a
-// CTA of this grid that has not launched yet is cancelled and its item runs here next.  Every role
-// reads the response at the end of its current item, so the next item's Q / K / V loads and first
-// S MMAs overlap the current item's last steps and epilogue, and no CTA launch, barrier set-up,
-// TMEM allocation or Q-load latency sits between items.  Items keep the launch order (heaviest
-// first): the stealing is dynamic, the last items go to whichever SMs free up first.
+// Persistent (single CTA, one per SM): a CTA starts on item blockIdx.x, and when its TMA warp has
+// issued the last load of an item it takes the next item from the launch's work counter
+// (atomicAdd; items in launch order, heaviest first, so the last items go to whichever SMs free up
+// first).  Every role reads the item id at the end of its current item, so the next item's
+// Q / K / V loads and first S MMAs overlap the current item's last steps and epilogue, and no CTA
+// launch, barrier set-up, TMEM allocation or Q-load latency sits between items.
+// (clusterlaunchcontrol.try_cancel work stealing was tried first: it hung when other work ran on
+// the GPU concurrently — the bench's end-to-end leg with its copy streams.)
 // Cross-item hazards: the Q tiles are reloaded after the previous item's last S MMA (Qfree), O_t
 // is overwritten by the next item's first PV_t only after the softmax warps have read it (Ofree),
 // the staging tile of O_t is rewritten only after its previous TMA store has read it.
@@ -308,23 +315,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.n_shared = PAIR ? min(c.it.nkv, decode_item(*c.p, c.w ^ 1).nkv) : 0;  // item_begin[] even
     return c;
   };
-  // next item: wait for the response of the k-th request (buffer k & 1), read it, -1 if none
+  // next item: wait for the k-th fetched item id (buffer k & 1), read it, -1 if none
   auto next_gid = [&](int k, bool reader) -> int {
     const int b = k & 1;
     mbar_wait_sleep(bW(b), (k >> 1) & 1);
-    uint32_t ok, x;
-    asm volatile(
-        "{\n\t.reg .b128 h;\n\t.reg .pred p;\n\t"
-        "ld.shared.b128 h, [%2];\n\t"
-        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, h;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t"
-        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, h;\n\t}"
-        : "=r"(ok), "=r"(x)
-        : "r"(sW(b))
-        : "memory");
+    const int x = *reinterpret_cast<volatile int*>(smem + L::kWork + 16 * b);
     __syncwarp();
     if (reader && (threadIdx.x & 31) == 0) mbar_arrive(bWf(b));
-    return ok ? static_cast<int>(x) : -1;
+    return x;
   };
 
   // Register split: the softmax warpgroups hold a 128-wide S row per thread; the producer / MMA
@@ -393,16 +391,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         n0 += 2 * it.nkv;
         if constexpr (PAIR) break;  // a pair runs one item each
-        // every load of this item is issued: ask for the next item (response buffer k & 1, free
-        // once the readers of request k - 2 have read it)
+        // every load of this item is issued: fetch the next item (buffer k & 1, free once the
+        // readers of fetch k - 2 have read it); the CTA that finds the list empty last resets the
+        // launch's counter slot
         mbar_wait_sleep(bWf(k & 1), ((k >> 1) & 1) ^ 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(bW(k & 1), 16);
-          asm volatile(
-              "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
-                  sW(k & 1)),
-              "r"(bW(k & 1))
-              : "memory");
+          unsigned int* ctr = g_attn_ctr[La.ctr_slot];
+          const int nxt = static_cast<int>(atomicAdd(ctr, 1u)) + static_cast<int>(gridDim.x);
+          const int total = La.item_begin[La.n];
+          *reinterpret_cast<volatile int*>(smem + L::kWork + 16 * (k & 1)) = nxt < total ? nxt : -1;
+          if (nxt >= total && atomicAdd(ctr + 1, 1u) + 1u == gridDim.x) {
+            ctr[0] = 0u;  // every CTA has taken its last id: the slot is free for a later launch
+            ctr[1] = 0u;
+            __threadfence();
+          }
+          mbar_arrive(bW(k & 1));  // release: the id is visible to the readers' acquire
         }
         __syncwarp();
         gid = next_gid(k, false);
@@ -766,9 +769,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Launch policy.  Default: the persistent single-CTA kernel for every phase (CTAs steal pending
-// items with clusterlaunchcontrol.try_cancel, so no launch / set-up / Q-load gap sits between
-// items): L8 bench 112.6-112.8 K tokens/s vs 111.1 K for round 2's per-item paired kernel on the
+// Launch policy.  Default: the persistent single-CTA kernel for every phase (one CTA per SM taking
+// items from a work counter, so no launch / set-up / Q-load gap sits between items): L8 bench 112.6-112.8 K tokens/s vs 111.1 K for round 2's per-item paired kernel on the
 // same box, 32K 383 K vs 364 K, Qwen-14B 60.1 K vs 59.1 K (scripts/gpu/r2s2_persist2.sh).  The
 // paired 2-CTA kernel (multicast K/V, ~50 W less, one item per cluster) stays available:
 // APB_ATTN_PAIR=1 (every phase where it applies), APB_ATTN_PAIR=all (PHASE_ALL only, round 2's
@@ -781,10 +783,20 @@ static bool pair_enabled(int phase) {
 }
 
 template <int D, bool PAIR>
-static apb_status launch_impl(const AttnLaunch& La, cudaStream_t stream) {
+static apb_status launch_impl(const AttnLaunch& La_in, cudaStream_t stream) {
   using L = Layout<D>;
-  const int grid = La.item_begin[La.n];
-  if (grid == 0) return APB_OK;
+  const int items = La_in.item_begin[La_in.n];
+  if (items == 0) return APB_OK;
+  AttnLaunch La = La_in;
+  int grid = items;  // PAIR: one item per CTA (clusters of 2)
+  if constexpr (!PAIR) {
+    static std::atomic<uint32_t> launches{0};
+    La.ctr_slot = static_cast<int>(launches.fetch_add(1) % kCtrSlots);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = items < sms ? items : sms;  // persistent: one CTA per SM, the rest from the counter
+  }
   static std::atomic<uint64_t> smem_set{0};
   if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(apb_attention_kernel<D, PAIR>), L::kAlloc, smem_set))
     return st;

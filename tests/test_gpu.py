@@ -443,9 +443,8 @@ def test_attention_hosts_contract():
 
 @pytest.mark.parametrize("phase", ["all", "split"])
 def test_attention_persistent_steals_matches_paired(phase, monkeypatch):
-    """More work items than resident CTAs (host 1: 544 items, host 3: 576 over 148 SMs), so the
-    persistent kernel's CTAs take pending items from the launch (clusterlaunchcontrol) and run
-    several items each, with Q reloads, O hand-offs and barrier phases carried across items.  The
+    """More work items than persistent CTAs (host 1: 544 items, host 3: 576 over 148 SMs), so the
+    persistent kernel's CTAs take items from the launch's work counter and run several items each, with Q reloads, O hand-offs and barrier phases carried across items.  The
     paired kernel runs one item per cluster; both feed the same tiles to the same MMAs in the same
     order per item: bit-identical O and lse, in one launch per host and in one launch over hosts."""
     cfg = synth.Config("steal", 21, n=4 * 8192, H=4, l_a=512, l_p=256, hq=16, hk=4, d=128, d_hidden=256)
