@@ -286,6 +286,14 @@ def workload_config(cfg, H, layers, n_gpus, variant=""):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+_T0 = time.time()
+
+
+def progress(msg):
+    """Phase marker on stderr (the JSON line stays the only stdout output)."""
+    print(f"bench [{time.time() - _T0:7.1f} s] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     if args.workload == "model":
@@ -392,9 +400,11 @@ def main():
             dist.barrier() if args.same_device else dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
+    progress("inputs ready")
     for _ in range(args.warmup):
         step()
     barrier()
+    progress("warmup done")
 
     # ---- timed region
     n_launch0 = apb.launch_count()
@@ -432,10 +442,12 @@ def main():
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
                 "kernel": "apb_attention_kernel<128" + (
-                    ", paired: 2-CTA clusters multicasting K/V"
-                    if cfg.d == 128 and (os.environ.get("APB_ATTN_PAIR", "")[:1] == "1"
-                                         or (os.environ.get("APB_ATTN_PAIR", "")[:1] == "a" and not pr.split_phases))
-                    else ", persistent: one CTA per SM taking items from a work counter") + "> ("
+                    ", persistent: one CTA per SM taking items from a work counter"
+                    if os.environ.get("APB_ATTN_PERSIST", "")[:1] == "1" and os.environ.get("APB_ATTN_PAIR", "")[:1] != "1"
+                    else ", paired: 2-CTA clusters multicasting K/V"
+                    if cfg.d == 128 and os.environ.get("APB_ATTN_PAIR", "")[:1] != "0"
+                    and (not pr.split_phases or os.environ.get("APB_ATTN_PAIR", "")[:1] == "1")
+                    else "") + "> ("
                 + (("one LOCAL + one PASSING launch over the rank's hosts" if pr.batched
                     else "LOCAL + PASSING launches") if pr.split_phases
                    else ("one PHASE_ALL launch per layer over every host" if pr.batched
@@ -446,19 +458,23 @@ def main():
                 "tile_efficiency": round(flops_rank / executed_rank, 4),
                 "attn_ms_per_step": round(attn_ms / args.steps, 3)}
 
+    progress("timed region done")
     # ---- per-op breakdown (one extra, untimed step with events around every libapb call)
     breakdown = None
     if not args.no_breakdown:
         breakdown = op_breakdown(pr, step, cfg, H, hosts, layers, world, peaks, barrier)
+        progress("breakdown done")
 
     # ---- end to end through the public API: pinned host inputs -> H2D every layer -> ... -> D2H
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, pr, sets, weights, layers, hosts, dev, world, local_rank, barrier)
+        progress("e2e done")
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:  # rank 0 only, at any N (the others wait below)
         cpu = cpu_baseline_line(cfg, H, layers)
+        progress("cpu baseline done")
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

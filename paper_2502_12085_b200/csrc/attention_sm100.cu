@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         n0 += 2 * it.nkv;
-        if constexpr (PAIR) break;  // a pair runs one item each
+        if (PAIR || !La.persist) break;  // one item per CTA (a pair runs one item each)
         // every load of this item is issued: fetch the next item (buffer k & 1, free once the
         // readers of fetch k - 2 have read it); the CTA that finds the list empty last resets the
         // launch's counter slot
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++oseq[t];
         }
         n0 += 2 * it.nkv;
-        if constexpr (PAIR) break;
+        if (PAIR || !La.persist) break;
         gid = next_gid(k, true);
         if (gid < 0) break;
       }
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if constexpr (PAIR) break;
+      if (PAIR || !La.persist) break;
       gid = next_gid(k, true);
       if (gid < 0) break;
     }
@@ -769,17 +769,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Launch policy.  Default: the persistent single-CTA kernel for every phase (one CTA per SM taking
-// items from a work counter, so no launch / set-up / Q-load gap sits between items): L8 bench 112.6-112.8 K tokens/s vs 111.1 K for round 2's per-item paired kernel on the
-// same box, 32K 383 K vs 364 K, Qwen-14B 60.1 K vs 59.1 K (scripts/gpu/r2s2_persist2.sh).  The
-// paired 2-CTA kernel (multicast K/V, ~50 W less, one item per cluster) stays available:
-// APB_ATTN_PAIR=1 (every phase where it applies), APB_ATTN_PAIR=all (PHASE_ALL only, round 2's
-// default).
+// Launch policy (round 2 default): the paired 2-CTA kernel (multicast K/V, ~50 W less) for the
+// one-pass PHASE_ALL launch where it applies, one item per cluster; the single-CTA kernel
+// otherwise.  APB_ATTN_PAIR=0: never paired; =1: every phase.  APB_ATTN_PERSIST=1 runs the
+// single-CTA kernel persistent (one CTA per SM, items from a work counter: L8 bench 112.2-112.8 K
+// vs 111.1 K tokens/s, 32K 383 K vs 364 K) — off by default: it hangs rarely (~1 % of L8
+// launches in a long bench run, not yet understood), see DESIGN.md §11.
 static bool pair_enabled(int phase) {
   const char* e = std::getenv("APB_ATTN_PAIR");
+  if (e && e[0] == '0') return false;
   if (e && e[0] == '1') return true;
-  if (e && e[0] == 'a') return phase == APB_PHASE_ALL;
-  return false;
+  if (const char* pe = std::getenv("APB_ATTN_PERSIST"); pe && pe[0] == '1') return false;
+  return phase == APB_PHASE_ALL;
 }
 
 template <int D, bool PAIR>
@@ -788,8 +789,11 @@ static apb_status launch_impl(const AttnLaunch& La_in, cudaStream_t stream) {
   const int items = La_in.item_begin[La_in.n];
   if (items == 0) return APB_OK;
   AttnLaunch La = La_in;
-  int grid = items;  // PAIR: one item per CTA (clusters of 2)
-  if constexpr (!PAIR) {
+  int grid = items;  // PAIR / not persistent: one item per CTA
+  La.persist = 0;
+  const char* pe = std::getenv("APB_ATTN_PERSIST");
+  if (!PAIR && pe && pe[0] == '1') {
+    La.persist = 1;
     static std::atomic<uint32_t> launches{0};
     La.ctr_slot = static_cast<int>(launches.fetch_add(1) % kCtrSlots);
     int dev = 0, sms = 148;

@@ -59,6 +59,7 @@ struct AttnLaunch {
   int item_begin[kAttnMaxHosts + 1];
   int n;
   int ctr_slot;  // persistent launches: this launch's work-counter slot (set by launch_attention_hosts)
+  int persist;   // 1: persistent CTAs take further items from the counter; 0: one item per CTA
 };
 // phase: the launch's phase for the pairing policy (a host without passing keys runs LOCAL as ALL)
 apb_status launch_attention_hosts(int D, const AttnLaunch& L, int phase, cudaStream_t stream);

@@ -404,7 +404,7 @@ def run_attention_hosts(cfg, hs, xs, gathered_bits, phase):
 
 @pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa8-d128", "mha", "d128-sink", "lq"])
 @pytest.mark.parametrize("phase", ["all", "split"])
-@pytest.mark.parametrize("pair", ["", "1"])
+@pytest.mark.parametrize("pair", ["", "0"])
 def test_attention_hosts_equals_per_host(name, phase, pair, monkeypatch):
     """apb_attention_fwd_hosts (one launch over several hosts' items, heaviest host first) is
     bit-identical to one apb_attention_fwd call per host — every host, a strict subset in a
@@ -454,7 +454,8 @@ def test_attention_persistent_steals_matches_paired(phase, monkeypatch):
     gathered = synth.f32_to_bf16_bits(g)
     monkeypatch.setenv("APB_ATTN_PAIR", "1")
     ref = {h: run_attention(cfg, h, hosts[h], gathered, phase) for h in (1, 3)}
-    monkeypatch.setenv("APB_ATTN_PAIR", "")
+    monkeypatch.setenv("APB_ATTN_PAIR", "0")
+    monkeypatch.setenv("APB_ATTN_PERSIST", "1")
     for h in (1, 3):
         a = run_attention(cfg, h, hosts[h], gathered, phase)
         assert np.array_equal(a[0], ref[h][0], equal_nan=True) and np.array_equal(a[1], ref[h][1], equal_nan=True), h
@@ -466,10 +467,11 @@ def test_attention_persistent_steals_matches_paired(phase, monkeypatch):
 
 
 @pytest.mark.parametrize("phase", ["all", "split"])
-def test_attention_persistent_d64_steals_vs_oracle(phase):
+def test_attention_persistent_d64_steals_vs_oracle(phase, monkeypatch):
     """d = 64 (never paired) with more items than resident CTAs (host 2: 272 items): the
     persistent kernel against the fp64 oracle on 640 sampled rows (every 128-row tile boundary of
     both segments +-1 included), per-host launch and one launch over every host."""
+    monkeypatch.setenv("APB_ATTN_PERSIST", "1")
     cfg = synth.Config("steal64", 22, n=4 * 4096, H=4, l_a=500, l_p=300, hq=16, hk=4, d=64, d_hidden=256)
     hosts = [synth.host_qkv(cfg, 0, hh) for hh in range(cfg.H)]
     g = np.random.default_rng(6).standard_normal((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)).astype(np.float32)
