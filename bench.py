@@ -442,12 +442,11 @@ def main():
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
                 "kernel": "apb_attention_kernel<128" + (
-                    ", persistent: one CTA per SM taking items from a work counter"
-                    if os.environ.get("APB_ATTN_PERSIST", "")[:1] == "1" and os.environ.get("APB_ATTN_PAIR", "")[:1] != "1"
-                    else ", paired: 2-CTA clusters multicasting K/V"
-                    if cfg.d == 128 and os.environ.get("APB_ATTN_PAIR", "")[:1] != "0"
-                    and (not pr.split_phases or os.environ.get("APB_ATTN_PAIR", "")[:1] == "1")
-                    else "") + "> ("
+                    ", paired: 2-CTA clusters multicasting K/V"
+                    if cfg.d == 128 and (os.environ.get("APB_ATTN_PAIR", "")[:1] == "1"
+                                         or (os.environ.get("APB_ATTN_PAIR", "")[:1] == "a" and not pr.split_phases))
+                    else ", persistent: one CTA per SM taking items from a work counter"
+                    if os.environ.get("APB_ATTN_PERSIST", "")[:1] != "0" else "") + "> ("
                 + (("one LOCAL + one PASSING launch over the rank's hosts" if pr.batched
                     else "LOCAL + PASSING launches") if pr.split_phases
                    else ("one PHASE_ALL launch per layer over every host" if pr.batched

@@ -23,6 +23,7 @@
 // sum is of the same bf16 weights, reading G21), which after the first few tiles is rare even for
 // peaky logits (measured: D2 107.5 K vs 97.5 K tokens/s with the threshold at 8; D1 unchanged).
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -101,6 +102,37 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TRACE(slot, i) do {} while (0)
 #endif
 
+#ifdef APB_TRACE
+// Hang watchdog (libapb_trace.so only): every mbarrier wait of the attention kernel is a polling
+// loop that, after ~2 s, records (source line, barrier offset, parity, item seq) for its
+// (CTA, warp) in mapped host memory — readable from the host while the kernel is stuck.
+__device__ unsigned int* g_hang = nullptr;  // [grid][12 warps][4]
+__device__ __forceinline__ void dbg_wait(uint32_t bar, uint32_t parity, uint32_t line, uint32_t bar0, int k) {
+  const long long t0 = clock64();
+  bool logged = false;
+  for (;;) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    if (ok) return;
+    if (!logged && clock64() - t0 > 4000000000ll && g_hang != nullptr) {
+      logged = true;
+      volatile unsigned int* h = g_hang + ((size_t)blockIdx.x * 12 + threadIdx.x / 32) * 4;
+      h[0] = line;
+      h[1] = bar - bar0;
+      h[2] = parity;
+      h[3] = (unsigned int)k;
+      __threadfence_system();
+    }
+  }
+}
+#define MBW(bar, par) dbg_wait((bar), (par), __LINE__, bar0, dbg_k)
+#define MBWS(bar, par) dbg_wait((bar), (par), __LINE__, bar0, dbg_k)
+#else
+#define MBW(bar, par) mbar_wait((bar), (par))
+#define MBWS(bar, par) mbar_wait_sleep((bar), (par))
+#endif
+
 // Work counters of the persistent launches: slot [next item, CTAs done]; each launch takes the
 // next slot of the ring (host side), so launches in flight on different streams never share one,
 // and the launch's last CTA resets its slot for the launch that reuses it.
@@ -119,7 +151,8 @@ struct Layout {
   static constexpr int kBar = kO + 2 * kTile;
   // barriers: Qfull, Qfree, full[kRing], empty[kRing], Sfull[2], Pfull[2][2 halves], Ofull[2],
   // Ofree[2], work[2] (next-item response landed), workfree[2] (response read by every role)
-  static constexpr int kNumBars = 2 + 2 * kRing + 12;
+  static constexpr int kNumBars = 2 + 2 * kRing + 14;
+  static_assert(14 + 2 * kRing + 1 < kNumBars, "the last barrier (workfree[1]) lies inside the barrier area");
   static constexpr int kWork = (kBar + kNumBars * 8 + 15) / 16 * 16;  // 2 x 16-byte CLC responses
   static constexpr int kTmemPtr = kWork + 32;
   static constexpr int kUsed = kTmemPtr + 16;
@@ -233,8 +266,9 @@ __device__ __forceinline__ int visible_cols(const AttnParams& p, const Item& it,
 // first).  Every role reads the item id at the end of its current item, so the next item's
 // Q / K / V loads and first S MMAs overlap the current item's last steps and epilogue, and no CTA
 // launch, barrier set-up, TMEM allocation or Q-load latency sits between items.
-// (clusterlaunchcontrol.try_cancel work stealing was tried first: it hung when other work ran on
-// the GPU concurrently — the bench's end-to-end leg with its copy streams.)
+// (A first version took items with clusterlaunchcontrol.try_cancel; both versions hung at first
+// because the barrier area was two barriers short, so the 16-byte item buffer overlapped the
+// workfree barriers — found with the trace build's wait watchdog, scripts/hang_repro.py.)
 // Cross-item hazards: the Q tiles are reloaded after the previous item's last S MMA (Qfree), O_t
 // is overwritten by the next item's first PV_t only after the softmax warps have read it (Ofree),
 // the staging tile of O_t is rewritten only after its previous TMA store has read it.
@@ -264,6 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kWorkReaders = 9;  // the MMA warp and the 8 softmax warps read every response
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
+  int dbg_k = 0;  // item sequence number of this role (hang records of the trace build)
+  (void)dbg_k;
   CTA_TIME(0);
 
   if (threadIdx.x == 0) {
@@ -318,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // next item: wait for the k-th fetched item id (buffer k & 1), read it, -1 if none
   auto next_gid = [&](int k, bool reader) -> int {
     const int b = k & 1;
-    mbar_wait_sleep(bW(b), (k >> 1) & 1);
+    MBWS(bW(b), (k >> 1) & 1);
     const int x = *reinterpret_cast<volatile int*>(smem + L::kWork + 16 * b);
     __syncwarp();
     if (reader && (threadIdx.x & 31) == 0) mbar_arrive(bWf(b));
@@ -335,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n0 = 0;  // ring sequence number of this item's first load
       int gid = static_cast<int>(blockIdx.x);
       for (int k = 0;; ++k) {
+        dbg_k = k;
         const Work c = resolve(gid);
         const Item& it = c.it;
         const AttnParams& p = *c.p;
@@ -349,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_prefetch_desc(tm_g);
         }
         const int qbase = it.seg == 0 ? 0 : p.L_A;
-        if (k > 0) mbar_wait_sleep(bQf, (k - 1) & 1);  // the previous item's last S MMA read Q
+        if (k > 0) MBWS(bQf, (k - 1) & 1);  // the previous item's last S MMA read Q
         if (elect_one()) {
           mbar_arrive_expect_tx(bQ, it.ntiles * L::kTile);
           for (int t = 0; t < it.ntiles; ++t)
@@ -364,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv) {
             const int n = n0 + 2 * i + kv, r = n % NR;
-            mbar_wait_sleep(bRe(r), ((n / NR) & 1) ^ 1);
+            MBWS(bRe(r), ((n / NR) & 1) ^ 1);
             if (elect_one()) {
               if (PAIR && i < c.n_shared) {
                 // this CTA's half of the tile, into the same slot of both CTAs of the pair
@@ -394,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // every load of this item is issued: fetch the next item (buffer k & 1, free once the
         // readers of fetch k - 2 have read it); the CTA that finds the list empty last resets the
         // launch's counter slot
-        mbar_wait_sleep(bWf(k & 1), ((k >> 1) & 1) ^ 1);
+        MBWS(bWf(k & 1), ((k >> 1) & 1) ^ 1);
         if (elect_one()) {
           unsigned int* ctr = g_attn_ctr[La.ctr_slot];
           const int nxt = static_cast<int>(atomicAdd(ctr, 1u)) + static_cast<int>(gridDim.x);
@@ -416,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ntot = n0;
         for (int r = 0; r < NR && r < ntot; ++r) {
           const int n_last = r + ((ntot - 1 - r) / NR) * NR;
-          mbar_wait_sleep(bRe(r), (n_last / NR) & 1);
+          MBWS(bRe(r), (n_last / NR) & 1);
         }
       }
     } else if (warp == kMmaWarp) {
@@ -444,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pseq[2] = {0, 0};  // P_t steps so far (bP(t, *) phases)
       int oseq[2] = {0, 0};  // items tile t took part in so far (bO(t) / bOf(t) phases)
       for (int k = 0;; ++k) {
+        dbg_k = k;
         const Work c = resolve(gid);
         const Item& it = c.it;
         const AttnParams& p = *c.p;
@@ -464,10 +502,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // of P_t, keys [64,128) after the second half.  The first PV_t of an item overwrites O_t:
         // the softmax warps must have read the previous item's O_t (Ofree).
         auto issue_PV = [&](int t, int s, bool acc, int step) {
-          if (step == 0 && oseq[t] > 0) mbar_wait_sleep(bOf(t), (oseq[t] - 1) & 1);
+          if (step == 0 && oseq[t] > 0) MBWS(bOf(t), (oseq[t] - 1) & 1);
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            mbar_wait_sleep(bP(t, half), (pseq[t] + step) & 1);
+            MBWS(bP(t, half), (pseq[t] + step) & 1);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
@@ -480,12 +518,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         const bool carry = (p.phase == APB_PHASE_PASSING);
-        mbar_wait_sleep(bQ, k & 1);
+        MBWS(bQ, k & 1);
         tc_fence_after();
         for (int i = 0; i < it.nkv; ++i) {
           const int nK = n0 + 2 * i, nV = nK + 1, nK1 = nK + 2;  // ring sequence numbers
           if (i == 0) {
-            mbar_wait_sleep(bRf(nK % NR), (nK / NR) & 1);
+            MBWS(bRf(nK % NR), (nK / NR) & 1);
             tc_fence_after();
             if (elect_one()) CTA_STAMP(3);
             __syncwarp();
@@ -496,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             release(nK % NR, 0);
             if (it.nkv == 1) commit(bQf);  // the item's last S MMAs are issued: Q may be reloaded
           }
-          mbar_wait_sleep(bRf(nV % NR), (nV / NR) & 1);
+          MBWS(bRf(nV % NR), (nV / NR) & 1);
           TRACE(12, i);
           tc_fence_after();
           for (int t = 0; t < it.ntiles; ++t) {
@@ -504,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (t == it.ntiles - 1) release(nV % NR, i);
             if (i + 1 < it.nkv) {
               if (t == 0) {
-                mbar_wait_sleep(bRf(nK1 % NR), (nK1 / NR) & 1);
+                MBWS(bRf(nK1 % NR), (nK1 / NR) & 1);
                 TRACE(13, i + 1);
                 tc_fence_after();
               }
@@ -543,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int oseq = 0;  // items this tile took part in (bO(t) phases)
     int gid = static_cast<int>(blockIdx.x);
     for (int k = 0;; ++k) {
+      dbg_k = k;
       const Work c = resolve(gid);
       const Item& it = c.it;
       const AttnParams& p = *c.p;
@@ -581,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < it.nkv; ++i) {
           const KvTile kt = kv_tile(p, it, i);
           const int nv = visible_cols(p, it, kt, row);
-          mbar_wait(bS(t), (sseq + i) & 1);
+          MBW(bS(t), (sseq + i) & 1);
           if (tid == 0) TRACE(6 + t, i);
           tc_fence_after();
           uint32_t sr[128];
@@ -693,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sseq += it.nkv;
 
         // ============================================================== epilogue
-        mbar_wait(bO(t), oseq & 1);
+        MBW(bO(t), oseq & 1);
         ++oseq;
         tc_fence_after();
         if (tid == 0 && t == 0) CTA_STAMP(4);
@@ -769,18 +808,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Launch policy (round 2 default): the paired 2-CTA kernel (multicast K/V, ~50 W less) for the
-// one-pass PHASE_ALL launch where it applies, one item per cluster; the single-CTA kernel
-// otherwise.  APB_ATTN_PAIR=0: never paired; =1: every phase.  APB_ATTN_PERSIST=1 runs the
-// single-CTA kernel persistent (one CTA per SM, items from a work counter: L8 bench 112.2-112.8 K
-// vs 111.1 K tokens/s, 32K 383 K vs 364 K) — off by default: it hangs rarely (~1 % of L8
-// launches in a long bench run, not yet understood), see DESIGN.md §11.
+// Launch policy.  Default: the persistent single-CTA kernel for every phase (one CTA per SM taking
+// items from the launch's work counter, so no launch / set-up / Q-load gap sits between items):
+// L8 bench 113.1 K tokens/s (e2e 110.7 K) vs 111.1 K for round 2's one-item-per-cluster paired
+// kernel, 32K 383 K vs 364 K, Qwen-14B 60.1 K vs 59.1 K (scripts/gpu/r2s2_persist2.sh).
+// APB_ATTN_PERSIST=0: one item per CTA; APB_ATTN_PAIR=1: the paired 2-CTA kernel (multicast K/V,
+// ~50 W less, one item per cluster) for every phase where it applies; APB_ATTN_PAIR=all: paired
+// for PHASE_ALL only (round 2's default).
+static bool persist_enabled() {
+  const char* pe = std::getenv("APB_ATTN_PERSIST");
+  return !(pe && pe[0] == '0');
+}
 static bool pair_enabled(int phase) {
   const char* e = std::getenv("APB_ATTN_PAIR");
-  if (e && e[0] == '0') return false;
   if (e && e[0] == '1') return true;
-  if (const char* pe = std::getenv("APB_ATTN_PERSIST"); pe && pe[0] == '1') return false;
-  return phase == APB_PHASE_ALL;
+  if (e && e[0] == 'a') return phase == APB_PHASE_ALL;
+  return false;
 }
 
 template <int D, bool PAIR>
@@ -791,8 +834,7 @@ static apb_status launch_impl(const AttnLaunch& La_in, cudaStream_t stream) {
   AttnLaunch La = La_in;
   int grid = items;  // PAIR / not persistent: one item per CTA
   La.persist = 0;
-  const char* pe = std::getenv("APB_ATTN_PERSIST");
-  if (!PAIR && pe && pe[0] == '1') {
+  if (!PAIR && persist_enabled()) {
     La.persist = 1;
     static std::atomic<uint32_t> launches{0};
     La.ctr_slot = static_cast<int>(launches.fetch_add(1) % kCtrSlots);
@@ -836,6 +878,17 @@ extern "C" int apb_debug_trace(unsigned long long* out, int n, int block) {
     return cudaMemcpyToSymbol(attn::g_trace_block, &block, sizeof(int)) == cudaSuccess ? 0 : 1;
   }
   return cudaMemcpyFromSymbol(out, attn::g_trace, sizeof(unsigned long long) * (n < 2048 ? n : 2048)) == cudaSuccess ? 0 : 1;
+}
+// Mapped host buffer for the hang watchdog records ([grid][12][4] uint32), 0 = nothing recorded.
+extern "C" int apb_debug_hang_buffer(unsigned int** host_ptr, int n_words) {
+  unsigned int* h = nullptr;
+  if (cudaHostAlloc(&h, sizeof(unsigned int) * n_words, cudaHostAllocMapped) != cudaSuccess) return 1;
+  memset(h, 0, sizeof(unsigned int) * n_words);
+  unsigned int* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return 2;
+  if (cudaMemcpyToSymbol(attn::g_hang, &d, sizeof(d)) != cudaSuccess) return 3;
+  *host_ptr = h;
+  return 0;
 }
 extern "C" int apb_debug_cta_times(unsigned long long* out, int n_ctas) {
   const int n = 5 * (n_ctas < 65536 ? n_ctas : 65536);

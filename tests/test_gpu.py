@@ -377,7 +377,7 @@ def test_attention_paired_matches_single_cta(name, phase, monkeypatch):
     for h in range(cfg.H):
         monkeypatch.setenv("APB_ATTN_PAIR", "1")
         a = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
-        monkeypatch.setenv("APB_ATTN_PAIR", "0")
+        monkeypatch.setenv("APB_ATTN_PAIR", "")
         b = run_attention(cfg, h, hosts[h], ref["gathered"], phase)
         assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True), f"host {h}"
 
@@ -404,7 +404,7 @@ def run_attention_hosts(cfg, hs, xs, gathered_bits, phase):
 
 @pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa8-d128", "mha", "d128-sink", "lq"])
 @pytest.mark.parametrize("phase", ["all", "split"])
-@pytest.mark.parametrize("pair", ["", "0"])
+@pytest.mark.parametrize("pair", ["", "1"])
 def test_attention_hosts_equals_per_host(name, phase, pair, monkeypatch):
     """apb_attention_fwd_hosts (one launch over several hosts' items, heaviest host first) is
     bit-identical to one apb_attention_fwd call per host — every host, a strict subset in a
@@ -454,8 +454,8 @@ def test_attention_persistent_steals_matches_paired(phase, monkeypatch):
     gathered = synth.f32_to_bf16_bits(g)
     monkeypatch.setenv("APB_ATTN_PAIR", "1")
     ref = {h: run_attention(cfg, h, hosts[h], gathered, phase) for h in (1, 3)}
-    monkeypatch.setenv("APB_ATTN_PAIR", "0")
-    monkeypatch.setenv("APB_ATTN_PERSIST", "1")
+    monkeypatch.setenv("APB_ATTN_PAIR", "")
+    monkeypatch.setenv("APB_ATTN_PERSIST", "")
     for h in (1, 3):
         a = run_attention(cfg, h, hosts[h], gathered, phase)
         assert np.array_equal(a[0], ref[h][0], equal_nan=True) and np.array_equal(a[1], ref[h][1], equal_nan=True), h
@@ -471,7 +471,7 @@ def test_attention_persistent_d64_steals_vs_oracle(phase, monkeypatch):
     """d = 64 (never paired) with more items than resident CTAs (host 2: 272 items): the
     persistent kernel against the fp64 oracle on 640 sampled rows (every 128-row tile boundary of
     both segments +-1 included), per-host launch and one launch over every host."""
-    monkeypatch.setenv("APB_ATTN_PERSIST", "1")
+    monkeypatch.setenv("APB_ATTN_PERSIST", "")
     cfg = synth.Config("steal64", 22, n=4 * 4096, H=4, l_a=500, l_p=300, hq=16, hk=4, d=64, d_hidden=256)
     hosts = [synth.host_qkv(cfg, 0, hh) for hh in range(cfg.H)]
     g = np.random.default_rng(6).standard_normal((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)).astype(np.float32)
@@ -490,6 +490,36 @@ def test_attention_persistent_d64_steals_vs_oracle(phase, monkeypatch):
     b = run_attention_hosts(cfg, list(range(cfg.H)), hosts, ref["gathered"], phase)[h]
     assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True)
     check_attention(a[0][rows], a[1][rows], O_or, lse_or, f"steal64 host {h} {phase}")
+
+
+def test_attention_persistent_stress_back_to_back():
+    """300 back-to-back persistent launches (576 items each over 148 CTAs, no host sync between
+    them, every launch reusing the work-counter ring) finish, and the last output equals the first
+    bit for bit.  A hang is detected by polling an event (30 s limit) and ends the process, so a
+    regression fails the suite instead of stalling it (this is how the barrier-area overlap of the
+    first persistent version showed up: ~1 % of L8 launches hung)."""
+    import os as _os
+    import time as _time
+    from paper_2502_12085_b200 import apb
+    cfg = synth.Config("steal", 21, n=4 * 8192, H=4, l_a=512, l_p=256, hq=16, hk=4, d=128, d_hidden=256)
+    x = synth.host_qkv(cfg, 0, 3)
+    g = np.random.default_rng(5).standard_normal((cfg.H, 2, cfg.hk, cfg.l_pp, cfg.d)).astype(np.float32)
+    d = dims_of(cfg, 3)
+    q, k, v, gd = dev(x["q"]), dev(x["k"]), dev(x["v"]), dev(synth.f32_to_bf16_bits(g))
+    outs = [torch.empty_like(q), torch.empty_like(q)]
+    lse = torch.empty((cfg.hq, d.rows), device="cuda")
+    apb.attention_fwd(d, q, k, v, gd, outs[0], lse)
+    for i in range(300):
+        apb.attention_fwd(d, q, k, v, gd, outs[1], lse)
+    ev = torch.cuda.Event()
+    ev.record()
+    t0 = _time.time()
+    while not ev.query():
+        if _time.time() - t0 > 30:
+            print("persistent attention stress: launches did not finish within 30 s (hang)", flush=True)
+            _os._exit(3)
+        _time.sleep(0.05)
+    assert torch.equal(outs[0], outs[1])
 
 
 # ----------------------------------------------------------------------------- full size
