@@ -104,7 +104,7 @@ typedef enum { APB_WS_RETAIN = 0, APB_WS_SELECT = 1, APB_WS_ATTENTION = 2 } apb_
  * Kernel: tcgen05 GEMM (A = [Q|K|V] rows via three TMA maps, B = W1) with a fused fp32
  * epilogue (b1, SiLU, W2 dot), then b2 and the group max.  Deterministic (no atomics).
  * ws: caller-owned device workspace of apb_retain_workspace_size() bytes (16-byte aligned;
- * fp32 partial W2 sums [d_hidden/128][l_b][n_out]: one slot per 128 hidden units).  With it the CTA-pair GEMM runs (each
+ * fp32 partial W2 sums [d_hidden/128][n_out][l_b]: one slot per 128 hidden units).  With it the CTA-pair GEMM runs (each
  * pair 256 tokens x 256 hidden units, the [Q|K|V] rows read from HBM about once); with ws ==
  * NULL (or too small) a single-CTA kernel (128 tokens x all of d_hidden) computes the same
  * definition in its own fixed summation order.  d_hidden % 256 == 0 and n_out <= 64, else

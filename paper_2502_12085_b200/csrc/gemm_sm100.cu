@@ -95,7 +95,7 @@ struct Params {
   int n_hosts, tiles_per_host;
   int a_row0[kGemmMaxHosts];
   int64_t part_stride;
-  // SCORE: partial[nb][row][n_out] = W2[:, nb*256 .. +256] SiLU(acc + b1[...])  (fp32)
+  // SCORE: partial[nb][n_out][row] = W2[:, nb*128 .. +128] SiLU(acc + b1[...])  (fp32)
   const float* b1;
   const float* w2;
   int n_out, d_hidden;
@@ -311,7 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (p.epi == kEpiScore) {
         // retaining head (reading G2): a = SiLU(z + b1) for this item's hidden units
         // (BN, or BN/2 for a half-tile item), partial o[oc] = sum_h W2[oc][h] a_h in fp32 (fixed
-        // order: chunks of 32 in column order, packed FFMA2 pairs) -> part[slot][row][oc] with one
+        // order: chunks of 32 in column order, packed FFMA2 pairs) -> part[slot][oc][row] with one
         // slot per BN/2 hidden units (a whole tile writes each half's sum to that half's slot, so
         // the slots do not depend on the tiling); score_finalize_kernel sums the slots in order.
         // 32 outputs per pass over TMEM.
@@ -341,10 +341,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               // tile covering them would: the partial slots (and so the scores) do not depend on
               // which tiles of a launch run as half tiles (per-host and multi-host launches agree)
               if (row_ok) {
-                float* dst = part + ((int64_t)slot * p.M + row) * p.n_out + og;
+                float* dst = part + ((int64_t)slot * p.n_out + og) * p.M + row;
 #pragma unroll
                 for (int oc = 0; oc < 32; ++oc)
-                  if (oc < no) dst[oc] = o[oc];
+                  if (oc < no) dst[(int64_t)oc * p.M] = o[oc];
               }
 #pragma unroll
               for (int oc = 0; oc < 32; ++oc) o[oc] = 0.f;
@@ -378,10 +378,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
           if (row_ok) {  // the (second, for a whole tile) BN/2 hidden units' slot
-            float* dst = part + ((int64_t)(half < 0 ? slot + 1 : slot) * p.M + row) * p.n_out + og;
+            float* dst = part + ((int64_t)(half < 0 ? slot + 1 : slot) * p.n_out + og) * p.M + row;
 #pragma unroll
             for (int oc = 0; oc < 32; ++oc)
-              if (oc < no) dst[oc] = o[oc];
+              if (oc < no) dst[(int64_t)oc * p.M] = o[oc];
           }
         }
       } else if (p.epi == APB_EPI_SWIGLU) {
@@ -548,27 +548,24 @@ __global__ void __launch_bounds__(128) score_finalize_kernel(const float* __rest
       m = -INFINITY;
     }
   };
-  if ((n_out & 3) == 0) {
-    for (int c4 = 0; c4 < n_out / 4; ++c4) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int nb = 0; nb < n_parts; ++nb) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(part + ((int64_t)nb * l_b + t) * n_out) + c4);
-        a.x += v.x;
-        a.y += v.y;
-        a.z += v.z;
-        a.w += v.w;
-      }
-      emit(4 * c4, a.x);
-      emit(4 * c4 + 1, a.y);
-      emit(4 * c4 + 2, a.z);
-      emit(4 * c4 + 3, a.w);
+  // partials [slot][oc][token]: consecutive threads (tokens) read consecutive words; 8 outputs x
+  // 4 slots of loads in flight per thread (each output still sums its slots in ascending order)
+  for (int oc0 = 0; oc0 < n_out; oc0 += 8) {
+    const int no = min(8, n_out - oc0);
+    float o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = 0.f;
+#pragma unroll 4
+    for (int nb = 0; nb < n_parts; ++nb) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = q < no ? __ldg(part + ((int64_t)nb * n_out + oc0 + q) * l_b + t) : 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] += v[q];
     }
-  } else {
-    for (int oc = 0; oc < n_out; ++oc) {
-      float o = 0.f;
-      for (int nb = 0; nb < n_parts; ++nb) o += __ldg(part + ((int64_t)nb * l_b + t) * n_out + oc);
-      emit(oc, o);
-    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < no) emit(oc0 + q, o[q]);
   }
 }
 

@@ -75,7 +75,7 @@ struct ScoreParams {
 };
 apb_status launch_retain_score(const ScoreParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, const CUtensorMap& tw1, cudaStream_t stream);
-// CTA-pair GEMM form (gemm_sm100.cu): partials [d_hidden/(BN/2)][l_b][n_out] in `part`, then a
+// CTA-pair GEMM form (gemm_sm100.cu): partials [d_hidden/(BN/2)][n_out][l_b] in `part`, then a
 // fixed-order finalize (tw1: box {64, BN/2}, tw1h: box {64, BN/4} for the half tiles of the last
 // wave; BN = score_tile_n())
 int score_tile_n();  // hidden units per scoring GEMM tile (128 or 256)
