@@ -138,6 +138,7 @@ __device__ __forceinline__ void dbg_wait(uint32_t bar, uint32_t parity, uint32_t
 // and the launch's last CTA resets its slot for the launch that reuses it.
 constexpr int kCtrSlots = 64;
 __device__ unsigned int g_attn_ctr[kCtrSlots][2];
+static std::atomic<uint32_t> g_launches{0};  // host: persistent launches so far (slot = count mod 64)
 
 template <int D>
 struct Layout {
@@ -295,7 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bWf = [&](int b) { return bar0 + 8u * (14 + 2 * NR + b); };
   auto sW = [&](int b) { return sbase + L::kWork + 16u * b; };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtr);
-  constexpr int kWorkReaders = 9;  // the MMA warp and the 8 softmax warps read every response
+  // readers of every fetched item id: the MMA warp and the 8 softmax warps; a persistent pair
+  // fetches once per cluster (the leader CTA's TMA warp) and both CTAs' readers — the peer's TMA
+  // warp included — report to the leader's workfree barrier
+  constexpr int kWorkReaders = PAIR ? 19 : 9;
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x / 32));
   int dbg_k = 0;  // item sequence number of this role (hang records of the trace build)
@@ -354,10 +358,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   // next item: wait for the k-th fetched item id (buffer k & 1), read it, -1 if none
   auto next_gid = [&](int k, bool reader) -> int {
     const int b = k & 1;
-    MBWS(bW(b), (k >> 1) & 1);
+    if constexpr (PAIR) {
+      // the leader stored the pair id into both CTAs and released it at cluster scope
+      mbar_wait_acq_cluster(bW(b), (k >> 1) & 1);
+    } else {
+      MBWS(bW(b), (k >> 1) & 1);
+    }
     const int x = *reinterpret_cast<volatile int*>(smem + L::kWork + 16 * b);
     __syncwarp();
-    if (reader && (threadIdx.x & 31) == 0) mbar_arrive(bWf(b));
+    if (reader && (threadIdx.x & 31) == 0) {
+      if constexpr (PAIR)
+        mbar_arrive_cluster(mapa_shared(bWf(b), 0));
+      else
+        mbar_arrive(bWf(b));
+    }
+    if constexpr (PAIR) return x < 0 ? -1 : 2 * x + static_cast<int>(cluster_ctarank());
     return x;
   };
 
@@ -427,25 +442,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         n0 += 2 * it.nkv;
-        if (PAIR || !La.persist) break;  // one item per CTA (a pair runs one item each)
+        if (!La.persist) break;  // one item per CTA (per cluster)
         // every load of this item is issued: fetch the next item (buffer k & 1, free once the
         // readers of fetch k - 2 have read it); the CTA that finds the list empty last resets the
-        // launch's counter slot
-        MBWS(bWf(k & 1), ((k >> 1) & 1) ^ 1);
-        if (elect_one()) {
-          unsigned int* ctr = g_attn_ctr[La.ctr_slot];
-          const int nxt = static_cast<int>(atomicAdd(ctr, 1u)) + static_cast<int>(gridDim.x);
-          const int total = La.item_begin[La.n];
-          *reinterpret_cast<volatile int*>(smem + L::kWork + 16 * (k & 1)) = nxt < total ? nxt : -1;
-          if (nxt >= total && atomicAdd(ctr + 1, 1u) + 1u == gridDim.x) {
-            ctr[0] = 0u;  // every CTA has taken its last id: the slot is free for a later launch
-            ctr[1] = 0u;
-            __threadfence();
+        // launch's counter slot.  A pair fetches a pair index once, in the leader, and stores it
+        // into both CTAs.
+        if (!PAIR || cluster_ctarank() == 0) {
+          if constexpr (PAIR)
+            mbar_wait_acq_cluster(bWf(k & 1), ((k >> 1) & 1) ^ 1);
+          else
+            MBWS(bWf(k & 1), ((k >> 1) & 1) ^ 1);
+          if (elect_one()) {
+            unsigned int* ctr = g_attn_ctr[La.ctr_slot];
+            const int units = PAIR ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+            const int total = PAIR ? La.item_begin[La.n] / 2 : La.item_begin[La.n];
+            const int nxt = static_cast<int>(atomicAdd(ctr, 1u)) + units;
+            const int id = nxt < total ? nxt : -1;
+            const uint32_t slot = sbase + L::kWork + 16u * (k & 1);
+            *reinterpret_cast<volatile int*>(smem + L::kWork + 16 * (k & 1)) = id;
+            if (nxt >= total && atomicAdd(ctr + 1, 1u) + 1u == static_cast<unsigned int>(units)) {
+              ctr[0] = 0u;  // every CTA (cluster) has taken its last id: the slot is free for a later launch
+              ctr[1] = 0u;
+              __threadfence();
+            }
+            if constexpr (PAIR) {
+              asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa_shared(slot, 1)), "r"(id) : "memory");
+              mbar_arrive_cluster(mapa_shared(bW(k & 1), 1));  // release at cluster scope
+              mbar_arrive_cluster(bW(k & 1));
+            } else {
+              mbar_arrive(bW(k & 1));  // release: the id is visible to the readers' acquire
+            }
           }
-          mbar_arrive(bW(k & 1));  // release: the id is visible to the readers' acquire
+          __syncwarp();
         }
-        __syncwarp();
-        gid = next_gid(k, false);
+        gid = next_gid(k, PAIR && cluster_ctarank() == 1);  // the peer's TMA warp is a reader
         if (gid < 0) break;
       }
       if constexpr (PAIR) {
@@ -562,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++oseq[t];
         }
         n0 += 2 * it.nkv;
-        if (PAIR || !La.persist) break;
+        if (!La.persist) break;
         gid = next_gid(k, true);
         if (gid < 0) break;
       }
@@ -791,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (PAIR || !La.persist) break;
+      if (!La.persist) break;
       gid = next_gid(k, true);
       if (gid < 0) break;
     }
@@ -832,16 +862,20 @@ static apb_status launch_impl(const AttnLaunch& La_in, cudaStream_t stream) {
   const int items = La_in.item_begin[La_in.n];
   if (items == 0) return APB_OK;
   AttnLaunch La = La_in;
-  int grid = items;  // PAIR / not persistent: one item per CTA
+  int grid = items;  // not persistent: one item per CTA
   La.persist = 0;
-  if (!PAIR && persist_enabled()) {
+  // a persistent pair needs equal partner walks for every item pair (its two rings advance
+  // together): g % 4 == 0, where both items of a pair cover the same row tile
+  bool equal_walks = true;
+  for (int i = 0; i < La.n; ++i) equal_walks = equal_walks && La.p[i].g % 4 == 0;
+  if (persist_enabled() && (!PAIR || equal_walks)) {
     La.persist = 1;
-    static std::atomic<uint32_t> launches{0};
-    La.ctr_slot = static_cast<int>(launches.fetch_add(1) % kCtrSlots);
+    La.ctr_slot = static_cast<int>(g_launches.fetch_add(1) % kCtrSlots);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = items < sms ? items : sms;  // persistent: one CTA per SM, the rest from the counter
+    if (PAIR) grid &= ~1;              // whole clusters (items is even for a paired launch)
   }
   static std::atomic<uint64_t> smem_set{0};
   if (apb_status st = set_max_smem_once(reinterpret_cast<const void*>(apb_attention_kernel<D, PAIR>), L::kAlloc, smem_set))
