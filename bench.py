@@ -446,6 +446,7 @@ def main():
                     if cfg.d == 128 and (os.environ.get("APB_ATTN_PAIR", "")[:1] == "1"
                                          or (os.environ.get("APB_ATTN_PAIR", "")[:1] == "a" and not pr.split_phases))
                     else ", persistent: one CTA per SM taking items from a work counter"
+                    + (" (LOCAL one item per CTA)" if pr.split_phases else "")
                     if os.environ.get("APB_ATTN_PERSIST", "")[:1] != "0" else "") + "> ("
                 + (("one LOCAL + one PASSING launch over the rank's hosts" if pr.batched
                     else "LOCAL + PASSING launches") if pr.split_phases

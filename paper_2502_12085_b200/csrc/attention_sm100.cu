@@ -842,12 +842,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // items from the launch's work counter, so no launch / set-up / Q-load gap sits between items):
 // L8 bench 113.1 K tokens/s (e2e 110.7 K) vs 111.1 K for round 2's one-item-per-cluster paired
 // kernel, 32K 383 K vs 364 K, Qwen-14B 60.1 K vs 59.1 K (scripts/gpu/r2s2_persist2.sh).
-// APB_ATTN_PERSIST=0: one item per CTA; APB_ATTN_PAIR=1: the paired 2-CTA kernel (multicast K/V,
+// APB_ATTN_PERSIST=0: one item per CTA everywhere, =1: persistent LOCAL too; APB_ATTN_PAIR=1: the paired 2-CTA kernel (multicast K/V,
 // ~50 W less, one item per cluster) for every phase where it applies; APB_ATTN_PAIR=all: paired
 // for PHASE_ALL only (round 2's default).
-static bool persist_enabled() {
+// The LOCAL launch of the split schedule (N > 1) stays one item per CTA by default: it overlaps
+// the side stream's scoring / selection / exchange, whose kernels get SMs as LOCAL's CTAs retire
+// (persistent CTAs would hold every SM until LOCAL ends and serialise the compression behind it).
+static bool persist_enabled(int phase) {
   const char* pe = std::getenv("APB_ATTN_PERSIST");
-  return !(pe && pe[0] == '0');
+  if (pe && pe[0] == '0') return false;
+  if (pe && pe[0] == '1') return true;
+  return phase != APB_PHASE_LOCAL;
 }
 static bool pair_enabled(int phase) {
   const char* e = std::getenv("APB_ATTN_PAIR");
@@ -857,7 +862,7 @@ static bool pair_enabled(int phase) {
 }
 
 template <int D, bool PAIR>
-static apb_status launch_impl(const AttnLaunch& La_in, cudaStream_t stream) {
+static apb_status launch_impl(const AttnLaunch& La_in, int phase, cudaStream_t stream) {
   using L = Layout<D>;
   const int items = La_in.item_begin[La_in.n];
   if (items == 0) return APB_OK;
@@ -868,7 +873,7 @@ static apb_status launch_impl(const AttnLaunch& La_in, cudaStream_t stream) {
   // together): g % 4 == 0, where both items of a pair cover the same row tile
   bool equal_walks = true;
   for (int i = 0; i < La.n; ++i) equal_walks = equal_walks && La.p[i].g % 4 == 0;
-  if (persist_enabled() && (!PAIR || equal_walks)) {
+  if (persist_enabled(phase) && (!PAIR || equal_walks)) {
     La.persist = 1;
     La.ctr_slot = static_cast<int>(g_launches.fetch_add(1) % kCtrSlots);
     int dev = 0, sms = 148;
@@ -943,10 +948,10 @@ apb_status launch_attention_hosts(int D, const AttnLaunch& La, int phase, cudaSt
     even_heads = even_heads && (p.n_local_items / p.hk) % 2 == 0 && (p.n_anchor_items / p.hk) % 2 == 0;
   }
   if (D == 128 && even_heads && attn::pair_enabled(phase))
-    return attn::launch_impl<128, true>(La, stream);
+    return attn::launch_impl<128, true>(La, phase, stream);
 #endif
-  if (D == 128) return attn::launch_impl<128, false>(La, stream);
-  if (D == 64) return attn::launch_impl<64, false>(La, stream);
+  if (D == 128) return attn::launch_impl<128, false>(La, phase, stream);
+  if (D == 64) return attn::launch_impl<64, false>(La, phase, stream);
   return fail(APB_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
 }
 
