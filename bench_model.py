@@ -97,7 +97,8 @@ def main(args=None):
         dist.broadcast_object_list(uid, src=0)
         comm = apb.Comm(uid[0], world, rank)
     shape = ModelShape(hidden=HIDDEN, inter=INTER, n_heads=cfg.hq, n_kv_heads=cfg.hk, head_dim=cfg.d)
-    model = ApbModelRank(base, shape, hosts, comm, dev, skip_unused_last=True)
+    model = ApbModelRank(base, shape, hosts, comm, dev, skip_unused_last=True,
+                         batched=getattr(args, "attn_launch", "batched") == "batched")
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(2502 * 12085 + 7 + rank)
