@@ -477,6 +477,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         gid = next_gid(k, PAIR && cluster_ctarank() == 1);  // the peer's TMA warp is a reader
         if (gid < 0) break;
+        {
+          // the next item's Q tiles into L2 now: they are loaded into shared memory only once
+          // this item's last S MMAs have read the current Q (Qfree), and then hit L2
+          const Work nc = resolve(gid);
+          const int nqb = nc.it.seg == 0 ? 0 : nc.p->L_A;
+          if (elect_one())
+            for (int t = 0; t < nc.it.ntiles; ++t)
+              for (int h = 0; h < L::kHalves; ++h)
+                tma_prefetch_3d(&La.tq[nc.hh], h * 64, nc.it.qht[t], nqb + nc.it.rtt[t] * BM);
+          __syncwarp();
+        }
       }
       if constexpr (PAIR) {
         // drain: every release of this CTA's slots (by both MMA warps) has landed before exit
