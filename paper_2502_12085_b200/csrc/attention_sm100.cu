@@ -49,10 +49,15 @@ constexpr int kMmaWarp = 9;
 #define APB_RESCALE_THRESHOLD 16.0f
 #endif
 constexpr float kRescaleThreshold = APB_RESCALE_THRESHOLD;
+// Of every 16 column pairs, this many are exponentiated on the FMA pipe (Cody-Waite + degree-3
+// polynomial) instead of MUFU.EX2: 4 of 32 pairs per half row.  Persistent kernel, L8 bench
+// (scripts/gpu/r2s2_variants.sh, same box): 0 -> 115.0 K, 1 -> 112.0 K, 2 -> 118.6 K, 3 -> 113.5 K,
+// 4 -> 115.5 K, 6 -> 106.9 K tokens/s.  (Round 1 measured 2 and 4 slower with the one-item-per-CTA
+// kernel; with the item gaps gone the MUFU pipe is the co-limiter and the offload pays.)
 #ifndef APB_POLY_PAIRS
-#define APB_POLY_PAIRS 0
+#define APB_POLY_PAIRS 2
 #endif
-constexpr int kPolyPairs = APB_POLY_PAIRS;  // of every 16 column pairs, evaluated with the FMA-pipe polynomial
+constexpr int kPolyPairs = APB_POLY_PAIRS;
 
 // 2^x for a pair of fp32 (x <= ~8): clamp at -126 (masked columns give ~0 denormals), split
 // x = j + f with j = rint(x) via the 1.5*2^23 magic constant, 2^f by a degree-3 minimax
