@@ -57,7 +57,13 @@ constexpr float kRescaleThreshold = APB_RESCALE_THRESHOLD;
 #ifndef APB_POLY_PAIRS
 #define APB_POLY_PAIRS 2
 #endif
-constexpr int kPolyPairs = APB_POLY_PAIRS;
+// which of the 16 pair positions (bit i: pair i of every 16) use the polynomial; default the first
+// APB_POLY_PAIRS positions (other placements of 2: 0x0101, 0x0011, 0xC000 measured equal or up to
+// 1 % slower, 0x0300 3 % slower)
+#ifndef APB_POLY_MASK
+#define APB_POLY_MASK ((1u << APB_POLY_PAIRS) - 1u)
+#endif
+constexpr uint32_t kPolyMask = APB_POLY_MASK;
 
 // 2^x for a pair of fp32 (x <= ~8): clamp at -126 (masked columns give ~0 denormals), split
 // x = j + f with j = rint(x) via the 1.5*2^23 magic constant, 2^f by a degree-3 minimax
@@ -683,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (cc >= nv) s[cc] = -INFINITY;
           }
           // 2^(s*scale*log2e - m) for the 64 columns of one half; packed FFMA2 for the argument;
-          // kPolyPairs of every 16 column pairs on the FMA pipe (Cody-Waite + degree-3 polynomial,
+          // the kPolyMask pairs of every 16 on the FMA pipe (Cody-Waite + degree-3 polynomial,
           // rel. error 7.5e-5 << bf16's 3.9e-3), the rest on MUFU.EX2.
           auto exp_half = [&](int half, float m_use, uint32_t (&pk)[32], uint64_t (&acc2)[4]) {
             const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_use, -m_use);
@@ -692,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int col = half * 64 + 2 * cc;
               const uint64_t x2 = ffma2(f2_pack(s[col], s[col + 1]), sc2, nm2);
               float p0, p1;
-              if ((cc % 16) < kPolyPairs) {
+              if ((kPolyMask >> (cc % 16)) & 1u) {
                 const uint64_t p2 = exp2_poly2(x2);
                 f2_unpack(p2, p0, p1);
               } else {
