@@ -64,6 +64,10 @@ constexpr float kRescaleThreshold = APB_RESCALE_THRESHOLD;
 #define APB_POLY_MASK ((1u << APB_POLY_PAIRS) - 1u)
 #endif
 constexpr uint32_t kPolyMask = APB_POLY_MASK;
+#ifndef APB_POLY_MASK1
+#define APB_POLY_MASK1 APB_POLY_MASK
+#endif
+constexpr uint32_t kPolyMask1 = APB_POLY_MASK1;  // the second half row's positions (default: the same)
 
 // 2^x for a pair of fp32 (x <= ~8): clamp at -126 (masked columns give ~0 denormals), split
 // x = j + f with j = rint(x) via the 1.5*2^23 magic constant, 2^f by a degree-3 minimax
@@ -698,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int col = half * 64 + 2 * cc;
               const uint64_t x2 = ffma2(f2_pack(s[col], s[col + 1]), sc2, nm2);
               float p0, p1;
-              if ((kPolyMask >> (cc % 16)) & 1u) {
+              if ((((half == 0) ? kPolyMask : kPolyMask1) >> (cc % 16)) & 1u) {
                 const uint64_t p2 = exp2_poly2(x2);
                 f2_unpack(p2, p0, p1);
               } else {
