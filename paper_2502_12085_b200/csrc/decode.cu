@@ -310,17 +310,19 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
 }
 
 // LSE merge of n partials per row (MergeScore).  lse_in_log2 selects the input log base;
-// the output lse is natural.  One CTA (8 warps) per row: the weights of all parts are formed once
-// in shared memory (parallel max / sum); warp w accumulates parts w, w+8, ... (lanes across
-// head_dim, coalesced), and the 8 warp partials are added in a fixed order — deterministic.
+// the output lse is natural.  One CTA (8 warps) per (row, block of 32 columns) — a CTA handles
+// column blocks [cb0, cb0 + NCB): the weights of all parts are formed in shared memory (parallel
+// max / sum, recomputed by each column block); warp w accumulates parts w, w+8, ... (lanes across
+// the columns, 8 parts' loads in flight), and the 8 warp partials are added in a fixed order —
+// deterministic, and the same bits whichever column split runs it.
 constexpr int kMergeWarps = 8;
-template <int D, typename OutT>
-__device__ __forceinline__ void merge_row(int64_t row, int n, const float* __restrict__ parts_o,
+template <int D, typename OutT, int NCB>
+__device__ __forceinline__ void merge_row(int64_t row, int cb0, int n, const float* __restrict__ parts_o,
                                           const float* __restrict__ parts_lse, int64_t stride_o, int64_t stride_lse,
                                           int lse_in_log2, OutT* __restrict__ out, float* __restrict__ out_lse) {
   extern __shared__ float wsm[];  // [n] weights
   __shared__ float red[kMergeWarps];
-  __shared__ float part[kMergeWarps][D];
+  __shared__ float part[kMergeWarps][NCB * 32];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const float to2 = lse_in_log2 ? 1.f : 1.4426950408889634f;  // convert to the log2 domain
   float m = -INFINITY;
@@ -350,47 +352,49 @@ __device__ __forceinline__ void merge_row(int64_t row, int n, const float* __res
   z = 0.f;
 #pragma unroll
   for (int w = 0; w < kMergeWarps; ++w) z += red[w];
-  constexpr int kPer = D / 32;
-  float acc[kPer];
+  float acc[NCB];
 #pragma unroll
-  for (int e = 0; e < kPer; ++e) acc[e] = 0.f;
+  for (int e = 0; e < NCB; ++e) acc[e] = 0.f;
+  const int col0 = cb0 * 32 + lane;
   int h = warp;
-  // four parts' loads in flight per warp, accumulated in the same (part-ascending) order
-  for (; h + 3 * kMergeWarps < n; h += 4 * kMergeWarps) {
-    float v[4][kPer];
+  // eight parts' loads in flight per warp, accumulated in the same (part-ascending) order
+  constexpr int kU = NCB >= 4 ? 4 : 8;
+  for (; h + (kU - 1) * kMergeWarps < n; h += kU * kMergeWarps) {
+    float v[kU][NCB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float* src = parts_o + (h + u * kMergeWarps) * stride_o + row * D;
+    for (int u = 0; u < kU; ++u) {
+      const float* src = parts_o + (h + u * kMergeWarps) * stride_o + row * D + col0;
 #pragma unroll
-      for (int e = 0; e < kPer; ++e) v[u][e] = __ldg(src + e * 32 + lane);
+      for (int e = 0; e < NCB; ++e) v[u][e] = __ldg(src + e * 32);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const float w = wsm[h + u * kMergeWarps];
 #pragma unroll
-      for (int e = 0; e < kPer; ++e) acc[e] = fmaf(w, v[u][e], acc[e]);
+      for (int e = 0; e < NCB; ++e) acc[e] = fmaf(w, v[u][e], acc[e]);
     }
   }
   for (; h < n; h += kMergeWarps) {
     const float w = wsm[h];
-    const float* src = parts_o + h * stride_o + row * D;
+    const float* src = parts_o + h * stride_o + row * D + col0;
 #pragma unroll
-    for (int e = 0; e < kPer; ++e) acc[e] = fmaf(w, __ldg(src + e * 32 + lane), acc[e]);
+    for (int e = 0; e < NCB; ++e) acc[e] = fmaf(w, __ldg(src + e * 32), acc[e]);
   }
 #pragma unroll
-  for (int e = 0; e < kPer; ++e) part[warp][e * 32 + lane] = acc[e];
+  for (int e = 0; e < NCB; ++e) part[warp][e * 32 + lane] = acc[e];
   __syncthreads();
-  for (int e = tid; e < D; e += kMergeWarps * 32) {
+  for (int e = tid; e < NCB * 32; e += kMergeWarps * 32) {
     float sum = 0.f;
 #pragma unroll
     for (int w = 0; w < kMergeWarps; ++w) sum += part[w][e];
     const float o = z > 0.f ? sum / z : 0.f;
     if constexpr (sizeof(OutT) == 2)
-      out[row * D + e] = __float2bfloat16_rn(o);
+      out[row * D + cb0 * 32 + e] = __float2bfloat16_rn(o);
     else
-      out[row * D + e] = o;
+      out[row * D + cb0 * 32 + e] = o;
   }
-  if (tid == 0 && out_lse) out_lse[row] = (z > 0.f) ? (m + __log2f(z)) * 0.69314718055994530942f : -INFINITY;
+  if (tid == 0 && cb0 == 0 && out_lse)
+    out_lse[row] = (z > 0.f) ? (m + __log2f(z)) * 0.69314718055994530942f : -INFINITY;
 }
 
 template <int D, typename OutT>
@@ -399,7 +403,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(int n, int64_t 
                                                                  int64_t stride_lse, int lse_in_log2,
                                                                  OutT* __restrict__ out, float* __restrict__ out_lse) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched with PDL
-  merge_row<D, OutT>(blockIdx.x, n, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, out, out_lse);
+  // grid (rows, D / 32): one column block per CTA
+  merge_row<D, OutT, 1>(blockIdx.x, blockIdx.y, n, parts_o, parts_lse, stride_o, stride_lse, lse_in_log2, out, out_lse);
 }
 
 // Fold of a multi-host launch: CTA (row, host i) merges host i's splits (log2 lse in the
@@ -413,7 +418,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fold_hosts_kernel(const Deco
   asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched with PDL
   const int i = blockIdx.y, s0 = hb.split_begin[i];
   float* dst = parts + (int64_t)i * part_stride;
-  merge_row<D, float>(blockIdx.x, hb.split_begin[i + 1] - s0, ws_o + (int64_t)s0 * rows * D, ws_lse + (int64_t)s0 * rows,
+  merge_row<D, float, D / 32>(blockIdx.x, 0, hb.split_begin[i + 1] - s0, ws_o + (int64_t)s0 * rows * D, ws_lse + (int64_t)s0 * rows,
                       rows * D, rows, 1, dst, dst + lse_offset);
 }
 
@@ -586,7 +591,8 @@ apb_status launch_merge(int n, int64_t rows, int D, const float* parts_o, const 
                         int64_t stride_lse, int lse_in_log2, void* out, bool out_bf16, float* out_lse,
                         cudaStream_t stream, bool pdl) {
   if (rows == 0) return APB_OK;
-  cudaLaunchConfig_t cfg = pdl_config(dim3((unsigned)rows), dec::kMergeWarps * 32, (size_t)n * sizeof(float), stream, pdl);
+  cudaLaunchConfig_t cfg = pdl_config(dim3((unsigned)rows, (unsigned)(D / 32)), dec::kMergeWarps * 32,
+                                       (size_t)n * sizeof(float), stream, pdl);
   cudaLaunchAttribute attr = pdl_attr();
   cfg.attrs = &attr;
   __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(out);
