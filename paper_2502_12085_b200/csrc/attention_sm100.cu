@@ -631,8 +631,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_base + t * 128;
     const uint32_t tO = tmem + lane_base + 256 + t * D;
-    const float* no_p = nullptr;
-    (void)no_p;
     int sseq = 0;  // S_t steps so far (bS(t) phases)
     int oseq = 0;  // items this tile took part in (bO(t) phases)
     int gid = static_cast<int>(blockIdx.x);
