@@ -10,6 +10,8 @@
 // partial (O, log2-sum-exp) per split in the workspace.
 // merge_kernel: log-sum-exp merge of n partials per row — used both to fold the chunks of one
 // host and, across hosts, as MergeScore.  Fixed merge order, no atomics: deterministic.
+#include <cstdlib>
+
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -34,7 +36,7 @@ constexpr int kSplitTarget = APB_DEC_CTAS_PER_SM * 148;  // CTAs per launch to a
 // CTAs than fit at once; per L8 step: 3 x 148 0.148 ms, 4 x 0.142, 5 x 0.132, 6 x 0.124, 8 x 0.124,
 // 12 x 0.133 ms).
 #ifndef APB_DEC_HOSTS_CTAS_PER_SM
-#define APB_DEC_HOSTS_CTAS_PER_SM 6
+#define APB_DEC_HOSTS_CTAS_PER_SM 9
 #endif
 constexpr int kHostsSplitTarget = APB_DEC_HOSTS_CTAS_PER_SM * 148;
 
@@ -61,10 +63,24 @@ struct MmaSmem {
   static constexpr int kKV = D * 2;                   // K / V chunk row: dense, 16-byte chunks XOR-swizzled
   static constexpr int kStage = 2 * MKC * kKV;        // K and V chunk
   static constexpr int kPRow = MKC + 8;
-  static constexpr int bytes(int MT) {
-    return kMStages * kStage + 16 * MT * kRow * 2 + 16 * MT * kPRow * 2 + 2 * 8 * 16 * MT * 4;
+  __host__ __device__ static constexpr int bytes(int MT, int stages = kMStages) {
+    return stages * kStage + 16 * MT * kRow * 2 + 16 * MT * kPRow * 2 + 2 * 8 * 16 * MT * 4;
   }
 };
+// TMA-fed variant: the K / V chunks arrive by cp.async.bulk.tensor (one elected thread issues two
+// 64-column SW128 boxes per tensor per chunk) into a 3-stage ring with one mbarrier per stage;
+// the tensor maps of every host of the launch sit in the parameter space.
+#ifndef APB_DEC_TSTAGES
+#define APB_DEC_TSTAGES 2
+#endif
+constexpr int kTStages = APB_DEC_TSTAGES;
+struct DecMaps {
+  CUtensorMap k[kDecMaxHosts], v[kDecMaxHosts];
+};
+template <int D>
+__host__ __device__ constexpr int tma_bytes(int MT) {  // + the stage barriers + slack to align the ring at 1 KB
+  return MmaSmem<D>::bytes(MT, kTStages) + 8 * kTStages + 1024;
+}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -87,19 +103,33 @@ template <int D>
 __device__ __forceinline__ uint32_t kv_off(int r, int c) {
   return static_cast<uint32_t>(r * (D * 2) + ((c ^ (r & 7)) << 4));
 }
+// the TMA (SW128) layout of a chunk: 64-column halves of [64 keys][128 B], 16-byte chunk index
+// XOR (r & 7) inside each 128-byte row (the same bank spread for ldmatrix)
+template <int D, bool TMA>
+__device__ __forceinline__ uint32_t kv_addr(int r, int c) {
+  if constexpr (TMA)
+    return static_cast<uint32_t>((c >> 3) * (SKC * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+  else
+    return kv_off<D>(r, c);
+}
 
-template <int D, int MT>
+template <int D, int MT, bool TMA>
 __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParams p, const DecodeHosts hb,
-                                                                 int chunks_per_split) {
+                                                                 int chunks_per_split,
+                                                                 const __grid_constant__ DecMaps maps) {
   using L = MmaSmem<D>;
-  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int kS = TMA ? kTStages : kMStages;  // ring stages
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // the TMA ring is 1 KB aligned (SW128 boxes); the cp.async ring needs 16 B
+  uint8_t* smem = TMA ? smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u)
+                      : smem_raw;
   constexpr int NT = D / 64;  // O n-tiles (of 8 columns) per warp: D/8 tiles over 8 warps
   // programmatic dependent launch: the merge / fold that follows may be scheduled as soon as every
   // CTA of this grid has started (it waits in griddepcontrol.wait for this grid's completion and
   // memory flush), so its launch latency and ramp overlap this grid's tail
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int R = p.t * p.g;
-  __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(smem + kMStages * L::kStage);  // [16 MT][kRow]
+  __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(smem + kS * L::kStage);  // [16 MT][kRow]
   __nv_bfloat16* pss = qs + 16 * MT * L::kRow;                                       // [16 MT][kPRow]
   float* xm = reinterpret_cast<float*>(pss + 16 * MT * L::kPRow);                    // [8][16 MT]
   float* xl = xm + 8 * 16 * MT;                                                      // [8][16 MT]
@@ -112,9 +142,11 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
   const __nv_bfloat16* v_cache = p.v_cache;
   int64_t cache_len = p.cache_len;
   int has_new = p.has_new;
+  int hi = 0;  // this split's host within the launch (its tensor maps)
   if (hb.n > 0) {
     int i = 0;
     while (i + 1 < hb.n && split >= hb.split_begin[i + 1]) ++i;
+    hi = i;
     split_local = split - hb.split_begin[i];
     k_cache = hb.k_cache[i];
     v_cache = hb.v_cache[i];
@@ -129,11 +161,37 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
   constexpr int kVec = D / 8;
   auto stage_k = [&](int s) { return smem + s * L::kStage; };
   auto stage_v = [&](int s) { return smem + s * L::kStage + MKC * L::kKV; };
+  // TMA: one barrier per stage after the Q / P / x scratch
+  const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem + L::bytes(MT, kS)));
+  if constexpr (TMA) {
+    if (tid == 0) {
+      for (int st = 0; st < kS; ++st) mbar_init(bar0 + 8u * st, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   auto load_chunk = [&](int c, int s) {
     const int64_t k0 = (c_first + c) * MKC;
     uint8_t* ks = stage_k(s);
     uint8_t* vs = stage_v(s);
-    for (int idx = tid; idx < MKC * kVec; idx += kMThreads) {
+    if constexpr (TMA) {
+      // the slot's previous chunk was read before the last __syncthreads; order those generic
+      // reads before the async-proxy writes, then two SW128 boxes per tensor (rows past the
+      // cache are zero-filled; the new tokens' rows are patched in after the wait)
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t fb = bar0 + 8u * s;
+        mbar_arrive_expect_tx(fb, 2 * MKC * D * 2);
+        const uint32_t ku = static_cast<uint32_t>(__cvta_generic_to_shared(ks));
+        const uint32_t vu = static_cast<uint32_t>(__cvta_generic_to_shared(vs));
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h) {
+          tma_load_3d(ku + h * (MKC * 128), &maps.k[hi], fb, h * 64, j, (int)k0);
+          tma_load_3d(vu + h * (MKC * 128), &maps.v[hi], fb, h * 64, j, (int)k0);
+        }
+      }
+    } else {
+      for (int idx = tid; idx < MKC * kVec; idx += kMThreads) {
       const int kk = idx / kVec, cv = idx % kVec;
       const int64_t key = k0 + kk;
       const bool cached = key < cache_len, valid = key < n_keys;
@@ -143,6 +201,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
                                        : p.v_new + (key - cache_len) * p.new_row_stride;
       cp_async16(ks + kv_off<D>(kk, cv), valid ? kb + (int64_t)j * D + cv * 8 : p.q, valid);
       cp_async16(vs + kv_off<D>(kk, cv), valid ? vb + (int64_t)j * D + cv * 8 : p.q, valid);
+      }
     }
   };
   // queries as bf16 rows (16-byte async copies; rows >= R zero-filled), in the first group
@@ -152,7 +211,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
     cp_async16(qs + r * L::kRow + cv * 8, r < R ? p.q + ((int64_t)sr * p.hq + qh) * D + cv * 8 : p.q, r < R);
   }
 #pragma unroll
-  for (int s = 0; s < kMStages - 1; ++s) {
+  for (int s = 0; s < kS - 1; ++s) {
     if (s < nch) load_chunk(s, s);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
@@ -171,12 +230,29 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
   const float sl2 = p.scale_log2;
 
   for (int c = 0; c < nch; ++c) {
-    const int s = c % kMStages;
-    if (c + kMStages - 1 < nch) load_chunk(c + kMStages - 1, (c + kMStages - 1) % kMStages);
+    const int s = c % kS;
+    if (c + kS - 1 < nch) load_chunk(c + kS - 1, (c + kS - 1) % kS);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group %0;" ::"n"(kMStages - 1) : "memory");
-    __syncthreads();
     const int64_t k0 = (c_first + c) * MKC;
+    if constexpr (TMA) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(kS - 1) : "memory");  // the queries (first group)
+      mbar_wait(bar0 + 8u * s, (c / kS) & 1);
+      if (has_new && k0 + MKC > cache_len) {
+        // the new tokens' own keys (last host) into their rows of the chunk
+        for (int idx = tid; idx < MKC * kVec; idx += kMThreads) {
+          const int kk = idx / kVec, cv = idx % kVec;
+          const int64_t key = k0 + kk;
+          if (key >= cache_len && key < n_keys) {
+            const int64_t nr = (key - cache_len) * p.new_row_stride + (int64_t)j * D + cv * 8;
+            *reinterpret_cast<uint4*>(stage_k(s) + kv_addr<D, true>(kk, cv)) = *reinterpret_cast<const uint4*>(p.k_new + nr);
+            *reinterpret_cast<uint4*>(stage_v(s) + kv_addr<D, true>(kk, cv)) = *reinterpret_cast<const uint4*>(p.v_new + nr);
+          }
+        }
+      }
+    } else {
+      asm volatile("cp.async.wait_group %0;" ::"n"(kS - 1) : "memory");
+    }
+    __syncthreads();
     const uint32_t ks_u = static_cast<uint32_t>(__cvta_generic_to_shared(stage_k(s)));
     const uint32_t vs_u = static_cast<uint32_t>(__cvta_generic_to_shared(stage_v(s)));
     // ---- S = Q K^T for this warp's 8 keys
@@ -188,7 +264,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
 #pragma unroll
     for (int kb = 0; kb < D / 32; ++kb) {  // two k-steps of 16 per ldmatrix.x4 of K
       uint32_t b[4];
-      ldsm_x4(ks_u + kv_off<D>(warp * 8 + (lane % 8), kb * 4 + lane / 8), b[0], b[1], b[2], b[3]);
+      ldsm_x4(ks_u + kv_addr<D, TMA>(warp * 8 + (lane % 8), kb * 4 + lane / 8), b[0], b[1], b[2], b[3]);
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         uint32_t a[4], a2[4];
@@ -259,7 +335,7 @@ __global__ void __launch_bounds__(kMThreads) decode_mma_kernel(const DecodeParam
       for (int np = 0; np < NT; np += 2) {  // pairs of n-tiles per ldmatrix.x4.trans
         uint32_t b[4];
         const int col = warp * (D / 8) + np * 8 + (lane / 16) * 8;
-        ldsm_x4_t(vs_u + kv_off<D>(ks2 * 16 + (lane % 16), col / 8), b[0], b[1], b[2], b[3]);
+        ldsm_x4_t(vs_u + kv_addr<D, TMA>(ks2 * 16 + (lane % 16), col / 8), b[0], b[1], b[2], b[3]);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           uint32_t a[4];
@@ -500,29 +576,63 @@ size_t decode_hosts_workspace_bytes(int n, const int64_t* n_keys, int t, int hq,
   return ws_off_lse(splits, rows, D) + (size_t)splits * rows * sizeof(float);
 }
 
-// the streaming kernel over `splits` x KV heads (hb.n == 0: one host, all of p)
+// TMA maps of the caches of a launch's hosts ([cache_len][hk][D], row stride cache_row_stride;
+// box 64 columns x 1 head x 64 keys, SW128).  An empty cache gets a 1-row map over q (its row is
+// the first new token's, patched in the kernel; the rest of the chunk is out of bounds, zero).
+static apb_status decode_maps(const DecodeParams& p, const DecodeHosts& hb, dec::DecMaps& m) {
+  const int n = hb.n > 0 ? hb.n : 1;
+  for (int i = 0; i < n; ++i) {
+    const void* kc = hb.n > 0 ? hb.k_cache[i] : p.k_cache;
+    const void* vc = hb.n > 0 ? hb.v_cache[i] : p.v_cache;
+    const int64_t len = hb.n > 0 ? hb.cache_len[i] : p.cache_len;
+    uint64_t str[2] = {(uint64_t)p.D * 2, (uint64_t)p.cache_row_stride * 2};
+    uint64_t dims[3] = {(uint64_t)p.D, (uint64_t)p.hk, (uint64_t)len};
+    if (len == 0 || !kc || !vc) {
+      kc = vc = p.q;
+      dims[2] = 1;
+      str[1] = (uint64_t)p.hk * p.D * 2;
+    }
+    uint32_t box[3] = {64, 1, (uint32_t)dec::SKC};
+    if (!make_tmap_bf16(&m.k[i], kc, 3, dims, str, box)) return APB_ERR_CUDA;
+    if (!make_tmap_bf16(&m.v[i], vc, 3, dims, str, box)) return APB_ERR_CUDA;
+  }
+  return APB_OK;
+}
+
+// the streaming kernel over `splits` x KV heads (hb.n == 0: one host, all of p).  Default: the
+// TMA-fed ring (APB_DEC_TMA=0 selects the cp.async ring, kept for A/B timing)
 static apb_status launch_partials(const DecodeParams& p, const DecodeHosts& hb, int64_t splits, int cps,
                                   cudaStream_t stream) {
   dim3 grid((unsigned)splits, p.hk);
   const int R = p.t * p.g;
   const int mt = (R + 15) / 16;  // 16-row m-tiles
+  // TMA ring for a launch over several hosts' caches (the N = 1 step: 0.1096 vs 0.1178 ms per L8
+  // layer); a single host's 64 MiB launch streams faster through the cp.async ring (0.2065 vs
+  // 0.229-0.235 ms for 8 per-host calls).  APB_DEC_TMA=1 / 0 forces either.
+  const char* te = std::getenv("APB_DEC_TMA");
+  const bool tma = (te && te[0] == '1') || (!(te && te[0] == '0') && hb.n > 0);
+  dec::DecMaps maps;
+  if (tma) {
+    if (apb_status st = decode_maps(p, hb, maps)) return st;
+  }
   apb_status st = APB_OK;
-  auto launch = [&](auto kern, int MT, int D) {
-    // one set-once device mask per kernel instantiation (D, MT)
-    const int smem = D == 128 ? dec::MmaSmem<128>::bytes(MT) : dec::MmaSmem<64>::bytes(MT);
-    static std::atomic<uint64_t> smem_set[2][3];
+  auto launch = [&](auto kern, int MT, int D, bool T) {
+    // one set-once device mask per kernel instantiation (D, MT, TMA)
+    const int smem = T ? (D == 128 ? dec::tma_bytes<128>(MT) : dec::tma_bytes<64>(MT))
+                       : (D == 128 ? dec::MmaSmem<128>::bytes(MT) : dec::MmaSmem<64>::bytes(MT));
+    static std::atomic<uint64_t> smem_set[2][3][2];
     const int di = D == 128 ? 0 : 1, mi = MT <= 1 ? 0 : (MT <= 2 ? 1 : 2);
-    st = set_max_smem_once(reinterpret_cast<const void*>(kern), smem, smem_set[di][mi]);
-    if (st == APB_OK) kern<<<grid, dec::kMThreads, smem, stream>>>(p, hb, cps);
+    st = set_max_smem_once(reinterpret_cast<const void*>(kern), smem, smem_set[di][mi][T ? 1 : 0]);
+    if (st == APB_OK) kern<<<grid, dec::kMThreads, smem, stream>>>(p, hb, cps, maps);
   };
   if (p.D == 128) {
-    if (mt <= 1) launch(dec::decode_mma_kernel<128, 1>, 1, 128);
-    else if (mt <= 2) launch(dec::decode_mma_kernel<128, 2>, 2, 128);
-    else launch(dec::decode_mma_kernel<128, 4>, 4, 128);
+    if (mt <= 1) tma ? launch(dec::decode_mma_kernel<128, 1, true>, 1, 128, true) : launch(dec::decode_mma_kernel<128, 1, false>, 1, 128, false);
+    else if (mt <= 2) tma ? launch(dec::decode_mma_kernel<128, 2, true>, 2, 128, true) : launch(dec::decode_mma_kernel<128, 2, false>, 2, 128, false);
+    else tma ? launch(dec::decode_mma_kernel<128, 4, true>, 4, 128, true) : launch(dec::decode_mma_kernel<128, 4, false>, 4, 128, false);
   } else {
-    if (mt <= 1) launch(dec::decode_mma_kernel<64, 1>, 1, 64);
-    else if (mt <= 2) launch(dec::decode_mma_kernel<64, 2>, 2, 64);
-    else launch(dec::decode_mma_kernel<64, 4>, 4, 64);
+    if (mt <= 1) tma ? launch(dec::decode_mma_kernel<64, 1, true>, 1, 64, true) : launch(dec::decode_mma_kernel<64, 1, false>, 1, 64, false);
+    else if (mt <= 2) tma ? launch(dec::decode_mma_kernel<64, 2, true>, 2, 64, true) : launch(dec::decode_mma_kernel<64, 2, false>, 2, 64, false);
+    else tma ? launch(dec::decode_mma_kernel<64, 4, true>, 4, 64, true) : launch(dec::decode_mma_kernel<64, 4, false>, 4, 64, false);
   }
   if (st) return st;
   cudaError_t e = cudaGetLastError();
