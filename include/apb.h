@@ -310,7 +310,9 @@ apb_status apb_comm_abort(apb_comm* comm);
  * out: bf16 rows with out_row_stride elements (multiple of 8).  lse: NULL or [n_heads][L_A+l_b].
  * ws: APB_WS_ATTENTION bytes, shared by the LOCAL and PASSING calls of one layer.
  * Kernel: warp-specialised tcgen05 (TMEM accumulators, TMA loads, online softmax),
- * fully masked tiles never visited.                                                    */
+ * fully masked tiles never visited; persistent (one CTA per SM taking work items from a
+ * per-launch counter slot, 64 slots per device) for APB_PHASE_ALL / PASSING, so at most 64
+ * attention launches may run concurrently on one device (launches on one stream never do).  */
 apb_status apb_attention_fwd(const apb_dims* dims, const void* q, const void* k, const void* v,
                              int64_t q_row_stride, int64_t kv_row_stride, const void* gathered,
                              void* out, int64_t out_row_stride, float* lse, apb_phase phase,
