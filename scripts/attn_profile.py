@@ -126,6 +126,9 @@ def main():
         n_loc = (nB * g_ + 1) // 2 * cfg.hk
         n_anc = 0 if a.phase == "passing" else (nA * g_ + 1) // 2 * cfg.hk
         n = n_loc + n_anc
+        if os.environ.get("APB_ATTN_PERSIST", "")[:1] != "0" and os.environ.get("APB_ATTN_PAIR", "")[:1] != "1":
+            n = min(n, torch.cuda.get_device_properties(0).multi_processor_count)  # persistent CTAs
+            n_loc = min(n_loc, n)
         buf = (ctypes.c_ulonglong * (5 * n))()
         lib.apb_debug_cta_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.apb_debug_cta_times(buf, n)
@@ -147,14 +150,14 @@ def main():
             idx = np.where(sm == s_)[0]
             o = idx[np.argsort(st[idx])]
             gaps += list(st[o][1:] - en[o][:-1])
-        gaps = np.array(gaps)
+        gaps = np.array(gaps if gaps else [0])
         dur = en - st
         print(f"ctas {n} (local {n_loc}, anchor {n_anc}); span {span / 1e3:.1f} us; SM util {busy / (nsm * span):.3f}; "
               f"SM last-finish p10/p50/p90 {np.percentile(last, 10) / span:.3f}/{np.percentile(last, 50) / span:.3f}/"
               f"{np.percentile(last, 90) / span:.3f}; gap between CTAs on an SM mean {gaps.mean():.0f} ns "
               f"p90 {np.percentile(gaps, 90):.0f} ns; CTA us local mean {dur[:n_loc].mean() / 1e3:.1f} max "
               f"{dur[:n_loc].max() / 1e3:.1f} min {dur[:n_loc].min() / 1e3:.1f}"
-              + (f"; anchor mean {dur[n_loc:].mean() / 1e3:.1f}" if n_anc else ""))
+              + (f"; anchor mean {dur[n_loc:].mean() / 1e3:.1f}" if n_anc and n > n_loc else ""))
     if a.trace is not None:
         import numpy as np
         buf = (ctypes.c_ulonglong * 2048)()
