@@ -12,3 +12,5 @@ timeout -k 10 600 ncu --metrics gpu__time_duration.sum --clock-control none --cs
 timeout -k 10 900 ncu --set full --clock-control none --import-source on -k regex:apb_attention -c 1 -o gpurun_out/y_attn_full python bench.py --layers 1 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-breakdown > /dev/null 2>&1; echo "NCU3 $?"
 timeout -k 10 600 ncu --set full --clock-control none -k regex:"gemm_kernel|score_finalize|select|gather" -c 4 -o gpurun_out/y_aux_full python bench.py --layers 1 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-breakdown > /dev/null 2>&1; echo "NCU4 $?"
 for f in y_bench y_bench_model y_bench_d2; do python -c "import json;d=json.load(open('gpurun_out/$f.json'));print('$f',round(d['value']),d['roofline']['frac'],(d.get('e2e') or {}).get('value'),d['clocks'])"; done
+timeout -k 10 300 python scripts/decode_profile.py > gpurun_out/y_decode.json 2> gpurun_out/y_decode.err; echo "DECODE $?"; tail -1 gpurun_out/y_decode.json
+timeout -k 10 300 python scripts/decode_profile.py --per-host > gpurun_out/y_decode_ph.json 2> gpurun_out/y_decode_ph.err; echo "DECODE_PH $?"; tail -1 gpurun_out/y_decode_ph.json
