@@ -224,12 +224,14 @@ def test_retain_score_hosts_equals_per_host(name, tail, monkeypatch):
             assert torch.equal(sc[i], ref), (hs, h)
 
 
-@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3"])
+@pytest.mark.parametrize("name", ["toy", "d128-ragged", "gqa3", "big"])
 def test_select_topk_hosts_equals_per_host(name):
-    """apb_select_topk_hosts (one select launch over every host's KV heads, one gather launch)
-    gives the per-host indices and send slots bit for bit."""
+    """apb_select_topk_hosts (one select launch over every host's KV heads, one gather launch;
+    "big": l_b = 40000 > 32K, where each host runs the 8-CTA cluster kernel) gives the oracle's
+    indices and send slots bit for bit."""
     from paper_2502_12085_b200 import apb
-    cfg = CASES[name]
+    cfg = CASES[name] if name in CASES else synth.Config("big", 24, n=3 * 40000, H=3, l_a=64, l_p=2048, hq=8,
+                                                        hk=4, d=128, d_hidden=256)
     xs = [synth.host_qkv(cfg, 0, h) for h in range(cfg.H)]
     sc = [torch.from_numpy(np.ascontiguousarray(synth.random_scores(cfg, 0, h, ties=True), dtype=np.float32)).cuda()
           for h in range(cfg.H)]
