@@ -54,6 +54,14 @@ def test_binary_is_sm100a_with_tcgen05_and_tma(lib):
             assert "UTCHMMA" in body and not legacy, name
         elif legacy:
             assert "decode_mma_kernel" in name, name
+    # the decode streaming kernel's TMA instantiations (template flag true, mangled "Lb1E") read the
+    # caches with TMA into an mbarrier ring; the cp.async ones (Lb0E) do not
+    dec = [f for f in funcs if "decode_mma_kernel" in f.split("\n", 1)[0]]
+    tma = [f for f in dec if "Lb1E" in f.split("\n", 1)[0]]
+    assert tma and all("UTMALDG" in f and "SYNCS" in f for f in tma)
+    assert all("UTMALDG" not in f for f in dec if "Lb0E" in f.split("\n", 1)[0])
+    # the attention kernel stores its output tiles with TMA
+    assert any("UTMASTG" in f for f in funcs if "attention_kernel" in f.split("\n", 1)[0])
 
 
 def _dims(**kw):
