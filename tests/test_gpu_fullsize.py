@@ -17,9 +17,10 @@ oracle.attention_blas, pinned in tests/test_oracle.py):
              row boundary +-1, segment ends, random rows), all heads:
              max|dO| <= 2e-2, mean|dO| <= 2e-3, |d lse| <= 1e-2 (north_star)
 
-Also: the same layer under D3 (attention sink + planted needles, the retrieval structure of the
-paper's RULER / InfiniteBench workloads), the 32K config with EVERY row of every host, and the
-Qwen-2.5-14B and Yi-34B-200K configs (ordered schedule, fewer sampled rows).
+Also: the same layer under D2 (peaky logits, the bench's second line) and D3 (attention sink +
+planted needles, the retrieval structure of the paper's RULER / InfiniteBench workloads), the 32K
+config with EVERY row of every host, and the Qwen-2.5-14B and Yi-34B-200K configs (batched
+schedule, fewer sampled rows).
 Paper passages: Top-l_p and compaction P:177-180 (Alg. apb_prefill); masked attention
 eq:apb P:203-221.
 """
@@ -172,6 +173,13 @@ def test_llama8b_128k_d3_sink_needles():
     """The same layer under D3 (sink key + 16 needles x3 per block + shared query direction):
     peaked scores and softmax rows at full size, the bench's (batched) schedule."""
     _full_protocol(synth.CONFIGS["llama8b-128k"].replace(dist="D3"), n_crit=1536, n_other=384,
+                   schedules=("batched",))
+
+
+def test_llama8b_128k_d2_peaky():
+    """The bench's D2 line (Q, K ~ N(0, 4): logits with 4x D1's spread, the peaky case the lazy
+    rescale threshold was tuned on) at full size in the bench's batched schedule."""
+    _full_protocol(synth.CONFIGS["llama8b-128k"].replace(dist="D2"), n_crit=1024, n_other=256,
                    schedules=("batched",))
 
 
